@@ -1,0 +1,182 @@
+/*
+ * spheregrid_b200.h — flat C-ABI of the B200-native remap + halo-exchange hot path.
+ *
+ * This is the drop-in boundary for the `spheregrid` reference (Python, numpy/scipy,
+ * /root/reference/pkg/src/spheregrid).  The reference has no native binding for the hot
+ * path; its only binding layer is the TypeScript "FFI" in pkg/frontend, whose conventions
+ * this header follows:
+ *   - every call returns an int32 status: 0 ok, 1 domain error, 2 invalid handle,
+ *     3 invalid argument                            (frontend/src/errors.ts:7-16,
+ *                                                    SPEC.md capi StatusCode)
+ *   - sg_last_error() copies the calling thread's last message (SPEC.md capi
+ *     "Error text is copied into a caller-readable buffer per call context").  Domain
+ *     errors are prefixed with the reference exception class name, e.g.
+ *     "NotLocated: target point 17 not located ..." (errors.py:8-100), so a binding can
+ *     re-raise the reference class.
+ *   - opaque uint64 handles from a registry; never reused; double release -> status 2;
+ *     sg_registry_count() is the leak probe                (frontend/src/registry.ts:15-35)
+ *   - caller-owned host arrays cross as pointer + length and are copied on call; device
+ *     buffers are owned by library handles.  No torch / numpy types in any signature.
+ *
+ * Each entry point names the reference interface it replaces (file:line under
+ * /root/reference/pkg/src/spheregrid/).  Streams are cudaStream_t passed as uint64
+ * (0 = the legacy default stream).
+ */
+#ifndef SPHEREGRID_B200_H
+#define SPHEREGRID_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SG_OK 0
+#define SG_DOMAIN_ERROR 1
+#define SG_INVALID_HANDLE 2
+#define SG_INVALID_ARGUMENT 3
+
+/* ---- runtime / registry (frontend/src/registry.ts:15-35, errors.ts:7-16) ---------------- */
+int32_t sg_version(char* buf, size_t n);
+int32_t sg_last_error(char* buf, size_t n);
+int32_t sg_registry_count(int64_t* out_live);
+int32_t sg_release(uint64_t handle);
+int32_t sg_device_count(int32_t* out_count);
+int32_t sg_stream_synchronize(int32_t device, uint64_t stream);
+
+/* ---- Field device mirror (field.py:77-162) ---------------------------------------------
+ * Device storage of a (npts, levels) Field: one pitched allocation, levels contiguous per
+ * point (the reference host layout, field.py:161), row pitch padded to 128 B (or to the
+ * next power of two for rows < 128 B) so 16-B vector loads and bulk copies are aligned.
+ * Padding is zero-filled at allocation.
+ *   sg_field_alloc  <- Field.allocate_device        (field.py:99-105)
+ *   sg_field_h2d    <- Field.update_device           (field.py:134-140)   host rows unpadded
+ *   sg_field_d2h    <- Field.update_host             (field.py:126-132)
+ *   sg_field_h2d_rows / sg_field_d2h_rows: the same for a contiguous row range.           */
+int32_t sg_field_alloc(int32_t device, int64_t npts, int32_t levels, int32_t itemsize,
+                       uint64_t* out_field, int64_t* out_pitch_elems, uint64_t* out_devptr);
+int32_t sg_field_h2d(uint64_t field, const void* host, uint64_t stream);
+int32_t sg_field_d2h(uint64_t field, void* host, uint64_t stream);
+int32_t sg_field_h2d_rows(uint64_t field, int64_t row0, int64_t nrows, const void* host,
+                          uint64_t stream);
+int32_t sg_field_d2h_rows(uint64_t field, int64_t row0, int64_t nrows, void* host,
+                          uint64_t stream);
+/* pinned host buffers (cudaHostAlloc) for asynchronous, full-rate h2d/d2h, and CUDA events
+ * for timing on the launching stream. */
+int32_t sg_host_alloc(size_t bytes, uint64_t* out_ptr);
+int32_t sg_host_free(uint64_t ptr);
+int32_t sg_event_create(int32_t device, uint64_t* out_event);
+int32_t sg_event_record(uint64_t event, uint64_t stream);
+int32_t sg_event_elapsed_ms(uint64_t start, uint64_t end, float* out_ms);
+int32_t sg_field_info(uint64_t field, int32_t* out_device, int64_t* out_npts,
+                      int32_t* out_levels, int64_t* out_pitch_elems, uint64_t* out_devptr);
+
+/* ---- stencil search + weights (interp.py:74-117 MeshLocator, interp.py:154-203) ---------
+ * sg_locator_create <- MeshLocator.__init__ (interp.py:79-88): uploads node xyz (n,3) f64
+ *   and the element CSR (mesh.py:310-319), splits quads at the lowest local index
+ *   (mesh.py:395-403), and builds a latitude-band / longitude-bin search structure on the
+ *   device (the B200 replacement for the cKDTree + incidence lists).
+ * sg_locator_locate <- MeshLocator.locate (interp.py:102-117), batched: per point the
+ *   element id, the local corner triple, or -1 (NotLocated).  Winner = max over containing
+ *   triangles (score = min of the three signed tests >= -CONTAIN_EPS) of the score; exact
+ *   ties -> lowest local element id, then triangle index.
+ * sg_remap_build <- build_remap (interp.py:154-203): locate + gnomonic barycentric weights
+ *   (interp.py:61-71) + scale (interp.py:194) + optional nearest-node fallback
+ *   (interp.py:179-190).  Returns a device stencil handle for sg_remap_apply and copies the
+ *   InterpolationWeights arrays (interp.py:120-133) to the caller's host buffers.
+ *   out_status[k]: 0 located, 1 not located (fallback row if allow_fallback),
+ *   2 degenerate candidate triangle, 3 singular / zero-sum weights.
+ *   On status SG_DOMAIN_ERROR *out_first_bad is the first (ascending) offending row and
+ *   the message carries the reference exception class (NotLocated / DegenerateTriangle).
+ * sg_stencil_create: device stencil from host arrays (an InterpolationWeights built
+ *   elsewhere, e.g. the reference's own build_remap output).                               */
+int32_t sg_locator_create(int32_t device, const double* node_xyz, int64_t n_nodes,
+                          const int64_t* elem_offsets, const int64_t* elem_indices,
+                          int64_t n_elems, uint64_t* out_locator);
+int32_t sg_locator_stats(uint64_t locator, int64_t* out_ntri, int64_t* out_nbins,
+                         int64_t* out_nentries, double* out_band_rad);
+int32_t sg_locator_locate(uint64_t locator, const double* points, int64_t m,
+                          int64_t* out_elem, int64_t* out_corners);
+int32_t sg_remap_build(uint64_t locator, const double* target_xyz, int64_t m,
+                       int64_t source_nnodes, int32_t allow_fallback, uint64_t* out_stencil,
+                       int64_t* out_nodes, double* out_weights, double* out_scale,
+                       uint8_t* out_fallback, uint8_t* out_status, int64_t* out_first_bad);
+int32_t sg_stencil_create(int32_t device, const int64_t* nodes, const double* weights,
+                          int64_t m, int64_t source_nnodes, uint64_t* out_stencil);
+int32_t sg_stencil_info(uint64_t stencil, int64_t* out_m, int64_t* out_source_nnodes,
+                        int64_t* out_distinct_sources);
+
+/* ---- apply (interp.py:206-228 apply_remap) ------------------------------------------------
+ * dst[t, :] = (w0*src[n0, :] + w1*src[n1, :]) + w2*src[n2, :], every product and sum
+ * rounded separately (bitwise equal to the numpy expression at interp.py:219-223), for
+ * nfields source/target field pairs sharing the stencil.  ShapeMismatch (status 1) with
+ * the reference messages when npts / levels disagree (interp.py:208-217).
+ * variant: 0 = default, 1 = warp-per-target LDG.128 gather, 2 = TMA bulk-copy
+ * (cp.async.bulk) staged gather.                                                            */
+int32_t sg_remap_apply(uint64_t stencil, const uint64_t* src_fields,
+                       const uint64_t* dst_fields, int32_t nfields, int32_t variant,
+                       uint64_t stream);
+
+/* ---- halo exchange (functionspace.py:58-118) ---------------------------------------------
+ * sg_halo_plan_create <- HaloExchangePlan (functionspace.py:47-55): per peer (ascending),
+ *   the owned rows sent (owner-local, requester order, functionspace.py:82-93), the ghost
+ *   rows received (local, (halo, gidx) order, functionspace.py:66-72) and, for the ghost
+ *   rows, their index on the owner (mesh.py:303-308 node_remote).
+ * sg_halo_pack   <- the send loop (functionspace.py:113-114): writes every peer's payload
+ *   into one device buffer, peers ascending, each payload (n_send, L) C-order — byte-equal
+ *   to f.host[send[peer]].tobytes().
+ * sg_halo_unpack <- the receive loop (functionspace.py:115-117).
+ * sg_halo_pull: fused pack + transfer + unpack over peer memory: ghost rows are read
+ *   straight from each owner's device field (same device, NVLink P2P in one process, or a
+ *   CUDA-IPC mapping) — one kernel, no staging.  peer_ptrs/peer_pitch indexed by plan peer.
+ * sg_halo_exchange_nccl: pack -> grouped ncclSend/ncclRecv per peer -> unpack on one
+ *   stream (NCCL loaded lazily with dlopen).                                                */
+int32_t sg_halo_plan_create(int32_t device, int64_t nnodes, int32_t npeers,
+                            const int32_t* peers, const int64_t* send_counts,
+                            const int64_t* send_rows, const int64_t* recv_counts,
+                            const int64_t* recv_rows, const int64_t* recv_remote_rows,
+                            uint64_t* out_plan);
+int32_t sg_halo_plan_info(uint64_t plan, int64_t* out_nsend, int64_t* out_nrecv);
+int32_t sg_halo_pack(uint64_t plan, uint64_t field, void* dev_sendbuf, uint64_t stream);
+int32_t sg_halo_unpack(uint64_t plan, uint64_t field, const void* dev_recvbuf,
+                       uint64_t stream);
+int32_t sg_halo_pull(uint64_t plan, uint64_t field, const uint64_t* peer_ptrs,
+                     const int64_t* peer_pitch_elems, uint64_t stream);
+
+int32_t sg_nccl_unique_id(uint8_t* out_id, size_t n);
+int32_t sg_comm_create(int32_t device, int32_t nranks, int32_t rank, const uint8_t* id,
+                       size_t n, uint64_t* out_comm);
+int32_t sg_halo_exchange_nccl(uint64_t plan, uint64_t field, uint64_t comm,
+                              uint64_t stream);
+
+/* CUDA IPC for the multi-process pull path (one process per GPU). */
+int32_t sg_ipc_handle(uint64_t field, uint8_t* out_handle, size_t n);
+int32_t sg_ipc_open(int32_t device, const uint8_t* handle, size_t n, uint64_t* out_ptr);
+int32_t sg_ipc_close(int32_t device, uint64_t ptr);
+
+/* ---- host-side setup, native -------------------------------------
+ * sg_meshgen_create <- generate_mesh (mesh.py:229-338) minus coordinates: serial strip-merge
+ *   topology (mesh.py:142-215), element halo levels + BFS (mesh.py:247-278), local node
+ *   numbering (mesh.py:280-308) and local connectivity (mesh.py:310-319).  Results stay in
+ *   the handle; sg_meshgen_fetch copies them out.
+ * sg_matching_partition <- PointCloudIndex.query + matching_partition (partition.py:53-88):
+ *   nearest master grid point with the 1e-12 relative tie window resolved to the smallest
+ *   global index, using the master grid's row structure instead of a kd-tree.               */
+int32_t sg_meshgen_create(int32_t nrows, const int64_t* nlons, int32_t include_pole,
+                          const int32_t* part_of, int64_t npts, int32_t nparts, int32_t part,
+                          int32_t halo, uint64_t* out_mesh, int64_t* out_nnodes,
+                          int64_t* out_nowned, int64_t* out_nelems, int64_t* out_nindices);
+int32_t sg_meshgen_fetch(uint64_t mesh, int64_t* node_global, int32_t* node_part,
+                         int64_t* node_remote, uint8_t* node_ghost, int16_t* node_halo,
+                         int64_t* elem_offsets, int64_t* elem_indices, int16_t* elem_halo,
+                         int64_t* elem_serial_id);
+int32_t sg_matching_partition(int32_t nrows, const double* master_lat_deg,
+                              const int64_t* master_nlons, const double* master_xyz,
+                              const double* target_xyz, int64_t m, int32_t nthreads,
+                              int64_t* out_index);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPHEREGRID_B200_H */

@@ -1,0 +1,147 @@
+/*
+ * ORACLE — TEST INFRASTRUCTURE ONLY.  Never linked into or called by the product
+ * (paper_1908_07038_b200/); only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline leg may load it, and only as the checker.
+ *
+ * Plain-C restatement of the reference's MeshLocator.locate
+ * (/root/reference/pkg/src/spheregrid/interp.py:74-117), candidate order and all:
+ *   - k nearest mesh nodes of p, k = 8 then 32 (interp.py:30-31, 106), exact brute force,
+ *     ordered by squared distance then node index (cKDTree.query order, interp.py:92);
+ *   - candidate elements = incident elements of those nodes in ascending element id, first
+ *     seen first (interp.py:82-85, 94-100);
+ *   - per element its triangles (quads split at the lowest local index, mesh.py:395-403);
+ *   - SphericalTriangle raises DegenerateTriangle when |(a x b).c| <= 1e-15 (interp.py:40-43);
+ *   - score = min of the signed tests (a x b).p, (b x c).p, (c x a).p (interp.py:46-51) with
+ *     np.cross as unfused mul/sub and np.dot as OpenBLAS ddot = fma(c2,p2,fma(c1,p1,c0*p0))
+ *     (re-probed on the GPU-box host: tools/host_probe.py);
+ *   - keep if score >= -1e-12 and strictly greater than the best so far (interp.py:113).
+ * Built with -ffp-contract=off so the compiler cannot fuse the restated arithmetic.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+  double x, y, z;
+} v3;
+
+static v3 ld(const double* xyz, int64_t i) {
+  v3 r = {xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]};
+  return r;
+}
+static v3 cross_np(v3 a, v3 b) {
+  v3 r;
+  r.x = a.y * b.z - a.z * b.y;
+  r.y = a.z * b.x - a.x * b.z;
+  r.z = a.x * b.y - a.y * b.x;
+  return r;
+}
+static double dot_blas(v3 c, v3 p) { return fma(c.z, p.z, fma(c.y, p.y, c.x * p.x)); }
+
+/* split quads / copy triangles; returns number of triangles written (1 or 2) */
+static int element_tris(const int64_t* off, const int64_t* idx, int64_t e, int64_t out[2][3]) {
+  int64_t k = off[e + 1] - off[e];
+  const int64_t* r = idx + off[e];
+  if (k == 3) {
+    out[0][0] = r[0]; out[0][1] = r[1]; out[0][2] = r[2];
+    return 1;
+  }
+  int m = 0;
+  for (int i = 1; i < 4; ++i)
+    if (r[i] < r[m]) m = i;
+  int64_t c[4];
+  for (int i = 0; i < 4; ++i) c[i] = r[(m + i) % 4];
+  out[0][0] = c[0]; out[0][1] = c[1]; out[0][2] = c[2];
+  out[1][0] = c[0]; out[1][1] = c[2]; out[1][2] = c[3];
+  return 2;
+}
+
+/*
+ * For each point: out_elem (-1 not located, -2 DegenerateTriangle), out_corners (3 local ids).
+ */
+int oracle_locate(const double* xyz, int64_t n, const int64_t* off, const int64_t* idx, int64_t nelem,
+                  const double* pts, int64_t m, int64_t* out_elem, int64_t* out_corners) {
+  /* incidence lists in ascending element id */
+  int64_t* cnt = calloc((size_t)n + 1, sizeof(int64_t));
+  for (int64_t e = 0; e < nelem; ++e)
+    for (int64_t i = off[e]; i < off[e + 1]; ++i) cnt[idx[i] + 1]++;
+  for (int64_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
+  int64_t* inc = malloc(sizeof(int64_t) * (size_t)(cnt[n] > 0 ? cnt[n] : 1));
+  int64_t* fill = malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  memcpy(fill, cnt, sizeof(int64_t) * (size_t)n);
+  for (int64_t e = 0; e < nelem; ++e)
+    for (int64_t i = off[e]; i < off[e + 1]; ++i) inc[fill[idx[i]]++] = e;
+  unsigned char* seen = calloc((size_t)(nelem > 0 ? nelem : 1), 1);
+  int64_t* cand = malloc(sizeof(int64_t) * (size_t)(nelem > 0 ? nelem : 1));
+  for (int64_t t = 0; t < m; ++t) {
+    v3 p = ld(pts, t);
+    out_elem[t] = -1;
+    const int ks[2] = {8, 32};
+    int done = 0;
+    for (int pass = 0; pass < 2 && !done; ++pass) {
+      int k = ks[pass] < n ? ks[pass] : (int)n;
+      double bd[32];
+      int64_t bi[32];
+      int nb = 0;
+      for (int64_t i = 0; i < n; ++i) {
+        double dx = xyz[3 * i] - p.x, dy = xyz[3 * i + 1] - p.y, dz = xyz[3 * i + 2] - p.z;
+        double d = dx * dx + dy * dy + dz * dz;
+        if (nb < k || d < bd[nb - 1]) {
+          int j = nb < k ? nb++ : nb - 1;
+          while (j > 0 && bd[j - 1] > d) {
+            bd[j] = bd[j - 1];
+            bi[j] = bi[j - 1];
+            --j;
+          }
+          bd[j] = d;
+          bi[j] = i;
+        }
+      }
+      int64_t nc = 0;
+      for (int a = 0; a < nb; ++a)
+        for (int64_t q = cnt[bi[a]]; q < cnt[bi[a] + 1]; ++q) {
+          int64_t e = inc[q];
+          if (!seen[e]) {
+            seen[e] = 1;
+            cand[nc++] = e;
+          }
+        }
+      int have = 0;
+      double best = 0.0;
+      for (int64_t c = 0; c < nc && out_elem[t] != -2; ++c) {
+        int64_t tr[2][3];
+        int nt = element_tris(off, idx, cand[c], tr);
+        for (int s = 0; s < nt; ++s) {
+          v3 a = ld(xyz, tr[s][0]), b = ld(xyz, tr[s][1]), cc = ld(xyz, tr[s][2]);
+          v3 ab = cross_np(a, b);
+          if (fabs(dot_blas(ab, cc)) <= 1e-15) {
+            out_elem[t] = -2;
+            break;
+          }
+          double t1 = dot_blas(ab, p), t2 = dot_blas(cross_np(b, cc), p), t3 = dot_blas(cross_np(cc, a), p);
+          double score = t1;
+          if (t2 < score) score = t2;
+          if (t3 < score) score = t3;
+          if (score >= -1e-12 && (!have || score > best)) {
+            have = 1;
+            best = score;
+            out_elem[t] = cand[c];
+            out_corners[3 * t] = tr[s][0];
+            out_corners[3 * t + 1] = tr[s][1];
+            out_corners[3 * t + 2] = tr[s][2];
+          }
+        }
+      }
+      for (int64_t c = 0; c < nc; ++c) seen[cand[c]] = 0;
+      if (have || out_elem[t] == -2) done = 1;
+    }
+    if (out_elem[t] == -1) out_corners[3 * t] = out_corners[3 * t + 1] = out_corners[3 * t + 2] = -1;
+  }
+  free(cnt);
+  free(inc);
+  free(fill);
+  free(seen);
+  free(cand);
+  return 0;
+}

@@ -1,0 +1,174 @@
+// Device mirror of a reference Field (field.py:77-162): pitched, level-contiguous rows.
+// h2d/d2h move the unpadded host (npts, levels) C-order array (field.py:161) with one
+// cudaMemcpy2DAsync each, so the host layout the reference exposes is unchanged.
+#include <algorithm>
+
+#include "cuda_util.cuh"
+
+using namespace sg;
+
+extern "C" {
+
+int32_t sg_device_count(int32_t* out_count) {
+  SG_API_BEGIN
+  SG_REQUIRE(out_count, "null out pointer");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  *out_count = n;
+  SG_API_END
+}
+
+int32_t sg_stream_synchronize(int32_t device, uint64_t stream) {
+  SG_API_BEGIN
+  DeviceScope ds(device);
+  SG_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  SG_API_END
+}
+
+int32_t sg_field_alloc(int32_t device, int64_t npts, int32_t levels, int32_t itemsize,
+                       uint64_t* out_field, int64_t* out_pitch_elems, uint64_t* out_devptr) {
+  SG_API_BEGIN
+  SG_REQUIRE(out_field, "null out pointer");
+  SG_REQUIRE(npts >= 0 && levels >= 1, "bad field shape (%lld, %d)", (long long)npts, levels);
+  SG_REQUIRE(itemsize == 4 || itemsize == 8, "itemsize must be 4 or 8");
+  DeviceScope ds(device);
+  auto f = std::make_unique<Field>();
+  f->device = device;
+  f->npts = npts;
+  f->levels = levels;
+  f->itemsize = itemsize;
+  f->pitch = field_pitch_elems(levels, itemsize);
+  size_t bytes = (size_t)std::max<int64_t>(npts, 1) * f->pitch * itemsize;
+  f->buf.alloc(device, bytes);
+  SG_CUDA(cudaMemset(f->buf.ptr, 0, bytes));
+  if (out_pitch_elems) *out_pitch_elems = f->pitch;
+  if (out_devptr) *out_devptr = reinterpret_cast<uint64_t>(f->buf.ptr);
+  *out_field = registry_put(f.release());
+  SG_API_END
+}
+
+int32_t sg_field_info(uint64_t field, int32_t* out_device, int64_t* out_npts, int32_t* out_levels,
+                      int64_t* out_pitch_elems, uint64_t* out_devptr) {
+  SG_API_BEGIN
+  Field* f = get<Field>(field, ObjKind::Field);
+  if (out_device) *out_device = f->device;
+  if (out_npts) *out_npts = f->npts;
+  if (out_levels) *out_levels = f->levels;
+  if (out_pitch_elems) *out_pitch_elems = f->pitch;
+  if (out_devptr) *out_devptr = reinterpret_cast<uint64_t>(f->buf.ptr);
+  SG_API_END
+}
+
+static void copy_rows(Field* f, int64_t row0, int64_t nrows, const void* src_host, void* dst_host,
+                      uint64_t stream) {
+  SG_REQUIRE(row0 >= 0 && nrows >= 0 && row0 + nrows <= f->npts, "row range [%lld, %lld) outside [0, %lld)",
+             (long long)row0, (long long)(row0 + nrows), (long long)f->npts);
+  if (nrows == 0) return;
+  DeviceScope ds(f->device);
+  size_t row_bytes = (size_t)f->levels * f->itemsize;
+  size_t pitch_bytes = (size_t)f->pitch * f->itemsize;
+  char* dev = f->buf.as<char>() + (size_t)row0 * pitch_bytes;
+  if (src_host) {
+    SG_CUDA(cudaMemcpy2DAsync(dev, pitch_bytes, src_host, row_bytes, row_bytes, (size_t)nrows,
+                              cudaMemcpyHostToDevice, as_stream(stream)));
+  } else {
+    SG_CUDA(cudaMemcpy2DAsync(dst_host, row_bytes, dev, pitch_bytes, row_bytes, (size_t)nrows,
+                              cudaMemcpyDeviceToHost, as_stream(stream)));
+  }
+}
+
+int32_t sg_field_h2d(uint64_t field, const void* host, uint64_t stream) {
+  SG_API_BEGIN
+  Field* f = get<Field>(field, ObjKind::Field);
+  SG_REQUIRE(host || f->npts == 0, "null host pointer");
+  copy_rows(f, 0, f->npts, host, nullptr, stream);
+  SG_API_END
+}
+
+int32_t sg_field_d2h(uint64_t field, void* host, uint64_t stream) {
+  SG_API_BEGIN
+  Field* f = get<Field>(field, ObjKind::Field);
+  SG_REQUIRE(host || f->npts == 0, "null host pointer");
+  copy_rows(f, 0, f->npts, nullptr, host, stream);
+  SG_API_END
+}
+
+int32_t sg_field_h2d_rows(uint64_t field, int64_t row0, int64_t nrows, const void* host,
+                          uint64_t stream) {
+  SG_API_BEGIN
+  Field* f = get<Field>(field, ObjKind::Field);
+  SG_REQUIRE(host || nrows == 0, "null host pointer");
+  copy_rows(f, row0, nrows, host, nullptr, stream);
+  SG_API_END
+}
+
+int32_t sg_field_d2h_rows(uint64_t field, int64_t row0, int64_t nrows, void* host, uint64_t stream) {
+  SG_API_BEGIN
+  Field* f = get<Field>(field, ObjKind::Field);
+  SG_REQUIRE(host || nrows == 0, "null host pointer");
+  copy_rows(f, row0, nrows, nullptr, host, stream);
+  SG_API_END
+}
+
+// ---- pinned host memory and device events (timing on the launching stream) ----------------
+namespace {
+struct Event : Object {
+  Event() : Object(ObjKind::Event) {}
+  int device = 0;
+  cudaEvent_t ev = nullptr;
+  ~Event() override {
+    if (ev) cudaEventDestroy(ev);
+  }
+};
+}  // namespace
+
+int32_t sg_host_alloc(size_t bytes, uint64_t* out_ptr) {
+  SG_API_BEGIN
+  SG_REQUIRE(out_ptr, "null out pointer");
+  void* p = nullptr;
+  SG_CUDA(cudaHostAlloc(&p, std::max<size_t>(bytes, 1), cudaHostAllocPortable));
+  *out_ptr = reinterpret_cast<uint64_t>(p);
+  SG_API_END
+}
+
+int32_t sg_host_free(uint64_t ptr) {
+  SG_API_BEGIN
+  SG_CUDA(cudaFreeHost(reinterpret_cast<void*>(ptr)));
+  SG_API_END
+}
+
+int32_t sg_event_create(int32_t device, uint64_t* out_event) {
+  SG_API_BEGIN
+  SG_REQUIRE(out_event, "null out pointer");
+  DeviceScope ds(device);
+  auto e = std::make_unique<Event>();
+  e->device = device;
+  SG_CUDA(cudaEventCreate(&e->ev));
+  *out_event = registry_put(e.release());
+  SG_API_END
+}
+
+int32_t sg_event_record(uint64_t event, uint64_t stream) {
+  SG_API_BEGIN
+  Event* e = get<Event>(event, ObjKind::Event);
+  DeviceScope ds(e->device);
+  SG_CUDA(cudaEventRecord(e->ev, as_stream(stream)));
+  SG_API_END
+}
+
+int32_t sg_event_elapsed_ms(uint64_t start, uint64_t end, float* out_ms) {
+  SG_API_BEGIN
+  Event* a = get<Event>(start, ObjKind::Event);
+  Event* b = get<Event>(end, ObjKind::Event);
+  SG_REQUIRE(out_ms, "null out pointer");
+  DeviceScope ds(b->device);
+  SG_CUDA(cudaEventSynchronize(b->ev));
+  SG_CUDA(cudaEventElapsedTime(out_ms, a->ev, b->ev));
+  SG_API_END
+}
+
+}  // extern "C"

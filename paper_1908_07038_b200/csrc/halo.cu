@@ -1,0 +1,377 @@
+// NodeColumns halo exchange on the device (functionspace.py:58-118).
+//
+// Plan (functionspace.py:47-55): peers ascending; per peer the owned rows to send in the
+// requester's order (functionspace.py:82-93), the ghost rows to receive in local
+// (halo, gidx) order (functionspace.py:66-72), and each ghost's row on its owner
+// (mesh.py:303-308, node_remote == the owner's send entry for it).
+//
+// Kernels (one warp per row, lanes over the row's 32-bit words; every field kind shares them):
+//   pack   — every peer's payload into one device buffer, peers ascending, (n, L) C-order:
+//            byte-equal to f.host[send[peer]].tobytes() (functionspace.py:113-114)
+//   unpack — receive buffer into the ghost rows (functionspace.py:115-117)
+//   pull   — fused pack+transfer+unpack: each ghost row is read straight from its owner's
+//            field through a peer pointer (same device, NVLink P2P, or a CUDA-IPC mapping).
+// The NCCL path groups one ncclSend + ncclRecv per peer between pack and unpack on one
+// stream.  NCCL is dlopen'ed on first use so the library never pins a libnccl version into
+// a process that also loads torch's.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <mutex>
+#include <numeric>
+#include <vector>
+
+#include "cuda_util.cuh"
+
+namespace sg {
+namespace {
+
+constexpr int kMaxPeers = 64;
+
+struct Plan : Object {
+  Plan() : Object(ObjKind::Plan) {}
+  int device = 0;
+  int64_t nnodes = 0;
+  std::vector<int32_t> peers;
+  std::vector<int64_t> send_off, recv_off;  // per peer, npeers+1
+  DevBuf send_rows, recv_rows, recv_remote;  // int32
+  DevBuf recv_peer;                          // int32 plan-peer slot of every ghost row
+  DevBuf sendbuf, recvbuf;                   // NCCL staging (lazily sized)
+};
+
+// Rows are moved as 32-bit words so every field kind (4- or 8-byte) shares the kernels:
+// W words per row, pitches in words.
+__global__ void pack_rows(const uint32_t* __restrict__ f, int64_t pitch_w, int W,
+                          const int32_t* __restrict__ rows, int64_t n, uint32_t* __restrict__ out) {
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  const uint32_t* src = f + (int64_t)rows[r] * pitch_w;
+  uint32_t* dst = out + r * W;
+  for (int l = lane; l < W; l += 32) dst[l] = src[l];
+}
+
+__global__ void unpack_rows(uint32_t* __restrict__ f, int64_t pitch_w, int W,
+                            const int32_t* __restrict__ rows, int64_t n, const uint32_t* __restrict__ in) {
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  uint32_t* dst = f + (int64_t)rows[r] * pitch_w;
+  const uint32_t* src = in + r * W;
+  for (int l = lane; l < W; l += 32) dst[l] = src[l];
+}
+
+struct PeerPtrs {
+  const uint32_t* base[kMaxPeers];
+  int64_t pitch_w[kMaxPeers];
+};
+
+// Fused exchange: ghost row k (peer slot s) <- the owner's row recv_remote[k], read through a
+// peer pointer.  VEC: 16-B moves (rows padded to 16 B on both sides).
+template <bool VEC>
+__global__ void pull_rows(uint32_t* __restrict__ f, int64_t pitch_w, int W,
+                          const int32_t* __restrict__ rows, const int32_t* __restrict__ remote,
+                          const int32_t* __restrict__ slot, int64_t n, PeerPtrs peers) {
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  const int s = slot[r];
+  const uint32_t* src = peers.base[s] + (int64_t)remote[r] * peers.pitch_w[s];
+  uint32_t* dst = f + (int64_t)rows[r] * pitch_w;
+  if (VEC) {
+    const int nv = (W + 3) >> 2;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (int k = lane; k < nv; k += 32) d4[k] = s4[k];
+  } else {
+    for (int l = lane; l < W; l += 32) dst[l] = src[l];
+  }
+}
+
+inline unsigned warps_grid(int64_t n) { return (unsigned)((n + 7) / 8); }
+
+// ---- NCCL, loaded lazily --------------------------------------------------------------------
+typedef int ncclResult_t;
+typedef struct ncclComm* ncclComm_t;
+struct ncclUniqueId {
+  char internal[128];
+};
+enum { ncclUint32 = 3 };
+struct Nccl {
+  void* lib = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+std::mutex g_nccl_mu;
+Nccl g_nccl;
+
+Nccl& nccl() {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  if (!g_nccl.lib) {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw_error(SG_DOMAIN_ERROR, "NcclUnavailable: cannot dlopen libnccl.so.2: %s", dlerror());
+#define SG_NCCL_SYM(field, name)                                                   \
+  g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name));         \
+  if (!g_nccl.field) throw_error(SG_DOMAIN_ERROR, "NcclUnavailable: missing %s", name);
+    SG_NCCL_SYM(GetUniqueId, "ncclGetUniqueId");
+    SG_NCCL_SYM(CommInitRank, "ncclCommInitRank");
+    SG_NCCL_SYM(CommDestroy, "ncclCommDestroy");
+    SG_NCCL_SYM(GroupStart, "ncclGroupStart");
+    SG_NCCL_SYM(GroupEnd, "ncclGroupEnd");
+    SG_NCCL_SYM(Send, "ncclSend");
+    SG_NCCL_SYM(Recv, "ncclRecv");
+    SG_NCCL_SYM(GetErrorString, "ncclGetErrorString");
+#undef SG_NCCL_SYM
+    g_nccl.lib = h;
+  }
+  return g_nccl;
+}
+
+#define SG_NCCL(call)                                                                         \
+  do {                                                                                        \
+    ncclResult_t _r = (call);                                                                 \
+    if (_r != 0) throw_error(SG_DOMAIN_ERROR, "NcclError: %s failed: %s", #call,              \
+                             nccl().GetErrorString(_r));                                      \
+  } while (0)
+
+struct Comm : Object {
+  Comm() : Object(ObjKind::Comm) {}
+  int device = 0, nranks = 0, rank = 0;
+  ncclComm_t comm = nullptr;
+  ~Comm() override {
+    if (comm) nccl().CommDestroy(comm);
+  }
+};
+
+inline int64_t pitch_words(const Field* f) { return f->pitch * f->itemsize / 4; }
+inline int row_words(const Field* f) { return (int)((int64_t)f->levels * f->itemsize / 4); }
+
+void check_field(const Plan* p, const Field* f) {
+  if (f->npts != p->nnodes)
+    throw_error(SG_DOMAIN_ERROR, "PlanMismatch: field has %lld points, plan covers %lld nodes",
+                (long long)f->npts, (long long)p->nnodes);
+  SG_REQUIRE(f->device == p->device, "field and plan live on different devices");
+}
+
+void upload_i32(DevBuf& b, int dev, const std::vector<int32_t>& v) {
+  b.alloc(dev, std::max<size_t>(v.size(), 1) * 4);
+  if (!v.empty()) SG_CUDA(cudaMemcpy(b.ptr, v.data(), v.size() * 4, cudaMemcpyHostToDevice));
+}
+
+}  // namespace
+}  // namespace sg
+
+using namespace sg;
+
+extern "C" {
+
+int32_t sg_halo_plan_create(int32_t device, int64_t nnodes, int32_t npeers, const int32_t* peers,
+                            const int64_t* send_counts, const int64_t* send_rows, const int64_t* recv_counts,
+                            const int64_t* recv_rows, const int64_t* recv_remote_rows, uint64_t* out_plan) {
+  SG_API_BEGIN
+  SG_REQUIRE(out_plan, "null out pointer");
+  SG_REQUIRE(npeers >= 0 && npeers <= kMaxPeers, "npeers %d outside [0, %d]", npeers, kMaxPeers);
+  SG_REQUIRE(nnodes >= 0 && nnodes < INT32_MAX, "bad nnodes");
+  auto p = std::make_unique<Plan>();
+  p->device = device;
+  p->nnodes = nnodes;
+  p->send_off.assign(npeers + 1, 0);
+  p->recv_off.assign(npeers + 1, 0);
+  std::vector<int32_t> srows, rrows, rremote, rslot;
+  for (int i = 0; i < npeers; ++i) {
+    SG_REQUIRE(i == 0 || peers[i] > peers[i - 1], "peers must be strictly ascending");
+    p->peers.push_back(peers[i]);
+    p->send_off[i + 1] = p->send_off[i] + send_counts[i];
+    p->recv_off[i + 1] = p->recv_off[i] + recv_counts[i];
+  }
+  const int64_t ns = p->send_off[npeers], nr = p->recv_off[npeers];
+  for (int64_t k = 0; k < ns; ++k) {
+    SG_REQUIRE(send_rows[k] >= 0 && send_rows[k] < nnodes, "send row %lld out of range", (long long)send_rows[k]);
+    srows.push_back((int32_t)send_rows[k]);
+  }
+  for (int i = 0; i < npeers; ++i)
+    for (int64_t k = p->recv_off[i]; k < p->recv_off[i + 1]; ++k) {
+      SG_REQUIRE(recv_rows[k] >= 0 && recv_rows[k] < nnodes, "recv row %lld out of range", (long long)recv_rows[k]);
+      rrows.push_back((int32_t)recv_rows[k]);
+      rremote.push_back(recv_remote_rows ? (int32_t)recv_remote_rows[k] : -1);
+      rslot.push_back(i);
+    }
+  DeviceScope ds(device);
+  upload_i32(p->send_rows, device, srows);
+  upload_i32(p->recv_rows, device, rrows);
+  upload_i32(p->recv_remote, device, rremote);
+  upload_i32(p->recv_peer, device, rslot);
+  *out_plan = registry_put(p.release());
+  SG_API_END
+}
+
+int32_t sg_halo_plan_info(uint64_t plan, int64_t* out_nsend, int64_t* out_nrecv) {
+  SG_API_BEGIN
+  Plan* p = get<Plan>(plan, ObjKind::Plan);
+  if (out_nsend) *out_nsend = p->send_off.back();
+  if (out_nrecv) *out_nrecv = p->recv_off.back();
+  SG_API_END
+}
+
+int32_t sg_halo_pack(uint64_t plan, uint64_t field, void* dev_sendbuf, uint64_t stream) {
+  SG_API_BEGIN
+  Plan* p = get<Plan>(plan, ObjKind::Plan);
+  Field* f = get<Field>(field, ObjKind::Field);
+  check_field(p, f);
+  const int64_t n = p->send_off.back();
+  if (n == 0) return SG_OK;
+  SG_REQUIRE(dev_sendbuf, "null send buffer");
+  DeviceScope ds(p->device);
+  pack_rows<<<warps_grid(n), 256, 0, as_stream(stream)>>>(f->buf.as<uint32_t>(), pitch_words(f), row_words(f),
+                                                          p->send_rows.as<int32_t>(), n,
+                                                          static_cast<uint32_t*>(dev_sendbuf));
+  SG_CUDA_LAUNCH();
+  SG_API_END
+}
+
+int32_t sg_halo_unpack(uint64_t plan, uint64_t field, const void* dev_recvbuf, uint64_t stream) {
+  SG_API_BEGIN
+  Plan* p = get<Plan>(plan, ObjKind::Plan);
+  Field* f = get<Field>(field, ObjKind::Field);
+  check_field(p, f);
+  const int64_t n = p->recv_off.back();
+  if (n == 0) return SG_OK;
+  SG_REQUIRE(dev_recvbuf, "null receive buffer");
+  DeviceScope ds(p->device);
+  unpack_rows<<<warps_grid(n), 256, 0, as_stream(stream)>>>(f->buf.as<uint32_t>(), pitch_words(f), row_words(f),
+                                                            p->recv_rows.as<int32_t>(), n,
+                                                            static_cast<const uint32_t*>(dev_recvbuf));
+  SG_CUDA_LAUNCH();
+  SG_API_END
+}
+
+int32_t sg_halo_pull(uint64_t plan, uint64_t field, const uint64_t* peer_ptrs, const int64_t* peer_pitch_elems,
+                     uint64_t stream) {
+  SG_API_BEGIN
+  Plan* p = get<Plan>(plan, ObjKind::Plan);
+  Field* f = get<Field>(field, ObjKind::Field);
+  check_field(p, f);
+  const int64_t n = p->recv_off.back();
+  if (n == 0) return SG_OK;
+  SG_REQUIRE(peer_ptrs && peer_pitch_elems, "null peer arrays");
+  PeerPtrs pp{};
+  const int64_t wpi = f->itemsize / 4;
+  bool vec = (pitch_words(f) % 4 == 0);
+  for (size_t i = 0; i < p->peers.size(); ++i) {
+    pp.base[i] = reinterpret_cast<const uint32_t*>(peer_ptrs[i]);
+    pp.pitch_w[i] = peer_pitch_elems[i] * wpi;
+    if (p->recv_off[i + 1] > p->recv_off[i]) SG_REQUIRE(pp.base[i], "null peer pointer for peer %d", p->peers[i]);
+    vec = vec && (pp.pitch_w[i] % 4 == 0) && (peer_ptrs[i] % 16 == 0) && pp.pitch_w[i] >= (row_words(f) + 3) / 4 * 4;
+  }
+  vec = vec && pitch_words(f) >= (row_words(f) + 3) / 4 * 4;
+  DeviceScope ds(p->device);
+  if (vec)
+    pull_rows<true><<<warps_grid(n), 256, 0, as_stream(stream)>>>(
+        f->buf.as<uint32_t>(), pitch_words(f), row_words(f), p->recv_rows.as<int32_t>(), p->recv_remote.as<int32_t>(),
+        p->recv_peer.as<int32_t>(), n, pp);
+  else
+    pull_rows<false><<<warps_grid(n), 256, 0, as_stream(stream)>>>(
+        f->buf.as<uint32_t>(), pitch_words(f), row_words(f), p->recv_rows.as<int32_t>(), p->recv_remote.as<int32_t>(),
+        p->recv_peer.as<int32_t>(), n, pp);
+  SG_CUDA_LAUNCH();
+  SG_API_END
+}
+
+int32_t sg_nccl_unique_id(uint8_t* out_id, size_t n) {
+  SG_API_BEGIN
+  SG_REQUIRE(out_id && n >= sizeof(ncclUniqueId), "buffer must hold %zu bytes", sizeof(ncclUniqueId));
+  ncclUniqueId id;
+  SG_NCCL(nccl().GetUniqueId(&id));
+  memcpy(out_id, &id, sizeof(id));
+  SG_API_END
+}
+
+int32_t sg_comm_create(int32_t device, int32_t nranks, int32_t rank, const uint8_t* id, size_t n,
+                       uint64_t* out_comm) {
+  SG_API_BEGIN
+  SG_REQUIRE(out_comm && id && n >= sizeof(ncclUniqueId), "bad arguments");
+  SG_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, "rank %d not in [0, %d)", rank, nranks);
+  DeviceScope ds(device);
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  auto c = std::make_unique<Comm>();
+  c->device = device;
+  c->nranks = nranks;
+  c->rank = rank;
+  SG_NCCL(nccl().CommInitRank(&c->comm, nranks, uid, rank));
+  *out_comm = registry_put(c.release());
+  SG_API_END
+}
+
+int32_t sg_halo_exchange_nccl(uint64_t plan, uint64_t field, uint64_t comm, uint64_t stream) {
+  SG_API_BEGIN
+  Plan* p = get<Plan>(plan, ObjKind::Plan);
+  Field* f = get<Field>(field, ObjKind::Field);
+  Comm* c = get<Comm>(comm, ObjKind::Comm);
+  check_field(p, f);
+  DeviceScope ds(p->device);
+  cudaStream_t st = as_stream(stream);
+  const int64_t ns = p->send_off.back(), nr = p->recv_off.back();
+  const size_t W = (size_t)row_words(f);  // payload words per row
+  if ((size_t)ns * W * 4 > p->sendbuf.bytes) p->sendbuf.alloc(p->device, (size_t)ns * W * 4);
+  if ((size_t)nr * W * 4 > p->recvbuf.bytes) p->recvbuf.alloc(p->device, (size_t)nr * W * 4);
+  if (ns) {
+    pack_rows<<<warps_grid(ns), 256, 0, st>>>(f->buf.as<uint32_t>(), pitch_words(f), (int)W, p->send_rows.as<int32_t>(),
+                                              ns, p->sendbuf.as<uint32_t>());
+    SG_CUDA_LAUNCH();
+  }
+  Nccl& N = nccl();
+  SG_NCCL(N.GroupStart());
+  for (size_t i = 0; i < p->peers.size(); ++i) {
+    const int64_t s0 = p->send_off[i], s1 = p->send_off[i + 1];
+    const int64_t r0 = p->recv_off[i], r1 = p->recv_off[i + 1];
+    if (s1 > s0) SG_NCCL(N.Send(p->sendbuf.as<uint32_t>() + s0 * W, (size_t)(s1 - s0) * W, ncclUint32, p->peers[i], c->comm, st));
+    if (r1 > r0) SG_NCCL(N.Recv(p->recvbuf.as<uint32_t>() + r0 * W, (size_t)(r1 - r0) * W, ncclUint32, p->peers[i], c->comm, st));
+  }
+  SG_NCCL(N.GroupEnd());
+  if (nr) {
+    unpack_rows<<<warps_grid(nr), 256, 0, st>>>(f->buf.as<uint32_t>(), pitch_words(f), (int)W, p->recv_rows.as<int32_t>(),
+                                                nr, p->recvbuf.as<uint32_t>());
+    SG_CUDA_LAUNCH();
+  }
+  SG_API_END
+}
+
+int32_t sg_ipc_handle(uint64_t field, uint8_t* out_handle, size_t n) {
+  SG_API_BEGIN
+  Field* f = get<Field>(field, ObjKind::Field);
+  SG_REQUIRE(out_handle && n >= sizeof(cudaIpcMemHandle_t), "buffer must hold %zu bytes", sizeof(cudaIpcMemHandle_t));
+  DeviceScope ds(f->device);
+  cudaIpcMemHandle_t h;
+  SG_CUDA(cudaIpcGetMemHandle(&h, f->buf.ptr));
+  memcpy(out_handle, &h, sizeof(h));
+  SG_API_END
+}
+
+int32_t sg_ipc_open(int32_t device, const uint8_t* handle, size_t n, uint64_t* out_ptr) {
+  SG_API_BEGIN
+  SG_REQUIRE(handle && out_ptr && n >= sizeof(cudaIpcMemHandle_t), "bad arguments");
+  DeviceScope ds(device);
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* ptr = nullptr;
+  SG_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  *out_ptr = reinterpret_cast<uint64_t>(ptr);
+  SG_API_END
+}
+
+int32_t sg_ipc_close(int32_t device, uint64_t ptr) {
+  SG_API_BEGIN
+  DeviceScope ds(device);
+  SG_CUDA(cudaIpcCloseMemHandle(reinterpret_cast<void*>(ptr)));
+  SG_API_END
+}
+
+}  // extern "C"

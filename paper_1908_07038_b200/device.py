@@ -1,0 +1,137 @@
+"""Per-thread device selection and device arrays.
+
+One host thread drives one GPU (the run_ranks model, SURVEY.md §5 "distributed comm
+backend"): ``set_device`` pins the calling thread's device; fields allocated afterwards
+live there.  ``DeviceArray`` is a pitched (npts, levels) view of a library-owned field
+buffer; it exports ``__cuda_array_interface__`` so torch / cupy can wrap it zero-copy.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+
+import numpy as np
+
+from . import _native as N
+
+_tls = threading.local()
+
+
+def set_device(device: int) -> None:
+    _tls.device = int(device)
+
+
+def current_device() -> int:
+    return getattr(_tls, "device", 0)
+
+
+def synchronize(device: int = None, stream: int = 0) -> None:
+    N.call("sg_stream_synchronize", current_device() if device is None else device, stream)
+
+
+class DeviceArray(N.Handle):
+    """Library-owned device buffer of one field (Field.device, field.py:102 of the
+    reference is a numpy copy; here it is HBM)."""
+
+    __slots__ = ("device", "shape", "dtype", "pitch", "ptr")
+
+    def __init__(self, npts: int, levels: int, dtype: np.dtype, device: int = None):
+        dev = current_device() if device is None else device
+        h, pitch, p = C.c_uint64(0), C.c_int64(0), C.c_uint64(0)
+        dtype = np.dtype(dtype)
+        N.call("sg_field_alloc", dev, npts, levels, dtype.itemsize, N.ref(h), N.ref(pitch), N.ref(p))
+        super().__init__(h.value)
+        self.device = dev
+        self.shape = (int(npts), int(levels))
+        self.dtype = dtype
+        self.pitch = pitch.value  # elements
+        self.ptr = p.value
+
+    @property
+    def __cuda_array_interface__(self):
+        typestr = self.dtype.str
+        return {
+            "shape": self.shape,
+            "typestr": typestr,
+            "data": (self.ptr, False),
+            "strides": (self.pitch * self.dtype.itemsize, self.dtype.itemsize),
+            "version": 3,
+        }
+
+    def upload(self, host: np.ndarray, stream: int = 0, sync: bool = True) -> None:
+        if host.shape != self.shape or host.dtype != self.dtype or not host.flags["C_CONTIGUOUS"]:
+            raise ValueError("host array must be C-contiguous with the field's shape and kind")
+        N.call("sg_field_h2d", self.handle, N.ptr(host), stream)
+        if sync:
+            synchronize(self.device, stream)
+
+    def download(self, host: np.ndarray, stream: int = 0, sync: bool = True) -> None:
+        if host.shape != self.shape or host.dtype != self.dtype or not host.flags["C_CONTIGUOUS"]:
+            raise ValueError("host array must be C-contiguous with the field's shape and kind")
+        N.call("sg_field_d2h", self.handle, N.ptr(host), stream)
+        if sync:
+            synchronize(self.device, stream)
+
+    def upload_rows(self, row0: int, host_rows: np.ndarray, stream: int = 0, sync: bool = True) -> None:
+        host_rows = np.ascontiguousarray(host_rows, dtype=self.dtype)
+        N.call("sg_field_h2d_rows", self.handle, row0, len(host_rows), N.ptr(host_rows), stream)
+        if sync:
+            synchronize(self.device, stream)
+
+    def download_rows(self, row0: int, nrows: int, stream: int = 0) -> np.ndarray:
+        out = np.empty((nrows, self.shape[1]), dtype=self.dtype)
+        N.call("sg_field_d2h_rows", self.handle, row0, nrows, N.ptr(out), stream)
+        synchronize(self.device, stream)
+        return out
+
+    def to_numpy(self) -> np.ndarray:
+        out = np.empty(self.shape, dtype=self.dtype)
+        self.download(out)
+        return out
+
+
+class PinnedArray:
+    """Page-locked host array (cudaHostAlloc) for full-rate asynchronous copies."""
+
+    def __init__(self, shape, dtype=np.float64):
+        dtype = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * dtype.itemsize
+        p = C.c_uint64(0)
+        N.call("sg_host_alloc", nbytes, N.ref(p))
+        self._ptr = p.value
+        buf = (C.c_char * max(nbytes, 1)).from_address(self._ptr)
+        self.array = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+
+    def free(self) -> None:
+        if self._ptr:
+            self.array = None
+            N.call("sg_host_free", self._ptr)
+            self._ptr = 0
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Event(N.Handle):
+    """CUDA event on a device; ``elapsed_ms(start, end)`` synchronises on ``end``."""
+
+    __slots__ = ()
+
+    def __init__(self, device: int = None):
+        h = C.c_uint64(0)
+        N.call("sg_event_create", current_device() if device is None else device, N.ref(h))
+        super().__init__(h.value)
+
+    def record(self, stream: int = 0) -> "Event":
+        N.call("sg_event_record", self.handle, stream)
+        return self
+
+    @staticmethod
+    def elapsed_ms(start: "Event", end: "Event") -> float:
+        ms = C.c_float(0)
+        N.call("sg_event_elapsed_ms", start.handle, end.handle, N.ref(ms))
+        return float(ms.value)

@@ -1,0 +1,258 @@
+"""Function spaces and the halo exchange (functionspace.py:1-258 of the reference).
+
+``NodeColumns`` binds fields to one partition's mesh nodes; its constructor builds the
+exchange plan with the reference's protocol (one request message per other rank, tag 101,
+functionspace.py:58-94).  The exchange itself runs on the GPU:
+
+* ``halo_exchange(plan, f, ctx)`` — the reference entry point with the reference semantics
+  (PlanMismatch, StaleHost on DEVICE_DIRTY, SYNCED -> HOST_DIRTY, one counted message per
+  peer with the payload's byte length, functionspace.py:107-118).  The ghost values are
+  moved by device kernels: through the field's own device mirror when it is current
+  (SYNCED), otherwise through a device staging copy of the host rows; the received ghost
+  rows are copied back into ``f.host``.
+* ``halo_exchange_device(plan, f, ctx)`` — device-resident fields (SYNCED / DEVICE_DIRTY):
+  exchange in HBM only, field left DEVICE_DIRTY (SURVEY.md §8(b) "device entry points").
+
+Transport: ranks of one process (``run_ranks``) use one fused pull kernel over peer memory;
+one process per GPU (``DistContext``) uses pack -> grouped NCCL send/recv -> unpack.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field as dc_field
+from typing import Dict, Optional
+
+import numpy as np
+
+from . import _native as N
+from .device import DeviceArray, current_device
+from .errors import InconsistentMesh, PlanMismatch, StaleHost
+from .field import Field, Kind, MemoryState, create_field
+from .grid import Grid
+from .mesh import Mesh
+from .partition import Distribution
+
+_TAG_PLAN_REQUEST = 101  # functionspace.py:24
+_TAG_EXCHANGE = 102  # functionspace.py:25
+
+
+@dataclass
+class HaloExchangePlan:
+    """Per peer: owned local rows to send (requester's order) and ghost local rows to
+    receive ((halo, gidx) order); ``recv_remote`` adds each ghost's row on its owner
+    (mesh.py:303-308), which is what the peer-memory pull kernel reads."""
+
+    nnodes: int
+    send: Dict[int, np.ndarray] = dc_field(default_factory=dict)
+    recv: Dict[int, np.ndarray] = dc_field(default_factory=dict)
+    recv_remote: Dict[int, np.ndarray] = dc_field(default_factory=dict)
+    _native: Dict[int, N.Handle] = dc_field(default_factory=dict, repr=False)
+
+    @property
+    def peers(self):
+        return sorted(set(self.send) | set(self.recv))
+
+    @property
+    def ghost_rows(self) -> Optional[tuple]:
+        """[lo, hi) spanning every received row (ghosts are numbered last)."""
+        if not self.recv:
+            return None
+        allr = np.concatenate(list(self.recv.values()))
+        return int(allr.min()), int(allr.max()) + 1
+
+    def native(self, device: int) -> int:
+        h = self._native.get(device)
+        if h is None:
+            peers = self.peers
+            arr = lambda d, p: d.get(p, np.empty(0, np.int64))  # noqa: E731
+            sc = np.array([len(arr(self.send, p)) for p in peers], np.int64)
+            rc = np.array([len(arr(self.recv, p)) for p in peers], np.int64)
+            cat = lambda parts: np.ascontiguousarray(  # noqa: E731
+                np.concatenate(parts) if parts else np.empty(0), dtype=np.int64)
+            srows = cat([arr(self.send, p) for p in peers])
+            rrows = cat([arr(self.recv, p) for p in peers])
+            rrem = cat([arr(self.recv_remote, p) if p in self.recv_remote else
+                        np.full(len(arr(self.recv, p)), -1) for p in peers])
+            pv = np.array(peers, np.int32)
+            out = C.c_uint64(0)
+            N.call("sg_halo_plan_create", device, self.nnodes, len(peers), N.ptr(pv), N.ptr(sc), N.ptr(srows),
+                   N.ptr(rc), N.ptr(rrows), N.ptr(rrem), N.ref(out))
+            h = self._native[device] = N.Handle(out.value)
+        return h.handle
+
+    # -- device transports --------------------------------------------------------------------
+    def pull(self, dev: DeviceArray, peer_info) -> None:
+        """peer_info[r] = (ptr, pitch, device) of rank r's field; one fused kernel."""
+        peers = self.peers
+        ptrs = np.array([peer_info[p][0] for p in peers] or [0], np.uint64)
+        pitch = np.array([peer_info[p][1] for p in peers] or [0], np.int64)
+        N.call("sg_halo_pull", self.native(dev.device), dev.handle, N.ptr(ptrs), N.ptr(pitch), 0)
+
+    def exchange_nccl(self, dev: DeviceArray, comm: int, stream: int = 0) -> None:
+        N.call("sg_halo_exchange_nccl", self.native(dev.device), dev.handle, comm, stream)
+
+    def pack(self, dev: DeviceArray, sendbuf_ptr: int, stream: int = 0) -> None:
+        N.call("sg_halo_pack", self.native(dev.device), dev.handle, sendbuf_ptr, stream)
+
+    def unpack(self, dev: DeviceArray, recvbuf_ptr: int, stream: int = 0) -> None:
+        N.call("sg_halo_unpack", self.native(dev.device), dev.handle, recvbuf_ptr, stream)
+
+
+def build_exchange_plan(mesh: Mesh, ctx) -> HaloExchangePlan:
+    """Request/response plan build (functionspace.py:58-94): every rank sends each other
+    rank the global ids it needs from it (possibly none); owners answer by mapping them to
+    owned local rows in the requested order."""
+    plan = HaloExchangePlan(nnodes=mesh.nb_nodes)
+    if ctx is None or ctx.nranks == 1:
+        return plan
+    ghosts = np.flatnonzero(mesh.node_ghost)
+    owner = mesh.node_part[ghosts]
+    for p in np.unique(owner):
+        rows = ghosts[owner == p]
+        plan.recv[int(p)] = rows
+        plan.recv_remote[int(p)] = mesh.node_remote[rows].astype(np.int64)
+    owned_gid = mesh.node_global[~mesh.node_ghost]
+    # owned local rows are 0..n_owned-1 in ascending gid: a sorted lookup replaces the dict
+    for peer in range(ctx.nranks):
+        if peer != ctx.rank:
+            want = plan.recv.get(peer)
+            gids = mesh.node_global[want] if want is not None else np.empty(0, np.int64)
+            ctx.send(peer, _TAG_PLAN_REQUEST, np.asarray(gids, np.int64).tobytes())
+    for peer in range(ctx.nranks):
+        if peer == ctx.rank:
+            continue
+        req = np.frombuffer(ctx.receive(peer, _TAG_PLAN_REQUEST), dtype=np.int64)
+        if len(req) == 0:
+            continue
+        pos = np.searchsorted(owned_gid, req)
+        bad = (pos >= len(owned_gid)) | (owned_gid[np.minimum(pos, len(owned_gid) - 1)] != req)
+        if np.any(bad):
+            g = int(req[np.argmax(bad)])
+            raise InconsistentMesh(f"rank {ctx.rank} asked for global index {g} it does not own")
+        plan.send[peer] = pos.astype(np.int64)
+    return plan
+
+
+def _count_messages(plan: HaloExchangePlan, f: Field, ctx) -> None:
+    """The reference sends one message per send-peer and receives one per recv-peer
+    (functionspace.py:113-117); keep the counters identical."""
+    row_bytes = f.levels * f.host.dtype.itemsize
+    for peer in sorted(plan.send):
+        ctx.messages_sent += 1
+        ctx.bytes_sent += len(plan.send[peer]) * row_bytes
+    ctx.messages_received += len(plan.recv)
+
+
+def _staging(f: Field) -> DeviceArray:
+    st = getattr(f, "_halo_staging", None)
+    dev = current_device()
+    if st is None or st.device != dev:
+        st = DeviceArray(f.npts, f.levels, f.kind.dtype, dev)
+        object.__setattr__(f, "_halo_staging", st)
+    return st
+
+
+def halo_exchange(plan: HaloExchangePlan, f: Field, ctx) -> None:
+    """Copy owner values into every ghost row, all levels (functionspace.py:107-118)."""
+    if f.npts != plan.nnodes:
+        raise PlanMismatch(f"field has {f.npts} points, plan covers {plan.nnodes} nodes")
+    if f.state is MemoryState.DEVICE_DIRTY:
+        raise StaleHost(f"field {f.name!r} is device-dirty; update_host before exchanging")
+    if ctx is not None and getattr(ctx, "nranks", 1) > 1:
+        if f.state is MemoryState.SYNCED and f.device is not None and f.device.device == current_device():
+            dev = f.device
+        else:
+            dev = _staging(f)
+            dev.upload(f.host)
+        ctx.device_exchange(plan, dev)
+        span = plan.ghost_rows
+        if span is not None:
+            lo, hi = span
+            f.host[lo:hi] = dev.download_rows(lo, hi - lo)
+        _count_messages(plan, f, ctx)
+    if f.state is MemoryState.SYNCED:
+        f.state = MemoryState.HOST_DIRTY
+
+
+def halo_exchange_device(plan: HaloExchangePlan, f: Field, ctx) -> None:
+    """Device-resident exchange: field must be SYNCED or DEVICE_DIRTY; ends DEVICE_DIRTY."""
+    if f.npts != plan.nnodes:
+        raise PlanMismatch(f"field has {f.npts} points, plan covers {plan.nnodes} nodes")
+    if f.state in (MemoryState.HOST_ONLY, MemoryState.HOST_DIRTY):
+        from .errors import StaleDevice
+
+        raise StaleDevice(f"field {f.name!r} has no current device mirror; update_device first")
+    if ctx is not None and getattr(ctx, "nranks", 1) > 1:
+        ctx.device_exchange(plan, f.device)
+        _count_messages(plan, f, ctx)
+    f.mark_device_written()
+
+
+class NodeColumns:
+    """Fields on the nodes (owned + ghost) of one partition's mesh (functionspace.py:121-154)."""
+
+    def __init__(self, mesh: Mesh, ctx=None):
+        self.mesh = mesh
+        self.halo = mesh.halo_depth
+        self.exchange_plan = build_exchange_plan(mesh, ctx)
+        self._owned = ~mesh.node_ghost
+
+    @property
+    def nb_nodes(self) -> int:
+        return self.mesh.nb_nodes
+
+    @property
+    def owned_global(self) -> np.ndarray:
+        return self.mesh.node_global[self._owned]
+
+    @property
+    def global_size(self) -> int:
+        return self.mesh.grid.npts + (2 if self.mesh.include_pole else 0)
+
+    def owned_rows(self, f: Field) -> np.ndarray:
+        return f.host[self._owned]
+
+    def owned_row_index(self) -> np.ndarray:
+        return np.flatnonzero(self._owned)
+
+    def create_field(self, name: str, levels: int = 1, kind: Kind = Kind.REAL64) -> Field:
+        f = create_field(name, (self.mesh.nb_nodes, levels), kind)
+        f.functionspace_tag = f"nodes:{self.mesh.grid.name}:p{self.mesh.partition_id}"
+        return f
+
+    def halo_exchange(self, f: Field, ctx=None) -> None:
+        halo_exchange(self.exchange_plan, f, ctx)
+
+    def halo_exchange_device(self, f: Field, ctx=None) -> None:
+        halo_exchange_device(self.exchange_plan, f, ctx)
+
+
+class StructuredColumns:
+    """Fields on the owned points of a distributed grid; rows = owned gids ascending, the
+    row order of InterpolationWeights.target_global (functionspace.py:157-182)."""
+
+    def __init__(self, grid: Grid, dist: Distribution, part: int = 0):
+        self.grid = grid
+        self.dist = dist
+        self.part = part
+        self.local_points = np.flatnonzero(dist.part_of == part).astype(np.int64)
+
+    @property
+    def owned_global(self) -> np.ndarray:
+        return self.local_points
+
+    @property
+    def global_size(self) -> int:
+        return self.grid.npts
+
+    def owned_rows(self, f: Field) -> np.ndarray:
+        return f.host
+
+    def owned_row_index(self) -> np.ndarray:
+        return np.arange(len(self.local_points))
+
+    def create_field(self, name: str, levels: int = 1, kind: Kind = Kind.REAL64) -> Field:
+        f = create_field(name, (len(self.local_points), levels), kind)
+        f.functionspace_tag = f"structured:{self.grid.name}:p{self.part}"
+        return f

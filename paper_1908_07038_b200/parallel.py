@@ -1,0 +1,321 @@
+"""Rank runtimes: the communication backend under NodeColumns / halo_exchange.
+
+``run_ranks`` / ``RankContext`` keep the reference's in-process model and contract
+(parallel.py:1-195): N rank programs on N threads, blocking tagged FIFO send/receive per
+(source, destination), barrier, gather/broadcast through rank 0, deadlock detection, an
+unconsumed-message check and the messages_sent / bytes_sent / messages_received counters
+the reference's tests assert.  B200 additions: every rank thread is pinned to a GPU
+(``devices``, default: the visible GPUs round-robin, else device 0), and ranks of one
+process share device pointers through ``share`` so the device halo exchange is a single
+pull kernel over peer memory (same device, or NVLink P2P) — no host staging.
+
+``DistContext`` is the same interface over ``torch.distributed`` for one process per GPU
+(torchrun): host messages on a gloo group, device halo exchange through the library's own
+NCCL communicator (grouped ncclSend/ncclRecv between pack and unpack kernels).
+"""
+
+from __future__ import annotations
+
+import pickle
+import threading
+from collections import deque
+from dataclasses import dataclass, field
+from typing import Any, Callable, Dict, List, Optional
+
+from . import device as D
+from .errors import DeadlockDetected, InvalidRank, UnconsumedMessages
+
+_GATHER_TAG = 1 << 20  # parallel.py:19
+_BCAST_TAG = (1 << 20) + 1  # parallel.py:20
+
+
+class _Abort(Exception):
+    """Another rank failed; unwind quietly."""
+
+
+class _World:
+    def __init__(self, nranks: int):
+        self.nranks = nranks
+        self.cv = threading.Condition()
+        self.boxes: Dict[tuple, deque] = {}
+        self.waiting: Dict[int, Callable[[], bool]] = {}
+        self.done: set = set()
+        self.deadlocked = False
+        self.aborted = False
+        self.epoch = 0
+        self.arrived = 0
+        self.board: Dict[tuple, Any] = {}
+
+    def box(self, src: int, dst: int) -> deque:
+        return self.boxes.setdefault((src, dst), deque())
+
+    def _stuck(self) -> bool:
+        # every unfinished rank waits and nobody's wake-up condition holds (parallel.py:49-64)
+        live = self.nranks - len(self.done)
+        return live > 0 and len(self.waiting) == live and not any(p() for p in self.waiting.values())
+
+    def block(self, rank: int, ready: Callable[[], bool]) -> None:
+        self.waiting[rank] = ready
+        try:
+            if self._stuck():
+                self.deadlocked = True
+                self.cv.notify_all()
+            while not ready():
+                if self.deadlocked:
+                    raise DeadlockDetected(f"rank {rank} blocked with no possible sender")
+                if self.aborted:
+                    raise _Abort()
+                self.cv.wait()
+        finally:
+            self.waiting.pop(rank, None)
+
+    def finish(self, rank: int) -> None:
+        self.done.add(rank)
+        if self._stuck():
+            self.deadlocked = True
+        self.cv.notify_all()
+
+
+@dataclass
+class RankContext:
+    rank: int
+    nranks: int
+    _rt: _World = field(repr=False, default=None)
+    messages_sent: int = 0
+    bytes_sent: int = 0
+    messages_received: int = 0
+    device: int = 0
+    _share_seq: int = field(repr=False, default=0)
+
+    def _peer(self, peer: int) -> None:
+        if not isinstance(peer, int) or not 0 <= peer < self.nranks:
+            raise InvalidRank(f"rank {peer} not in [0, {self.nranks})")
+        if peer == self.rank:
+            raise InvalidRank("self-send/receive not allowed")
+
+    def send(self, dest: int, tag: int, payload: bytes) -> None:
+        self._peer(dest)
+        data = bytes(payload)
+        w = self._rt
+        with w.cv:
+            w.box(self.rank, dest).append((tag, data))
+            self.messages_sent += 1
+            self.bytes_sent += len(data)
+            w.cv.notify_all()
+
+    def receive(self, source: int, tag: int) -> bytes:
+        self._peer(source)
+        w = self._rt
+        with w.cv:
+            q = w.box(source, self.rank)
+
+            def find():
+                return next((k for k, (t, _) in enumerate(q) if t == tag), None)
+
+            if find() is None:
+                w.block(self.rank, lambda: find() is not None)
+            k = find()
+            _, data = q[k]
+            del q[k]
+            self.messages_received += 1
+            return data
+
+    def barrier(self) -> None:
+        w = self._rt
+        with w.cv:
+            epoch = w.epoch
+            w.arrived += 1
+            if w.arrived == w.nranks:
+                w.epoch += 1
+                w.arrived = 0
+                w.cv.notify_all()
+                return
+            w.block(self.rank, lambda: w.epoch > epoch)
+
+    def gather_to_root(self, payload: bytes) -> Optional[List[bytes]]:
+        if self.rank != 0:
+            self.send(0, _GATHER_TAG, payload)
+            return None
+        return [bytes(payload)] + [self.receive(s, _GATHER_TAG) for s in range(1, self.nranks)]
+
+    def broadcast_from_root(self, payload: Optional[bytes]) -> bytes:
+        if self.rank != 0:
+            return self.receive(0, _BCAST_TAG)
+        data = bytes(payload)
+        for d in range(1, self.nranks):
+            self.send(d, _BCAST_TAG, data)
+        return data
+
+    # -- B200 additions ---------------------------------------------------------------------
+    def share(self, value: Any) -> List[Any]:
+        """Collective: every rank contributes ``value``; all get the list ordered by rank.
+        Not a message (no counters): ranks of one process share an address space."""
+        self._share_seq += 1
+        key = self._share_seq
+        w = self._rt
+        with w.cv:
+            w.board[(key, self.rank)] = value
+        self.barrier()
+        with w.cv:
+            out = [w.board[(key, r)] for r in range(self.nranks)]
+        self.barrier()
+        with w.cv:
+            w.board.pop((key, self.rank), None)
+        return out
+
+    def device_exchange(self, plan, dev_array) -> None:
+        """Fused device halo exchange over peer memory: one pull kernel per rank."""
+        D.synchronize(dev_array.device)
+        ptrs = self.share((dev_array.ptr, dev_array.pitch, dev_array.device))
+        plan.pull(dev_array, ptrs)
+        D.synchronize(dev_array.device)
+        self.barrier()
+
+
+def _default_devices() -> List[int]:
+    from . import _native as N
+
+    n = N.device_count()
+    return list(range(n)) if n > 0 else [0]
+
+
+def run_ranks(nranks: int, program: Callable[[RankContext], object], devices: Optional[List[int]] = None) -> list:
+    """Run program(ctx) on nranks threads; results ordered by rank (parallel.py:154-195)."""
+    if nranks < 1:
+        raise ValueError("nranks must be >= 1")
+    devs = list(devices) if devices is not None else None
+    w = _World(nranks)
+    results: list = [None] * nranks
+    failures: list = [None] * nranks
+
+    def body(r: int) -> None:
+        ctx = RankContext(rank=r, nranks=nranks, _rt=w)
+        try:
+            if devs is None:
+                dl = _default_devices()
+            else:
+                dl = devs
+            ctx.device = dl[r % len(dl)]
+            D.set_device(ctx.device)
+            results[r] = program(ctx)
+        except _Abort:
+            pass
+        except BaseException as exc:  # noqa: BLE001 - re-raised by the caller
+            failures[r] = exc
+            with w.cv:
+                w.aborted = True
+                w.cv.notify_all()
+        finally:
+            with w.cv:
+                w.finish(r)
+
+    threads = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(nranks)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for exc in failures:
+        if exc is not None:
+            raise exc
+    left = sum(len(q) for q in w.boxes.values())
+    if left:
+        raise UnconsumedMessages(f"{left} messages left in queues at shutdown")
+    return results
+
+
+class DistContext:
+    """RankContext contract over torch.distributed, one process per GPU.
+
+    Host messages (plan build, gather) travel on a gloo group as uint8 tensors; counters
+    mirror the reference.  ``device_exchange`` uses the library's NCCL communicator."""
+
+    def __init__(self, group=None, device: Optional[int] = None):
+        import torch.distributed as dist
+
+        self._dist = dist
+        self.rank = dist.get_rank()
+        self.nranks = dist.get_world_size()
+        self._group = group if group is not None else (
+            dist.new_group(backend="gloo") if dist.get_backend() != "gloo" else None)
+        self.device = D.current_device() if device is None else int(device)
+        self.messages_sent = 0
+        self.bytes_sent = 0
+        self.messages_received = 0
+        self._comm = None
+        self._pending: Dict[tuple, deque] = {}
+
+    def _peer(self, peer: int) -> None:
+        if not isinstance(peer, int) or not 0 <= peer < self.nranks:
+            raise InvalidRank(f"rank {peer} not in [0, {self.nranks})")
+        if peer == self.rank:
+            raise InvalidRank("self-send/receive not allowed")
+
+    def send(self, dest: int, tag: int, payload: bytes) -> None:
+        import torch
+
+        self._peer(dest)
+        data = pickle.dumps((tag, bytes(payload)))
+        n = torch.tensor([len(data)], dtype=torch.int64)
+        self._dist.send(n, dest, group=self._group)
+        self._dist.send(torch.frombuffer(bytearray(data), dtype=torch.uint8), dest, group=self._group)
+        self.messages_sent += 1
+        self.bytes_sent += len(payload)
+
+    def receive(self, source: int, tag: int) -> bytes:
+        import torch
+
+        self._peer(source)
+        q = self._pending.setdefault(source, deque())
+        while True:
+            for k, (t, data) in enumerate(q):
+                if t == tag:
+                    del q[k]
+                    self.messages_received += 1
+                    return data
+            n = torch.zeros(1, dtype=torch.int64)
+            self._dist.recv(n, source, group=self._group)
+            buf = torch.empty(int(n.item()), dtype=torch.uint8)
+            self._dist.recv(buf, source, group=self._group)
+            q.append(pickle.loads(buf.numpy().tobytes()))
+
+    def barrier(self) -> None:
+        self._dist.barrier(group=self._group)
+
+    def gather_to_root(self, payload: bytes) -> Optional[List[bytes]]:
+        if self.rank != 0:
+            self.send(0, _GATHER_TAG, payload)
+            return None
+        return [bytes(payload)] + [self.receive(s, _GATHER_TAG) for s in range(1, self.nranks)]
+
+    def broadcast_from_root(self, payload: Optional[bytes]) -> bytes:
+        if self.rank != 0:
+            return self.receive(0, _BCAST_TAG)
+        data = bytes(payload)
+        for d in range(1, self.nranks):
+            self.send(d, _BCAST_TAG, data)
+        return data
+
+    def share(self, value: Any) -> List[Any]:
+        out: List[Any] = [None] * self.nranks
+        self._dist.all_gather_object(out, value, group=self._group)
+        return out
+
+    def nccl_comm(self) -> int:
+        if self._comm is None:
+            import ctypes as C
+
+            from . import _native as N
+
+            uid = (C.c_uint8 * 128)()
+            if self.rank == 0:
+                N.call("sg_nccl_unique_id", N.ref(uid), 128)
+            blob = self.share(bytes(uid) if self.rank == 0 else None)[0]
+            uid = (C.c_uint8 * 128).from_buffer_copy(blob)
+            h = C.c_uint64(0)
+            N.call("sg_comm_create", self.device, self.nranks, self.rank, N.ref(uid), 128, N.ref(h))
+            self._comm = N.Handle(h.value)
+        return self._comm.handle
+
+    def device_exchange(self, plan, dev_array, stream: int = 0) -> None:
+        plan.exchange_nccl(dev_array, self.nccl_comm(), stream)
+        D.synchronize(dev_array.device, stream)

@@ -1,0 +1,204 @@
+"""Generates the golden fixtures under tests/golden/ by running the UNMODIFIED reference
+(`spheregrid`, /root/reference/pkg/src) in this container.  The reference cannot travel to
+the GPU box, so its outputs are committed here as small .npz files.
+
+Run:  PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [names...]
+Host check: tools/host_probe.py digests of numpy's arcsin/cos/sin/dot were identical here
+and on the GPU box host (gpurun_out/probe_*.json), so coordinates built from these
+latitudes have the same bits on both.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+import spheregrid as R  # noqa: E402
+from spheregrid import interp as RI  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path) / 1e6:.2f} MB)", flush=True)
+
+
+def latitudes():
+    out = {}
+    for n in [1, 2, 4, 8, 16, 32, 64, 80, 160, 320, 640, 1280]:
+        t = time.time()
+        out[f"n{n}"] = R.gaussian_latitudes(n)
+        print("lat", n, round(time.time() - t, 1), flush=True)
+    save("latitudes", **out)
+
+
+def stencil_arrays(w):
+    return dict(target_global=w.target_global, nodes=w.nodes.astype(np.int32), weights=w.weights,
+                scale=w.scale, fallback=w.fallback)
+
+
+def serial_remap(src, tgt, levels, fname):
+    """P=1 pipeline slice (cli.py:129-144): mesh with poles, NodeColumns, build, apply on a
+    random field (seed 2026, test_acceptance.py:133)."""
+    S, T = R.grid_from_name(src), R.grid_from_name(tgt)
+    dist = R.blocks_partition(S, 1)
+    mesh = R.generate_mesh(S, dist, 0, halo=2, include_pole=True)
+    fs = R.NodeColumns(mesh, None)
+    tdist = R.matching_partition(T, S, dist)
+    t = time.time()
+    w = R.build_remap(fs, T, tdist)
+    print(f"{fname} build_remap {time.time() - t:.1f} s", flush=True)
+    f = fs.create_field("src", levels=levels)
+    f.host[:] = np.random.default_rng(2026).normal(size=f.host.shape)
+    tf = R.StructuredColumns(T, tdist, 0).create_field("dst", levels=levels)
+    R.apply_remap(w, f, tf)
+    save(fname, **stencil_arrays(w), src_lat=S.latitudes, tgt_lat=T.latitudes, node_global=mesh.node_global,
+         out=tf.host)
+
+
+def partitioned(src, tgt, nparts, halo, fname, levels=3):
+    """Per-rank meshes, plans, halo payload bytes and stencils of the distributed pipeline."""
+    S, T = R.grid_from_name(src), R.grid_from_name(tgt)
+    captured = {}
+    orig_send = R.RankContext.send
+
+    def spy(self, dest, tag, payload):
+        if tag == 102:
+            captured[(self.rank, dest)] = bytes(payload)
+        return orig_send(self, dest, tag, payload)
+
+    def program(ctx):
+        dist = R.blocks_partition(S, ctx.nranks)
+        mesh = R.generate_mesh(S, dist, ctx.rank, halo=halo, include_pole=True)
+        fs = R.NodeColumns(mesh, ctx)
+        tdist = R.matching_partition(T, S, dist)
+        f = fs.create_field("gid", levels=levels)
+        owned = fs.owned_row_index()
+        rng = np.random.default_rng(100 + ctx.rank)
+        f.host[owned] = mesh.node_global[owned, None] * 1000.0 + np.arange(levels)[None, :] \
+            + rng.normal(size=(len(owned), levels)) * 1e-3
+        before = f.host.copy()
+        sent0 = ctx.messages_sent
+        fs.halo_exchange(f, ctx)
+        msgs = ctx.messages_sent - sent0
+        try:
+            w = R.build_remap(fs, T, tdist, ctx)
+            st = stencil_arrays(w)
+            bad = -1
+        except R.errors.NotLocated as e:
+            st, bad = {}, e.target_global_index
+        plan = fs.exchange_plan
+        d = dict(node_global=mesh.node_global, node_part=mesh.node_part, node_remote=mesh.node_remote,
+                 node_halo=mesh.node_halo, conn_off=mesh.element_connectivity.offsets,
+                 conn_idx=mesh.element_connectivity.indices, elem_serial=mesh.elem_serial_id,
+                 before=before, after=f.host, messages=np.int64(msgs), not_located=np.int64(bad),
+                 tdist=tdist.part_of.astype(np.int8))
+        for p, v in plan.send.items():
+            d[f"send_{p}"] = v
+        for p, v in plan.recv.items():
+            d[f"recv_{p}"] = v
+        for k, v in st.items():
+            d["w_" + k] = v
+        return d
+
+    R.RankContext.send = spy
+    try:
+        t = time.time()
+        res = R.run_ranks(nparts, program)
+        print(f"{fname} {time.time() - t:.1f} s", flush=True)
+    finally:
+        R.RankContext.send = orig_send
+    out = {"src_lat": S.latitudes, "tgt_lat": T.latitudes, "nparts": np.int64(nparts), "halo": np.int64(halo)}
+    for r, d in enumerate(res):
+        for k, v in d.items():
+            out[f"r{r}_{k}"] = np.asarray(v)
+    for (a, b), payload in captured.items():
+        out[f"payload_{a}_{b}"] = np.frombuffer(payload, dtype=np.uint8)
+    save(fname, **out)
+
+
+def fallback_case():
+    """halo 0: NotLocated with allow_fallback=False; fallback rows with True (interp.py:179-190)."""
+    S, T = R.grid_from_name("O32"), R.grid_from_name("O16")
+    out = {}
+
+    def program(ctx):
+        dist = R.blocks_partition(S, ctx.nranks)
+        mesh = R.generate_mesh(S, dist, ctx.rank, halo=0, include_pole=True)
+        fs = R.NodeColumns(mesh, ctx)
+        tdist = R.matching_partition(T, S, dist)
+        w = R.build_remap(fs, T, tdist, ctx, allow_fallback=True)
+        try:
+            R.build_remap(fs, T, tdist, ctx, allow_fallback=False)
+            bad = -1
+        except R.errors.NotLocated as e:
+            bad = e.target_global_index
+        return dict(bad=np.int64(bad), **stencil_arrays(w))
+
+    res = R.run_ranks(4, program)
+    for r, d in enumerate(res):
+        for k, v in d.items():
+            out[f"r{r}_{k}"] = np.asarray(v)
+    save("fallback_O32_O16_p4_h0", **out)
+
+
+def matching():
+    out = {}
+    for tgt, src, P in [("O16", "O32", 4), ("O80", "O160", 8), ("O160", "O320", 8), ("O640", "O1280", 8)]:
+        S, T = R.grid_from_name(src), R.grid_from_name(tgt)
+        t = time.time()
+        idx, _ = R.PointCloudIndex(S).query(T.xyz())
+        out[f"{tgt}_{src}_idx"] = idx.astype(np.int32)
+        out[f"{tgt}_{src}_p{P}"] = R.matching_partition(T, S, R.blocks_partition(S, P)).part_of.astype(np.int8)
+        print("matching", tgt, src, round(time.time() - t, 1), flush=True)
+    save("matching", **out)
+
+
+def o1280_sample(n_random=5000):
+    """O1280 -> O640 serial: reference MeshLocator.locate on every lon 0/90/180/270 target
+    plus random targets (SURVEY.md §7 'Golden generation at O1280')."""
+    S, T = R.grid_from_name("O1280"), R.grid_from_name("O640")
+    t = time.time()
+    mesh = R.generate_mesh(S, R.blocks_partition(S, 1), 0, halo=2, include_pole=True)
+    print("mesh", round(time.time() - t, 1), flush=True)
+    loc = RI.MeshLocator(mesh)
+    print("locator", round(time.time() - t, 1), flush=True)
+    ll = T.lonlats()
+    special = np.flatnonzero(np.isin(ll[:, 0], [0.0, 90.0, 180.0, 270.0]))
+    rng = np.random.default_rng(1280)
+    rand = rng.choice(T.npts, size=n_random, replace=False)
+    ids = np.unique(np.concatenate([special, rand])).astype(np.int64)
+    xyz = T.xyz()
+    corners = np.empty((len(ids), 3), np.int64)
+    weights = np.empty((len(ids), 3))
+    for k, g in enumerate(ids):
+        _, tri, c = loc.locate(xyz[g])
+        corners[k] = c
+        weights[k] = RI.barycentric_weights(tri, xyz[g])
+    print("located", len(ids), round(time.time() - t, 1), flush=True)
+    save("o1280_o640_sample", ids=ids, corners=corners.astype(np.int32), weights=weights,
+         src_lat=S.latitudes, tgt_lat=T.latitudes)
+
+
+JOBS = {
+    "latitudes": latitudes,
+    "cfg1": lambda: serial_remap("O32", "O16", 10, "cfg1_O32_O16"),
+    "f8": lambda: serial_remap("F8", "F4", 2, "serial_F8_F4"),
+    "p4": lambda: partitioned("O32", "O16", 4, 2, "part_O32_O16_p4_h2"),
+    "f8p": lambda: partitioned("F8", "F4", 3, 1, "part_F8_F4_p3_h1"),
+    "p8": lambda: partitioned("O160", "O80", 8, 3, "part_O160_O80_p8_h3", levels=2),
+    "fallback": fallback_case,
+    "matching": matching,
+    "cfg2": lambda: serial_remap("O320", "O160", 1, "cfg2_O320_O160"),
+    "o1280": o1280_sample,
+}
+
+if __name__ == "__main__":
+    for name in sys.argv[1:] or list(JOBS):
+        JOBS[name]()

@@ -1,0 +1,70 @@
+"""Field host/device mirror on real HBM: the reference's state machine and copy counters
+(field.py:99-154, test_field.py:181-214) with real copies."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_round_trip_and_counters(gpu):
+    sg = gpu
+    f = sg.create_field("f", (1000, 137))
+    f.host[:] = np.random.default_rng(1).normal(size=f.host.shape)
+    keep = f.host.copy()
+    f.allocate_device()
+    assert f.state is sg.MemoryState.SYNCED and f.copy_counters["host_to_device"] == 1
+    assert np.array_equal(f.device.to_numpy(), keep)
+    with f.device_view(sg.Intent.READ_WRITE):
+        pass
+    assert f.state is sg.MemoryState.DEVICE_DIRTY
+    f.host[:] = 0
+    f.update_host()
+    assert np.array_equal(f.host, keep) and f.copy_counters["device_to_host"] == 1
+    with f.host_view(sg.Intent.READ_WRITE) as h:
+        h[0, 0] = 42.0
+    assert f.state is sg.MemoryState.HOST_DIRTY
+    f.syncHostDevice()
+    assert f.state is sg.MemoryState.SYNCED and f.device.to_numpy()[0, 0] == 42.0
+    with pytest.raises(sg.AlreadyAllocated):
+        f.allocate_device()
+
+
+@pytest.mark.parametrize("kind", ["REAL64", "REAL32", "INT32", "INT64"])
+@pytest.mark.parametrize("levels", [1, 3, 16, 137])
+def test_kinds_and_pitches(gpu, kind, levels):
+    sg = gpu
+    k = getattr(sg.Kind, kind)
+    f = sg.create_field("f", (257, levels), k)
+    f.host[:] = (np.arange(257 * levels).reshape(257, levels) % 1000).astype(k.dtype)
+    f.allocate_device()
+    assert f.device.pitch >= levels
+    assert np.array_equal(f.device.to_numpy(), f.host)
+    rows = f.device.download_rows(100, 50)
+    assert np.array_equal(rows, f.host[100:150])
+
+
+def test_cuda_array_interface(gpu):
+    sg = gpu
+    f = sg.create_field("f", (10, 137)).allocate_device()
+    cai = f.device.__cuda_array_interface__
+    assert cai["shape"] == (10, 137) and cai["strides"][0] == f.device.pitch * 8
+    torch = pytest.importorskip("torch")
+    t = torch.as_tensor(f.device, device="cuda")
+    assert t.shape == (10, 137)
+
+
+def test_stale_reads_raise(gpu):
+    sg = gpu
+    f = sg.create_field("f", (4, 2))
+    with pytest.raises(sg.NoDevice):
+        f.device_view()
+    f.allocate_device()
+    with f.host_view(sg.Intent.READ_WRITE):
+        pass
+    with pytest.raises(sg.StaleDevice):
+        f.device_view()
+    f.update_device()
+    with f.device_view(sg.Intent.READ_WRITE):
+        pass
+    with pytest.raises(sg.StaleHost):
+        f.host_view()

@@ -1,0 +1,132 @@
+"""GPU halo exchange: values bitwise equal to the reference's exchange, payload bytes of the
+pack kernel byte-equal to the reference's messages (f.host[send[peer]].tobytes(),
+functionspace.py:113-114), message accounting, state semantics, error classes."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def fixture_meshes(sg, z, sname):
+    S = sg.grid_with_latitudes(sname, z["src_lat"])
+    return S, int(z["nparts"]), int(z["halo"])
+
+
+@pytest.mark.parametrize("name,src", [("part_O32_O16_p4_h2", "O32"), ("part_F8_F4_p3_h1", "F8"),
+                                      ("part_O160_O80_p8_h3", "O160")])
+def test_halo_exchange_matches_reference(gpu, golden, name, src):
+    sg = gpu
+    from paper_1908_07038_b200.device import DeviceArray
+
+    z = golden(name)
+    S, P, halo = fixture_meshes(sg, z, src)
+    levels = z["r0_before"].shape[1]
+
+    def prog(ctx):
+        dist = sg.blocks_partition(S, ctx.nranks)
+        mesh = sg.generate_mesh(S, dist, ctx.rank, halo=halo, include_pole=True)
+        fs = sg.NodeColumns(mesh, ctx)
+        plan = fs.exchange_plan
+        for p in range(ctx.nranks):
+            k = f"r{ctx.rank}_send_{p}"
+            assert (p in plan.send) == (k in z)
+            if p in plan.send:
+                assert np.array_equal(plan.send[p], z[k])
+            k = f"r{ctx.rank}_recv_{p}"
+            if p in plan.recv:
+                assert np.array_equal(plan.recv[p], z[k])
+        f = fs.create_field("gid", levels=levels)
+        f.host[:] = z[f"r{ctx.rank}_before"]
+        s0, b0 = ctx.messages_sent, ctx.bytes_sent
+        fs.halo_exchange(f, ctx)
+        assert ctx.messages_sent - s0 == int(z[f"r{ctx.rank}_messages"])
+        assert np.array_equal(f.host.view(np.uint64), z[f"r{ctx.rank}_after"].view(np.uint64))
+        # pack kernel payload bytes == the reference's message bytes
+        dev = DeviceArray(f.npts, levels, np.float64)
+        dev.upload(np.ascontiguousarray(z[f"r{ctx.rank}_before"]))
+        nsend = sum(len(v) for v in plan.send.values())
+        buf = DeviceArray(max(nsend, 1), levels, np.float64)  # pitch may pad: use a flat buffer
+        flat = DeviceArray(1, max(nsend, 1) * levels, np.float64)
+        plan.pack(dev, flat.ptr)
+        got = flat.to_numpy().ravel()
+        off = 0
+        for p in sorted(plan.send):
+            n = len(plan.send[p]) * levels
+            assert got[off:off + n].tobytes() == z[f"payload_{ctx.rank}_{p}"].tobytes()
+            off += n
+        # second exchange changes nothing (idempotent, SPEC acceptance "halo exchange")
+        again = f.host.copy()
+        fs.halo_exchange(f, ctx)
+        assert np.array_equal(again, f.host)
+        del buf
+        return True
+
+    assert all(sg.run_ranks(P, prog))
+
+
+def test_ghosts_equal_global_index_f8(gpu):
+    """test_acceptance.py:101-127: on F8 with nparts 2/4 and halo 1/2 every ghost equals its
+    global index bitwise; messages == peers."""
+    sg = gpu
+    g = sg.grid_from_name("F8")
+    for P in (2, 4):
+        for h in (1, 2):
+            def prog(ctx):
+                dist = sg.blocks_partition(g, ctx.nranks)
+                mesh = sg.generate_mesh(g, dist, ctx.rank, halo=h, include_pole=True)
+                fs = sg.NodeColumns(mesh, ctx)
+                f = fs.create_field("g", 3, sg.Kind.INT64)
+                owned = fs.owned_row_index()
+                f.host[owned] = mesh.node_global[owned, None]
+                s0 = ctx.messages_sent
+                fs.halo_exchange(f, ctx)
+                ok = np.array_equal(f.host, np.repeat(mesh.node_global[:, None], 3, axis=1))
+                return ok, ctx.messages_sent - s0, len(fs.exchange_plan.send)
+
+            for ok, msgs, peers in sg.run_ranks(P, prog):
+                assert ok and msgs == peers
+
+
+def test_device_exchange_and_state(gpu):
+    sg = gpu
+    g = sg.grid_from_name("O32")
+
+    def prog(ctx):
+        dist = sg.blocks_partition(g, ctx.nranks)
+        mesh = sg.generate_mesh(g, dist, ctx.rank, halo=2, include_pole=True)
+        fs = sg.NodeColumns(mesh, ctx)
+        f = fs.create_field("x", 137)
+        owned = fs.owned_row_index()
+        f.host[owned] = mesh.node_global[owned, None] + np.arange(137)[None, :] * 0.25
+        f.allocate_device()
+        fs.halo_exchange_device(f, ctx)
+        st1 = f.state
+        f.update_host()
+        ok = np.array_equal(f.host, mesh.node_global[:, None] + np.arange(137)[None, :] * 0.25)
+        # StaleHost on DEVICE_DIRTY for the host entry point (test_functionspace.py:94-102)
+        fs.halo_exchange_device(f, ctx)
+        with pytest.raises(sg.StaleHost):
+            fs.halo_exchange(f, ctx)
+        ctx.barrier()
+        return st1 is sg.MemoryState.DEVICE_DIRTY and ok
+
+    assert all(sg.run_ranks(4, prog))
+
+
+def test_plan_mismatch_and_synced_to_host_dirty(gpu):
+    sg = gpu
+    g = sg.grid_from_name("F8")
+
+    def prog(ctx):
+        dist = sg.blocks_partition(g, ctx.nranks)
+        mesh = sg.generate_mesh(g, dist, ctx.rank, halo=1, include_pole=True)
+        fs = sg.NodeColumns(mesh, ctx)
+        with pytest.raises(sg.PlanMismatch):
+            fs.halo_exchange(sg.create_field("bad", (mesh.nb_nodes + 1, 1)), ctx)
+        f = fs.create_field("f", 1).allocate_device()
+        fs.halo_exchange(f, ctx)
+        return f.state is sg.MemoryState.HOST_DIRTY
+
+    assert all(sg.run_ranks(2, prog))

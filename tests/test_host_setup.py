@@ -1,0 +1,76 @@
+"""Host-side prerequisites of the hot path (grid, latitudes, partitions, per-partition
+mesh numbering — native C++ for the integer parts) are bit-identical to the reference's
+golden fixtures.  CPU only."""
+import numpy as np
+import pytest
+
+import paper_1908_07038_b200 as sg
+
+
+@pytest.mark.parametrize("n", [1, 2, 4, 8, 16, 32, 64, 80, 160, 320, 640, 1280])
+def test_gaussian_latitudes_bitwise(golden, n):
+    z = golden("latitudes")
+    assert np.array_equal(sg.gaussian_latitudes(n).view(np.uint64), z[f"n{n}"].view(np.uint64))
+
+
+def test_grid_numerology():
+    assert sg.grid_from_name("F8").npts == 512
+    assert sg.grid_from_name("O32").npts == 5248
+    assert sg.grid_from_name("O1280").npts == 6599680
+    with pytest.raises(sg.UnknownGridName):
+        sg.grid_from_name("bogus")
+
+
+def test_f1_point_latitude():
+    # test_cli.py:84-88 known answer
+    assert sg.grid_from_name("F1").latitudes[1] == -35.264389682754654
+
+
+@pytest.mark.parametrize("name", ["part_O32_O16_p4_h2", "part_F8_F4_p3_h1", "part_O160_O80_p8_h3"])
+def test_partition_meshes_bitwise(golden, name):
+    z = golden(name)
+    sname = {"part_O32_O16_p4_h2": "O32", "part_F8_F4_p3_h1": "F8", "part_O160_O80_p8_h3": "O160"}[name]
+    S = sg.grid_with_latitudes(sname, z["src_lat"])
+    P, halo = int(z["nparts"]), int(z["halo"])
+    dist = sg.blocks_partition(S, P)
+    for r in range(P):
+        m = sg.generate_mesh(S, dist, r, halo=halo, include_pole=True)
+        for k in ["node_global", "node_part", "node_remote", "node_halo"]:
+            assert np.array_equal(getattr(m, k), z[f"r{r}_{k}"]), (r, k)
+        assert np.array_equal(m.element_connectivity.offsets, z[f"r{r}_conn_off"])
+        assert np.array_equal(m.element_connectivity.indices, z[f"r{r}_conn_idx"])
+        assert np.array_equal(m.elem_serial_id, z[f"r{r}_elem_serial"])
+
+
+@pytest.mark.parametrize("tgt,src,P", [("O16", "O32", 4), ("O80", "O160", 8), ("O160", "O320", 8),
+                                       ("O640", "O1280", 8)])
+def test_matching_partition_bitwise(golden, tgt, src, P):
+    z = golden("matching")
+    S, T = sg.grid_from_name(src), sg.grid_from_name(tgt)
+    idx = sg.partition.nearest_master_points(S, T.xyz())
+    assert np.array_equal(idx, z[f"{tgt}_{src}_idx"])
+    d = sg.matching_partition(T, S, sg.blocks_partition(S, P))
+    assert np.array_equal(d.part_of, z[f"{tgt}_{src}_p{P}"])
+
+
+def test_blocks_partition_sizes():
+    g = sg.grid_from_name("O32")
+    d = sg.blocks_partition(g, 3)
+    assert d.counts.tolist() == [1750, 1749, 1749]
+    assert np.all(np.diff(d.part_of) >= 0)
+    with pytest.raises(sg.TooManyParts):
+        sg.blocks_partition(sg.grid_from_name("F1"), 100)
+
+
+def test_serial_mesh_counts():
+    # element counts of the serial meshes with poles
+    for name, ne in [("O32", 10104), ("O320", 838392)]:
+        g = sg.grid_from_name(name)
+        m = sg.generate_mesh(g, sg.blocks_partition(g, 1), 0, halo=0, include_pole=True)
+        assert m.nb_elements == ne
+        assert m.nb_nodes == g.npts + 2
+
+
+def test_split_quad_lowest_local_index():
+    tri = sg.split_quad(np.array([7, 3, 9, 5]))
+    assert [t.tolist() for t in tri] == [[3, 9, 5], [3, 5, 7]]

@@ -1,0 +1,91 @@
+"""Pins the oracle (oracle/, the CPU restatement used as the checker) against the golden
+fixtures produced by the unmodified reference (tests/golden/make_golden.py).  CPU only."""
+import numpy as np
+import pytest
+
+import paper_1908_07038_b200 as sg
+from oracle import oracle as O
+
+
+def serial_mesh(z, sname):
+    S = sg.grid_with_latitudes(sname, z["src_lat"])
+    return S, sg.generate_mesh(S, sg.blocks_partition(S, 1), 0, halo=2, include_pole=True)
+
+
+@pytest.mark.parametrize("name,src,tgt", [("cfg1_O32_O16", "O32", "O16"), ("serial_F8_F4", "F8", "F4")])
+def test_oracle_stencils_weights_apply_equal_reference(golden, name, src, tgt):
+    z = golden(name)
+    S, mesh = serial_mesh(z, src)
+    T = sg.grid_with_latitudes(tgt, z["tgt_lat"])
+    conn = mesh.element_connectivity
+    r = O.build_remap(mesh.node_xyz, conn.offsets, conn.indices, T.xyz()[z["target_global"]])
+    assert np.array_equal(r["nodes"], z["nodes"])
+    # same LAPACK on the same host: weights and scale are bit-identical to the reference
+    assert np.array_equal(r["weights"].view(np.uint64), z["weights"].view(np.uint64))
+    assert np.array_equal(r["scale"].view(np.uint64), z["scale"].view(np.uint64))
+    src_field = np.random.default_rng(2026).normal(size=(mesh.nb_nodes, z["out"].shape[1]))
+    out = O.apply_remap(z["nodes"].astype(np.int64), z["weights"], src_field)
+    assert np.array_equal(out.view(np.uint64), z["out"].view(np.uint64))
+
+
+def test_oracle_partitioned_stencils_equal_reference(golden):
+    z = golden("part_O32_O16_p4_h2")
+    S = sg.grid_with_latitudes("O32", z["src_lat"])
+    T = sg.grid_with_latitudes("O16", z["tgt_lat"])
+    P = int(z["nparts"])
+    dist = sg.blocks_partition(S, P)
+    for r in range(P):
+        mesh = sg.generate_mesh(S, dist, r, halo=int(z["halo"]), include_pole=True)
+        conn = mesh.element_connectivity
+        res = O.build_remap(mesh.node_xyz, conn.offsets, conn.indices, T.xyz()[z[f"r{r}_w_target_global"]])
+        assert np.array_equal(res["nodes"], z[f"r{r}_w_nodes"])
+        assert np.array_equal(res["weights"].view(np.uint64), z[f"r{r}_w_weights"].view(np.uint64))
+
+
+def test_oracle_not_located_on_halo_zero(golden):
+    z = golden("fallback_O32_O16_p4_h0")
+    S, T = sg.grid_from_name("O32"), sg.grid_from_name("O16")
+    dist = sg.blocks_partition(S, 4)
+    tdist = sg.matching_partition(T, S, dist)
+    for r in range(4):
+        mesh = sg.generate_mesh(S, dist, r, halo=0, include_pole=True)
+        owned = np.flatnonzero(tdist.part_of == r)
+        conn = mesh.element_connectivity
+        elem, _ = O.locate(mesh.node_xyz, conn.offsets, conn.indices, T.xyz()[owned])
+        bad = owned[elem < 0]
+        assert (bad[0] if len(bad) else -1) == int(z[f"r{r}_bad"])
+        assert np.array_equal(elem < 0, z[f"r{r}_fallback"])
+
+
+def test_oracle_halo_payloads_equal_reference_bytes(golden):
+    z = golden("part_O32_O16_p4_h2")
+    P = int(z["nparts"])
+    for r in range(P):
+        send = {p: z[f"r{r}_send_{p}"] for p in range(P) if f"r{r}_send_{p}" in z.files}
+        pay = O.halo_payloads(send, z[f"r{r}_before"])
+        for p, b in pay.items():
+            assert b == z[f"payload_{r}_{p}"].tobytes()
+    for r in range(P):
+        recv = {p: z[f"r{r}_recv_{p}"] for p in range(P) if f"r{r}_recv_{p}" in z.files}
+        pays = {p: z[f"payload_{p}_{r}"].tobytes() for p in recv}
+        out = O.halo_unpack(recv, z[f"r{r}_before"], pays)
+        assert np.array_equal(out.view(np.uint64), z[f"r{r}_after"].view(np.uint64))
+
+
+def test_oracle_matching_equals_reference(golden):
+    z = golden("matching")
+    for tgt, src in [("O16", "O32"), ("O40", "O80")]:
+        S, T = sg.grid_from_name(src), sg.grid_from_name(tgt)
+        idx = O.nearest_points(S.xyz(), T.xyz())
+        assert np.array_equal(idx, z[f"{tgt}_{src}_idx"])
+
+
+@pytest.mark.parametrize("n", [1, 2, 8, 16, 32])
+def test_oracle_gaussian_latitudes_equal_reference(golden, n):
+    z = golden("latitudes")
+    assert np.array_equal(O.gaussian_latitudes(n).view(np.uint64), z[f"n{n}"].view(np.uint64))
+
+
+def test_oracle_blocks_partition():
+    assert np.array_equal(O.blocks_partition(10, 3), sg.blocks_partition(sg.grid_from_name("F1"), 3).part_of[:0]
+                          if False else np.array([0, 0, 0, 0, 1, 1, 1, 2, 2, 2], np.int32))
