@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: O1280 -> O640 linear finite-element remap of a 137-level fp64
+field (BASELINE.json configs[2], the metric's configuration; it fits one B200).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One step = one execute of the remap over the whole configuration: at N=1 the apply kernel
+(interp.py:206-228 on the device); at N>1 (torchrun, one process per GPU, blocks_partition
++ matching_partition, mesh halo 2) the NodeColumns halo exchange of the source field (pack ->
+NCCL send/recv -> unpack) followed by the apply.  ``value`` is whole-job Gpts·lev/s with the
+inputs resident in HBM; ``e2e`` is the same metric through the public API
+(``apply_remap`` on host-resident fields in pinned memory: h2d of the source field, the
+kernel, d2h of the target field, every step).  Inputs (7.3 GB) exceed the 126 MB L2, so no
+flush is needed between steps.  ``--impl reference`` times the reference's CPU apply (the
+oracle port of interp.py:219-223, numpy, all host threads) on the same configuration.
+Synthetic data: level k of the field = Y_{l,m}(xyz)·(1 + k/L), (l, m) cycling through the 25
+real harmonics l <= 4.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (source, target, levels, fields)
+    "cfg3": ("O1280", "O640", 137, 1),
+    "cfg2": ("O320", "O160", 137, 4),
+    "cfg1": ("O32", "O16", 10, 1),
+}
+METRIC = "Gpts·lev/s O1280→O640 FE interp, 137 lev fp64"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config: str):
+    """dram bytes per launch of the apply kernel from the committed ncu summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_apply_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(config, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed regions."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.active = False
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self._t = threading.Thread(target=self._read, daemon=True)
+        self._t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            if self.active:
+                self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and "Active" in r[2 + i]
+                          and "Not" not in r[2 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def fill_smooth(out: np.ndarray, xyz: np.ndarray, field_index: int, rows=None) -> None:
+    """Synthetic analytic field into ``out`` (rows ``rows`` or all), in row chunks."""
+    from paper_1908_07038_b200.analytic import HARMONICS, spherical_harmonic
+
+    L = out.shape[1]
+    cols = [(field_index * L + k) % 25 for k in range(L)]
+    fac = 1.0 + np.arange(L) / L
+    idx = np.arange(len(xyz)) if rows is None else rows
+    for s in range(0, len(idx), 262144):
+        r = idx[s:s + 262144]
+        basis = np.stack([spherical_harmonic(l, m, xyz[r]) for l, m in HARMONICS], axis=1)
+        out[r] = basis[:, cols] * fac
+
+
+def setup_remap(sg, source, target, nparts, rank, ctx):
+    S, T = sg.grid_from_name(source), sg.grid_from_name(target)
+    dist = sg.blocks_partition(S, nparts)
+    mesh = sg.generate_mesh(S, dist, rank, halo=2, include_pole=True)  # cli.py:131
+    fs = sg.NodeColumns(mesh, ctx)
+    tdist = sg.matching_partition(T, S, dist)
+    w = sg.build_remap(fs, T, tdist, ctx)
+    return S, T, mesh, fs, tdist, w
+
+
+def cpu_apply(nodes, weights, src, out, nthreads):
+    """The reference's apply expression (interp.py:219-223) — the oracle port — over target
+    chunks on ``nthreads`` threads (numpy releases the GIL in gathers and ufuncs)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+
+    m = len(nodes)
+    chunk = 16384
+
+    def job(s):
+        sl = slice(s, min(s + chunk, m))
+        out[sl] = O.apply_remap(nodes[sl], weights[sl], src)
+
+    if nthreads <= 1:
+        for s in range(0, m, chunk):
+            job(s)
+        return
+    with ThreadPoolExecutor(nthreads) as ex:
+        list(ex.map(job, range(0, m, chunk)))
+
+
+def algorithmic_bytes(U, m, L, F):
+    """F·(U·L·8 + m·L·8) + m·(3·4 + 3·8)."""
+    return F * (U * L * 8 + m * L * 8) + m * 36
+
+
+# ------------------------------------------------------------------------------------------
+def run_reference(args):
+    """--impl reference: the reference's CPU apply on this host, all threads, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_1908_07038_b200 as sg
+
+    source, target, L, F = CONFIGS[args.config]
+    sg.set_device(0)
+    t0 = time.time()
+    # stencils: built once on the GPU (untimed setup; at cfg3 the CPU apply
+    # runs on the new build's stencils, verified bit-exact against the reference's locate)
+    S, T, mesh, fs, tdist, w = setup_remap(sg, source, target, 1, 0, None)
+    nodes, weights = w.nodes, w.weights
+    srcs = []
+    for f in range(F):
+        a = np.empty((mesh.nb_nodes, L))
+        fill_smooth(a, mesh.node_xyz, f)
+        srcs.append(a)
+    out = np.empty((len(w), L))
+    nthreads = os.cpu_count() or 1
+    log(f"reference setup {time.time() - t0:.1f}s, {nthreads} threads")
+    for _ in range(args.warmup):
+        for a in srcs:
+            cpu_apply(nodes, weights, a, out, nthreads)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        for a in srcs:
+            cpu_apply(nodes, weights, a, out, nthreads)
+        times.append(time.perf_counter() - t)
+    units = len(w) * L * F
+    ms = 1e3 * sum(times) / len(times)
+    value = units / (ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "Gpts·lev/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
+        "impl": "reference",
+        "config": {"workload": f"{source}->{target} FE remap apply, {L} levels x {F} field(s), P=1",
+                   "levels": L, "fields": F, "targets": len(w), "source_nodes": mesh.nb_nodes},
+        "cpu_baseline": {"value": value, "unit": "Gpts·lev/s", "cores": nthreads, "kind": "port",
+                         "sample": f"full {source}->{target} apply per step (oracle port of interp.py:219-223, "
+                                   f"numpy, {nthreads} threads over 16k-target chunks)"},
+        "e2e": {"value": value, "unit": "Gpts·lev/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+def run_single(args):
+    import paper_1908_07038_b200 as sg
+    from paper_1908_07038_b200.device import DeviceArray, Event, PinnedArray
+
+    source, target, L, F = CONFIGS[args.config]
+    dev = 0
+    sg.set_device(dev)
+    t0 = time.time()
+    S, T, mesh, fs, tdist, w = setup_remap(sg, source, target, 1, 0, None)
+    m, n = len(w), mesh.nb_nodes
+    U = w.distinct_sources()
+    log(f"setup {time.time() - t0:.1f}s: {n} source nodes, {m} targets, U={U}")
+    # host inputs in pinned memory (also the e2e inputs)
+    hsrc = [PinnedArray((n, L)) for _ in range(F)]
+    hdst = [PinnedArray((m, L)) for _ in range(F)]
+    for f in range(F):
+        fill_smooth(hsrc[f].array, mesh.node_xyz, f)
+    dsrc = [DeviceArray(n, L, np.float64) for _ in range(F)]
+    ddst = [DeviceArray(m, L, np.float64) for _ in range(F)]
+    for f in range(F):
+        dsrc[f].upload(hsrc[f].array)
+    log(f"inputs ready {time.time() - t0:.1f}s")
+
+    clocks = ClockSampler(dev)
+    clocks.start()
+    # ---- device-resident timing: one apply launch per step, events around every launch ----
+    for _ in range(args.warmup):
+        sg.apply_remap_device(w, dsrc, ddst, variant=args.variant)
+    sg.synchronize(dev)
+    ev = [Event(dev) for _ in range(args.steps + 1)]
+    clocks.active = True
+    ev[0].record()
+    for k in range(args.steps):
+        sg.apply_remap_device(w, dsrc, ddst, variant=args.variant)
+        ev[k + 1].record()
+    sg.synchronize(dev)
+    launch_ms = [Event.elapsed_ms(ev[k], ev[k + 1]) for k in range(args.steps)]
+    total_ms = Event.elapsed_ms(ev[0], ev[-1])
+    clocks.active = False
+    ms = total_ms / args.steps
+    units = m * L * F
+    value = units / (ms * 1e-3) / 1e9
+    # parity spot check of the timed output against the oracle (not timed)
+    from oracle import oracle as O
+
+    samp = np.random.default_rng(7).choice(m, size=min(m, 4096), replace=False)
+    got = ddst[0].to_numpy()[samp]
+    exp = O.apply_remap(w.nodes[samp], w.weights[samp], hsrc[0].array)
+    bitwise = bool(np.array_equal(got.view(np.uint64), exp.view(np.uint64)))
+
+    # ---- e2e through the public API: host fields in pinned memory -------------------------
+    fsrc = [sg.Field(name=f"src{f}", shape=(n, L), kind=sg.Kind.REAL64, host=hsrc[f].array) for f in range(F)]
+    fdst = [sg.Field(name=f"dst{f}", shape=(m, L), kind=sg.Kind.REAL64, host=hdst[f].array) for f in range(F)]
+    e2e_steps = max(3, min(args.steps, 10))
+    for f in range(F):
+        sg.apply_remap(w, fsrc[f], fdst[f])  # warm (staging buffers)
+    clocks.active = True
+    t = time.perf_counter()
+    for _ in range(e2e_steps):
+        for f in range(F):
+            sg.apply_remap(w, fsrc[f], fdst[f])
+    e2e_s = (time.perf_counter() - t) / e2e_steps
+    clocks.active = False
+    clocks.stop()
+    e2e_ok = bool(np.array_equal(hdst[0].array[samp].view(np.uint64), exp.view(np.uint64)))
+
+    # ---- CPU baseline: the reference's apply (oracle port), 1 thread, same workload --------
+    cpu = None
+    if not args.no_cpu_baseline:
+        out = np.empty((m, L))
+        times = []
+        for _ in range(2):
+            tt = time.perf_counter()
+            for f in range(F):
+                cpu_apply(w.nodes, w.weights, hsrc[f].array, out, 1)
+            times.append(time.perf_counter() - tt)
+        cpu = {"value": units / min(times) / 1e9, "unit": "Gpts·lev/s", "cores": 1, "kind": "port",
+               "sample": f"full {source}->{target} apply x{F} field(s), best of 2 (numpy expression of "
+                         f"interp.py:219-223, single-threaded like the reference)"}
+
+    peak, peak_src = measured_peak()
+    B = algorithmic_bytes(U, m, L, F)
+    kern_ms = statistics.mean(launch_ms)
+    achieved = B / (kern_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "Gpts·lev/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
+        "config": {"workload": f"{source}->{target} FE remap apply, {L} levels x {F} field(s), P=1",
+                   "levels": L, "fields": F, "targets": m, "source_nodes": n, "distinct_sources": U,
+                   "parallelism": "single GPU", "l2": "inputs 7.3 GB > 126 MB L2 (no flush needed)",
+                   "variant": args.variant},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic(args.config), "algorithmic_bytes_per_launch": B,
+                     "kernel_ms": kern_ms, "peak_source": peak_src},
+        "e2e": {"value": units / e2e_s / 1e9, "unit": "Gpts·lev/s", "h2d_bytes_per_step": n * L * 8 * F,
+                "d2h_bytes_per_step": m * L * 8 * F, "ms_per_step": e2e_s * 1e3,
+                "api": "paper_1908_07038_b200.apply_remap(weights, host Field, host Field)"},
+        "cpu_baseline": cpu,
+        "gpu_launches": args.steps,
+        "parity": {"apply_bitwise_vs_oracle_sample": bitwise, "e2e_bitwise": e2e_ok},
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+def run_multi(args):
+    """N > 1: one process per GPU (torchrun), halo exchange + apply per step."""
+    import torch.distributed as dist
+
+    import paper_1908_07038_b200 as sg
+    from paper_1908_07038_b200.device import DeviceArray, Event
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    os.environ.setdefault("GLOO_SOCKET_IFNAME", "lo")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sg.set_device(local)
+    ctx = sg.DistContext(device=local)
+    source, target, L, F = CONFIGS[args.config]
+    t0 = time.time()
+    S, T, mesh, fs, tdist, w = setup_remap(sg, source, target, world, rank, ctx)
+    m, n = len(w), mesh.nb_nodes
+    f = fs.create_field("src", levels=L)
+    owned = fs.owned_row_index()
+    fill_smooth(f.host, mesh.node_xyz, 0, rows=owned)
+    f.allocate_device()
+    tf = sg.StructuredColumns(T, tdist, rank).create_field("dst", levels=L).allocate_device()
+    plan = fs.exchange_plan
+    ctx.nccl_comm()
+    log(f"rank {rank}: setup {time.time() - t0:.1f}s, {n} nodes, {m} targets, "
+        f"{sum(len(v) for v in plan.recv.values())} ghosts")
+
+    def step():
+        plan.exchange_nccl(f.device, ctx.nccl_comm(), 0)
+        sg.apply_remap_device(w, [f.device], [tf.device], variant=args.variant)
+
+    for _ in range(args.warmup):
+        step()
+    sg.synchronize(local)
+    clocks = ClockSampler(local) if rank == 0 else None
+    if clocks:
+        clocks.start()
+        clocks.active = True
+    ctx.barrier()
+    e0, e1 = Event(local), Event(local)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    sg.synchronize(local)
+    my_ms = Event.elapsed_ms(e0, e1)
+    ctx.barrier()
+    import torch
+
+    t = torch.tensor([my_ms, float(m)], dtype=torch.float64)
+    tmax = t.clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    tsum = t.clone()
+    dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+    # halo-only timing (bytes over NVLink)
+    ctx.barrier()
+    h0, h1 = Event(local), Event(local)
+    h0.record()
+    for _ in range(args.steps):
+        plan.exchange_nccl(f.device, ctx.nccl_comm(), 0)
+    h1.record()
+    sg.synchronize(local)
+    hb = torch.tensor([Event.elapsed_ms(h0, h1) / args.steps,
+                       float(sum(len(v) for v in plan.send.values()) * L * 8)], dtype=torch.float64)
+    hmax = hb.clone()
+    dist.all_reduce(hmax, op=dist.ReduceOp.MAX)
+    hsum = hb.clone()
+    dist.all_reduce(hsum, op=dist.ReduceOp.SUM)
+    if clocks:
+        clocks.active = False
+        clocks.stop()
+    if rank == 0:
+        ms = float(tmax[0]) / args.steps
+        units = float(tsum[1]) * L
+        value = units / (ms * 1e-3) / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gpts·lev/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
+            "config": {"workload": f"{source}->{target} FE remap, {L} levels, blocks_partition P={world}, halo 2, "
+                                   "halo exchange + apply per step", "levels": L, "parallelism": f"domain x{world}",
+                       "l2": "inputs > L2"},
+            "halo": {"bytes_per_exchange": float(hsum[1]), "ms": float(hmax[0]),
+                     "GB_per_s": float(hsum[1]) / (float(hmax[0]) * 1e-3) / 1e9},
+            "gpu_launches": 3 * args.steps,
+            "clocks": clocks.summary() if clocks else None,
+            "e2e": None,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.barrier()
+    dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--variant", type=int, default=0, help="apply kernel: 0 default, 1 warp LDG, 2 TMA bulk")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (timing rule)")
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return run_multi(args)
+    return run_single(args)
+
+
+if __name__ == "__main__":
+    main()

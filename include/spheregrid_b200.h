@@ -46,10 +46,9 @@ int32_t sg_device_count(int32_t* out_count);
 int32_t sg_stream_synchronize(int32_t device, uint64_t stream);
 
 /* ---- Field device mirror (field.py:77-162) ---------------------------------------------
- * Device storage of a (npts, levels) Field: one pitched allocation, levels contiguous per
- * point (the reference host layout, field.py:161), row pitch padded to 128 B (or to the
- * next power of two for rows < 128 B) so 16-B vector loads and bulk copies are aligned.
- * Padding is zero-filled at allocation.
+ * Device storage of a (npts, levels) Field: one allocation, levels contiguous per point,
+ * dense rows (pitch == levels: the reference host layout, field.py:161).  The pitch is
+ * returned so callers never assume it.
  *   sg_field_alloc  <- Field.allocate_device        (field.py:99-105)
  *   sg_field_h2d    <- Field.update_device           (field.py:134-140)   host rows unpadded
  *   sg_field_d2h    <- Field.update_host             (field.py:126-132)
@@ -112,11 +111,25 @@ int32_t sg_stencil_info(uint64_t stencil, int64_t* out_m, int64_t* out_source_nn
  * rounded separately (bitwise equal to the numpy expression at interp.py:219-223), for
  * nfields source/target field pairs sharing the stencil.  ShapeMismatch (status 1) with
  * the reference messages when npts / levels disagree (interp.py:208-217).
- * variant: 0 = default, 1 = warp-per-target LDG.128 gather, 2 = TMA bulk-copy
- * (cp.async.bulk) staged gather.                                                            */
+ * variant: 0 = default (warp per target, vector loads), 2 = TMA bulk-copy (cp.async.bulk)
+ * staged gather with a producer warp, 3 = warp per target, 8-B loads.                                                            */
 int32_t sg_remap_apply(uint64_t stencil, const uint64_t* src_fields,
                        const uint64_t* dst_fields, int32_t nfields, int32_t variant,
                        uint64_t stream);
+/* The same for targets [t0, t1) only (pipelines, overlap of interior/boundary targets). */
+int32_t sg_remap_apply_range(uint64_t stencil, const uint64_t* src_fields,
+                             const uint64_t* dst_fields, int32_t nfields, int64_t t0,
+                             int64_t t1, int32_t variant, uint64_t stream);
+/* apply_remap with HOST buffers (the reference's call shape, interp.py:206-228): host
+ * source rows -> device, apply, device -> host target rows, as an nchunks-deep pipeline
+ * on three streams (h2d of source-row chunk c, apply of the targets whose stencils lie in
+ * chunks <= c, d2h of those target rows).  Only source rows the stencil references are
+ * copied (*out_rows_copied).  host_src/host_dst: dense (npts, levels) C-order fp64, ideally
+ * pinned (sg_host_alloc).  Synchronous: returns when host_dst holds the result. */
+int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields,
+                              const uint64_t* dst_fields, int32_t nfields,
+                              const uint64_t* host_src, const uint64_t* host_dst,
+                              int32_t nchunks, int32_t variant, int64_t* out_rows_copied);
 
 /* ---- halo exchange (functionspace.py:58-118) ---------------------------------------------
  * sg_halo_plan_create <- HaloExchangePlan (functionspace.py:47-55): per peer (ascending),

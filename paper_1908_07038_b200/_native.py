@@ -49,6 +49,8 @@ _SIGS = {
     "sg_stencil_create": [i32, vp, vp, i64, i64, vp],
     "sg_stencil_info": [u64, vp, vp, vp],
     "sg_remap_apply": [u64, vp, vp, i32, i32, u64],
+    "sg_remap_apply_range": [u64, vp, vp, i32, i64, i64, i32, u64],
+    "sg_remap_execute_host": [u64, vp, vp, i32, vp, vp, i32, i32, vp],
     "sg_halo_plan_create": [i32, i64, i32, vp, vp, vp, vp, vp, vp, vp],
     "sg_halo_plan_info": [u64, vp, vp],
     "sg_halo_pack": [u64, u64, vp, u64],

@@ -6,17 +6,22 @@
 // rounded exactly like numpy's evaluation of interp.py:219-223 (three separately rounded
 // products, two separately rounded adds: __dmul_rn / __dadd_rn are never FMA-contracted).
 //
-// Two kernels:
-//  * variant 1 (default): one warp per target row.  Lanes span the level dimension with
-//    16-B (double2) loads; every lane issues all of its 3 x ITERS row loads before the
-//    arithmetic so ~9 independent 16-B requests per lane are in flight.  Source rows have
-//    no reuse (U/m ≈ 3.0), so loads bypass L1 (ld.global.nc.L1::no_allocate)
-//    and stores stream (st.global.cs).
-//  * variant 2: TMA bulk copies.  A persistent CTA per SM slot walks tiles of TILE targets;
-//    one elected thread issues cp.async.bulk (global -> shared, mbarrier complete_tx) for
-//    the 3*TILE referenced source rows of a tile into a STAGES-deep ring, the CTA computes
-//    from shared memory and streams the rows out.
+// Kernels (all take a target range [t0, t1) so a host pipeline can run chunks):
+//  * warp per target (default).  Lanes span the level dimension; every lane issues all of
+//    its 3 x ITERS row loads before the arithmetic (9-15 independent loads in flight per
+//    lane).  16-B loads when rows are 16-B aligned (even pitch), 8-B loads otherwise (dense
+//    137-level rows).  Source rows have no reuse (U/m ≈ 3.0): loads bypass
+//    L1 (ld.global.nc.L1::no_allocate), stores stream (st.global.cs).
+//  * TMA bulk (variant 2): a producer warp issues cp.async.bulk global->shared copies of the
+//    3 rows of each target of a tile (16-B aligned superset of every row, so any pitch
+//    works) into a STAGES-deep ring guarded by full/empty mbarriers; 8 consumer warps (one
+//    target each) compute from shared memory and stream the rows out.
+//  * thread per target for levels <= 8.
+// sg_remap_execute_host pipelines host->device copies of source-row chunks, the apply of the
+// targets whose stencils are complete, and device->host copies of their rows on three
+// streams, and copies only source rows the stencil references.
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "stencil.cuh"
@@ -29,7 +34,7 @@ constexpr int kMaxFields = 8;
 struct ApplyArgs {
   const int4* idx;
   const double4* w;
-  int64_t m;
+  int64_t t0, t1;  // target range
   int32_t levels;
   int32_t nfields;
   const double* src[kMaxFields];
@@ -40,9 +45,7 @@ struct ApplyArgs {
 
 __device__ __forceinline__ double2 ldg_stream2(const double2* p) {
   double2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
-               : "=d"(v.x), "=d"(v.y)
-               : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
 __device__ __forceinline__ double ldg_stream1(const double* p) {
@@ -50,33 +53,31 @@ __device__ __forceinline__ double ldg_stream1(const double* p) {
   asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
-
 __device__ __forceinline__ double4 ldg_w4(const double4* p) {
   const double2* q = reinterpret_cast<const double2*>(p);
   const double2 a = __ldg(q), b = __ldg(q + 1);
   return make_double4(a.x, a.y, b.x, b.y);
 }
-
-__device__ __forceinline__ double combine(double w0, double w1, double w2, double a, double b,
-                                          double c) {
+__device__ __forceinline__ double combine(double w0, double w1, double w2, double a, double b, double c) {
   // numpy: (w0*a + w1*b) + w2*c, each op rounded (interp.py:219-223)
   return __dadd_rn(__dadd_rn(__dmul_rn(w0, a), __dmul_rn(w1, b)), __dmul_rn(w2, c));
 }
 
-// ---- variant 1: warp per target, 16-B vector loads over levels --------------------------
+// ---- warp per target, 16-B loads (even pitch) ------------------------------------------------
 template <int ITERS>
 __global__ void __launch_bounds__(256) apply_warp_v2(ApplyArgs a) {
   const int lane = threadIdx.x & 31;
-  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (t >= a.m) return;
+  const int64_t t = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (t >= a.t1) return;
   const int4 id = __ldg(a.idx + t);
   const double4 wt = ldg_w4(a.w + t);
-  const int nvec = (a.levels + 1) >> 1;  // pitch is even, padding is zero
+  const int nvec = (a.levels + 1) >> 1;  // even pitch: the pad element of an odd row exists
+  const bool odd = a.levels & 1;
   for (int f = 0; f < a.nfields; ++f) {
     const double2* r0 = reinterpret_cast<const double2*>(a.src[f] + (int64_t)id.x * a.src_pitch[f]);
     const double2* r1 = reinterpret_cast<const double2*>(a.src[f] + (int64_t)id.y * a.src_pitch[f]);
     const double2* r2 = reinterpret_cast<const double2*>(a.src[f] + (int64_t)id.z * a.src_pitch[f]);
-    double2* out = reinterpret_cast<double2*>(a.dst[f] + t * a.dst_pitch[f]);
+    double* outp = a.dst[f] + t * a.dst_pitch[f];
     double2 v0[ITERS], v1[ITERS], v2[ITERS];
 #pragma unroll
     for (int i = 0; i < ITERS; ++i) {
@@ -94,51 +95,84 @@ __global__ void __launch_bounds__(256) apply_warp_v2(ApplyArgs a) {
         double2 o;
         o.x = combine(wt.x, wt.y, wt.z, v0[i].x, v1[i].x, v2[i].x);
         o.y = combine(wt.x, wt.y, wt.z, v0[i].y, v1[i].y, v2[i].y);
-        __stcs(out + k, o);
+        if (odd && k == nvec - 1)
+          __stcs(outp + 2 * k, o.x);  // never touch the next row
+        else
+          __stcs(reinterpret_cast<double2*>(outp) + k, o);
       }
     }
   }
 }
 
-// Generic fallback: any pitch (odd, e.g. levels == 1), scalar loads, looped over levels.
-__global__ void __launch_bounds__(256) apply_warp_scalar(ApplyArgs a) {
+// ---- warp per target, 8-B loads (any pitch; dense odd rows) ----------------------------------
+template <int ITERS>
+__global__ void __launch_bounds__(256) apply_warp_v1(ApplyArgs a) {
   const int lane = threadIdx.x & 31;
-  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (t >= a.m) return;
+  const int64_t t = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (t >= a.t1) return;
+  const int4 id = __ldg(a.idx + t);
+  const double4 wt = ldg_w4(a.w + t);
+  const int L = a.levels;
+  for (int f = 0; f < a.nfields; ++f) {
+    const double* r0 = a.src[f] + (int64_t)id.x * a.src_pitch[f];
+    const double* r1 = a.src[f] + (int64_t)id.y * a.src_pitch[f];
+    const double* r2 = a.src[f] + (int64_t)id.z * a.src_pitch[f];
+    double* outp = a.dst[f] + t * a.dst_pitch[f];
+    double v0[ITERS], v1[ITERS], v2[ITERS];
+#pragma unroll
+    for (int i = 0; i < ITERS; ++i) {
+      const int k = lane + 32 * i;
+      if (k < L) {
+        v0[i] = ldg_stream1(r0 + k);
+        v1[i] = ldg_stream1(r1 + k);
+        v2[i] = ldg_stream1(r2 + k);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < ITERS; ++i) {
+      const int k = lane + 32 * i;
+      if (k < L) __stcs(outp + k, combine(wt.x, wt.y, wt.z, v0[i], v1[i], v2[i]));
+    }
+  }
+}
+
+// Any number of levels (> 256): looped.
+__global__ void __launch_bounds__(256) apply_warp_loop(ApplyArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (t >= a.t1) return;
   const int4 id = __ldg(a.idx + t);
   const double4 wt = ldg_w4(a.w + t);
   for (int f = 0; f < a.nfields; ++f) {
     const double* r0 = a.src[f] + (int64_t)id.x * a.src_pitch[f];
     const double* r1 = a.src[f] + (int64_t)id.y * a.src_pitch[f];
     const double* r2 = a.src[f] + (int64_t)id.z * a.src_pitch[f];
-    double* out = a.dst[f] + t * a.dst_pitch[f];
+    double* outp = a.dst[f] + t * a.dst_pitch[f];
     for (int l = lane; l < a.levels; l += 32)
-      __stcs(out + l, combine(wt.x, wt.y, wt.z, ldg_stream1(r0 + l), ldg_stream1(r1 + l),
-                              ldg_stream1(r2 + l)));
+      __stcs(outp + l, combine(wt.x, wt.y, wt.z, ldg_stream1(r0 + l), ldg_stream1(r1 + l), ldg_stream1(r2 + l)));
   }
 }
 
-// Thread-per-target variant for few levels (levels <= 8): a warp covers 32 targets, so the
-// stencil loads coalesce and each lane walks its target's short rows.
+// Thread per target for few levels (levels <= 8): the stencil loads of a warp coalesce.
 __global__ void __launch_bounds__(256) apply_thread_short(ApplyArgs a) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= a.m) return;
+  const int64_t t = a.t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.t1) return;
   const int4 id = __ldg(a.idx + t);
   const double4 wt = ldg_w4(a.w + t);
   for (int f = 0; f < a.nfields; ++f) {
     const double* r0 = a.src[f] + (int64_t)id.x * a.src_pitch[f];
     const double* r1 = a.src[f] + (int64_t)id.y * a.src_pitch[f];
     const double* r2 = a.src[f] + (int64_t)id.z * a.src_pitch[f];
-    double* out = a.dst[f] + t * a.dst_pitch[f];
+    double* outp = a.dst[f] + t * a.dst_pitch[f];
     for (int l = 0; l < a.levels; ++l)
-      out[l] = combine(wt.x, wt.y, wt.z, __ldg(r0 + l), __ldg(r1 + l), __ldg(r2 + l));
+      outp[l] = combine(wt.x, wt.y, wt.z, __ldg(r0 + l), __ldg(r1 + l), __ldg(r2 + l));
   }
 }
 
-// ---- variant 2: TMA bulk-copy staged gather ------------------------------------------------
-constexpr int kTile = 8;     // targets per tile
-constexpr int kStages = 4;   // ring depth
-constexpr int kV2Threads = 256;
+// ---- TMA bulk-copy staged gather ---------------------------------------------------------------
+constexpr int kTile = 8;  // targets per tile == consumer warps
+constexpr int kConsumerWarps = kTile;
+constexpr int kBulkThreads = (kConsumerWarps + 1) * 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -147,9 +181,11 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -160,91 +196,89 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst_smem)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
-// smem ring: [kStages][3*kTile rows][row_elems]; one work item = (tile, field)
-__global__ void __launch_bounds__(kV2Threads) apply_bulk(ApplyArgs a, int row_elems,
-                                                         uint32_t row_bytes) {
+// smem: ring of `stages` stages x 3*kTile row slots of `slot` doubles; each slot holds the
+// 16-B aligned superset of one source row (the row starts at element off = addr%16/8).
+__global__ void __launch_bounds__(kBulkThreads) apply_bulk(ApplyArgs a, int slot, int stages) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ uint64_t full_bar[kStages];
-  double* ring = reinterpret_cast<double*>(smem_raw);
-  const size_t stage_elems = (size_t)3 * kTile * row_elems;
-  const int64_t ntiles = (a.m + kTile - 1) / kTile;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + stages;
+  unsigned char* offs = reinterpret_cast<unsigned char*>(empty + stages);  // [stages][3*kTile]
+  double* ring = reinterpret_cast<double*>(smem_raw + ((16 * stages + 3 * kTile * stages + 127) / 128) * 128);
+  const int64_t ntiles = (a.t1 - a.t0 + kTile - 1) / kTile;
   const int64_t nwork = ntiles * a.nfields;  // work item = (tile, field)
-  const int64_t first = blockIdx.x;
-  const int64_t stride = gridDim.x;
-
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-
-  auto issue = [&](int64_t item, int stage) {
-    const int64_t tile = item / a.nfields;
-    const int f = (int)(item % a.nfields);
-    const int64_t t0 = tile * kTile;
-    const int nt = (int)(a.m - t0 < kTile ? a.m - t0 : kTile);
-    mbar_expect_tx(&full_bar[stage], (uint32_t)(3 * nt) * row_bytes);
-    double* base = ring + stage * stage_elems;
-    for (int j = 0; j < nt; ++j) {
-      const int4 id = __ldg(a.idx + t0 + j);
-      bulk_g2s(base + (3 * j + 0) * row_elems, a.src[f] + (int64_t)id.x * a.src_pitch[f], row_bytes,
-               &full_bar[stage]);
-      bulk_g2s(base + (3 * j + 1) * row_elems, a.src[f] + (int64_t)id.y * a.src_pitch[f], row_bytes,
-               &full_bar[stage]);
-      bulk_g2s(base + (3 * j + 2) * row_elems, a.src[f] + (int64_t)id.z * a.src_pitch[f], row_bytes,
-               &full_bar[stage]);
-    }
-  };
-
-  // prologue: fill the ring
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      const int64_t item = first + s * stride;
-      if (item < nwork) issue(item, s);
-    }
-  }
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int nvec = (a.levels + 1) >> 1;
-  int it = 0;
-  for (int64_t item = first; item < nwork; item += stride, ++it) {
-    const int stage = it % kStages;
-    const uint32_t parity = (it / kStages) & 1;
-    mbar_wait(&full_bar[stage], parity);
-    const int64_t tile = item / a.nfields;
-    const int f = (int)(item % a.nfields);
-    const int64_t t0 = tile * kTile;
-    const int nt = (int)(a.m - t0 < kTile ? a.m - t0 : kTile);
-    const double* base = ring + stage * stage_elems;
-    // warp j handles target j of the tile (kV2Threads/32 == kTile)
-    if (warp < nt) {
-      const double4 wt = ldg_w4(a.w + t0 + warp);
-      const double2* r0 = reinterpret_cast<const double2*>(base + (3 * warp + 0) * row_elems);
-      const double2* r1 = reinterpret_cast<const double2*>(base + (3 * warp + 1) * row_elems);
-      const double2* r2 = reinterpret_cast<const double2*>(base + (3 * warp + 2) * row_elems);
-      double2* out = reinterpret_cast<double2*>(a.dst[f] + (t0 + warp) * a.dst_pitch[f]);
-      for (int k = lane; k < nvec; k += 32) {
-        const double2 x = r0[k], y = r1[k], z = r2[k];
-        double2 o;
-        o.x = combine(wt.x, wt.y, wt.z, x.x, y.x, z.x);
-        o.y = combine(wt.x, wt.y, wt.z, x.y, y.y, z.y);
-        __stcs(out + k, o);
+  if (warp == kConsumerWarps) {
+    // ===== producer warp: lane j loads target j's stencil and issues its 3 row copies =====
+    int it = 0;
+    for (int64_t item = blockIdx.x; item < nwork; item += gridDim.x, ++it) {
+      const int stage = it % stages;
+      if (it >= stages) mbar_wait(&empty[stage], ((it / stages) - 1) & 1);
+      const int64_t tile = item / a.nfields;
+      const int f = (int)(item % a.nfields);
+      const int64_t tb = a.t0 + tile * kTile;
+      const int nt = (int)min((int64_t)kTile, a.t1 - tb);
+      uint32_t bytes[3] = {0, 0, 0};
+      const double* rows[3] = {nullptr, nullptr, nullptr};
+      if (lane < nt) {
+        const int4 id = __ldg(a.idx + tb + lane);
+        const int ids[3] = {id.x, id.y, id.z};
+        for (int c = 0; c < 3; ++c) {
+          const double* r = a.src[f] + (int64_t)ids[c] * a.src_pitch[f];
+          const uintptr_t p = reinterpret_cast<uintptr_t>(r);
+          const uintptr_t s0 = p & ~uintptr_t(15), s1 = (p + (uintptr_t)a.levels * 8 + 15) & ~uintptr_t(15);
+          rows[c] = reinterpret_cast<const double*>(s0);
+          bytes[c] = (uint32_t)(s1 - s0);
+          offs[stage * 3 * kTile + 3 * lane + c] = (unsigned char)((p - s0) >> 3);
+        }
+      }
+      uint32_t total = bytes[0] + bytes[1] + bytes[2];
+      for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+      if (lane == 0) mbar_expect_tx(&full[stage], total);
+      __syncwarp();
+      if (lane < nt) {
+        double* base = ring + (size_t)stage * 3 * kTile * slot;
+        for (int c = 0; c < 3; ++c) bulk_g2s(base + (3 * lane + c) * slot, rows[c], bytes[c], &full[stage]);
       }
     }
-    __syncthreads();  // stage fully consumed
-    if (threadIdx.x == 0) {
-      const int64_t next = item + (int64_t)kStages * stride;
-      if (next < nwork) issue(next, stage);
+    return;
+  }
+  // ===== consumer warps: warp j computes target j of the tile =====
+  int it = 0;
+  for (int64_t item = blockIdx.x; item < nwork; item += gridDim.x, ++it) {
+    const int stage = it % stages;
+    mbar_wait(&full[stage], (it / stages) & 1);
+    const int64_t tile = item / a.nfields;
+    const int f = (int)(item % a.nfields);
+    const int64_t tb = a.t0 + tile * kTile;
+    const int nt = (int)min((int64_t)kTile, a.t1 - tb);
+    if (warp < nt) {
+      const int64_t t = tb + warp;
+      const double4 wt = ldg_w4(a.w + t);
+      const double* base = ring + (size_t)stage * 3 * kTile * slot;
+      const unsigned char* o = offs + stage * 3 * kTile + 3 * warp;
+      const double* r0 = base + (3 * warp + 0) * slot + o[0];
+      const double* r1 = base + (3 * warp + 1) * slot + o[1];
+      const double* r2 = base + (3 * warp + 2) * slot + o[2];
+      double* outp = a.dst[f] + t * a.dst_pitch[f];
+      for (int l = lane; l < a.levels; l += 32) __stcs(outp + l, combine(wt.x, wt.y, wt.z, r0[l], r1[l], r2[l]));
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
   }
 }
 
@@ -258,36 +292,224 @@ __global__ void mark_sources(const int4* idx, int64_t m, unsigned char* mark) {
 }
 
 __global__ void count_marks(const unsigned char* mark, int64_t n, unsigned long long* out) {
-  __shared__ unsigned long long s;
-  if (threadIdx.x == 0) s = 0;
-  __syncthreads();
   unsigned long long c = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     c += mark[i];
-  atomicAdd(&s, c);
-  __syncthreads();
-  if (threadIdx.x == 0) atomicAdd(out, s);
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, c);
 }
 
-__global__ void pack_stencil(const int32_t* idx3, const double* w3, int64_t m, int4* idx,
-                             double4* w) {
+__global__ void pack_stencil(const int32_t* idx3, const double* w3, int64_t m, int4* idx, double4* w) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= m) return;
   idx[t] = make_int4(idx3[3 * t], idx3[3 * t + 1], idx3[3 * t + 2], 0);
   w[t] = make_double4(w3[3 * t], w3[3 * t + 1], w3[3 * t + 2], 0.0);
 }
 
-int g_num_sms = 0;
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+// Launches the apply of targets [t0, t1) for up to kMaxFields field pairs.
+void launch_apply(ApplyArgs a, int variant, cudaStream_t st) {
+  const int64_t m = a.t1 - a.t0;
+  if (m <= 0) return;
+  const int L = a.levels;
+  bool even = true;
+  for (int f = 0; f < a.nfields; ++f) even = even && a.src_pitch[f] % 2 == 0 && a.dst_pitch[f] % 2 == 0;
+  if (variant == 2 && L >= 2) {
+    const int slot = ((L + 2) * 8 + 15) / 16 * 2;  // doubles; holds the 16-B aligned superset
+    const size_t stage_bytes = (size_t)3 * kTile * slot * 8;
+    const int stages = (int)std::min<size_t>(8, std::max<size_t>(2, (size_t)(100 * 1024) / stage_bytes));
+    const size_t hdr = ((16 * stages + 3 * kTile * stages + 127) / 128) * 128;
+    const size_t smem = hdr + stages * stage_bytes;
+    SG_REQUIRE(smem <= 220 * 1024, "levels too large for the bulk-copy variant");
+    SG_CUDA(cudaFuncSetAttribute(apply_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_bulk, kBulkThreads, smem));
+    const int64_t nwork = (m + kTile - 1) / kTile * a.nfields;
+    const int64_t grid = std::min<int64_t>((int64_t)num_sms() * std::max(per_sm, 1), nwork);
+    apply_bulk<<<(unsigned)grid, kBulkThreads, smem, st>>>(a, slot, stages);
+  } else if (L <= 8) {
+    apply_thread_short<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(a);
+  } else {
+    const unsigned grid = (unsigned)((m + 7) / 8);  // 8 warps per block, warp per target
+    const int nv = (L + 1) / 2;
+    if (even && variant != 3) {
+      switch (nv <= 32 ? 1 : nv <= 64 ? 2 : nv <= 96 ? 3 : nv <= 128 ? 4 : 0) {
+        case 1: apply_warp_v2<1><<<grid, 256, 0, st>>>(a); break;
+        case 2: apply_warp_v2<2><<<grid, 256, 0, st>>>(a); break;
+        case 3: apply_warp_v2<3><<<grid, 256, 0, st>>>(a); break;
+        case 4: apply_warp_v2<4><<<grid, 256, 0, st>>>(a); break;
+        default: apply_warp_loop<<<grid, 256, 0, st>>>(a); break;
+      }
+    } else {
+      switch ((L + 31) / 32) {
+        case 1: apply_warp_v1<1><<<grid, 256, 0, st>>>(a); break;
+        case 2: apply_warp_v1<2><<<grid, 256, 0, st>>>(a); break;
+        case 3: apply_warp_v1<3><<<grid, 256, 0, st>>>(a); break;
+        case 4: apply_warp_v1<4><<<grid, 256, 0, st>>>(a); break;
+        case 5: apply_warp_v1<5><<<grid, 256, 0, st>>>(a); break;
+        case 6: apply_warp_v1<6><<<grid, 256, 0, st>>>(a); break;
+        case 7: apply_warp_v1<7><<<grid, 256, 0, st>>>(a); break;
+        case 8: apply_warp_v1<8><<<grid, 256, 0, st>>>(a); break;
+        default: apply_warp_loop<<<grid, 256, 0, st>>>(a); break;
+      }
+    }
+  }
+  SG_CUDA_LAUNCH();
+}
+
+struct FieldPairs {
+  std::vector<Field*> src, dst;
+  int32_t levels = -1;
+};
+
+FieldPairs check_pairs(const Stencil* s, const uint64_t* src_fields, const uint64_t* dst_fields, int nfields) {
+  SG_REQUIRE(nfields >= 1, "nfields must be >= 1");
+  SG_REQUIRE(src_fields && dst_fields, "null field arrays");
+  FieldPairs p;
+  p.src.resize(nfields);
+  p.dst.resize(nfields);
+  for (int f = 0; f < nfields; ++f) {
+    Field* a = p.src[f] = get<Field>(src_fields[f], ObjKind::Field);
+    Field* b = p.dst[f] = get<Field>(dst_fields[f], ObjKind::Field);
+    // exact reference messages, interp.py:208-217
+    if (a->npts != s->source_nnodes)
+      throw_error(SG_DOMAIN_ERROR, "ShapeMismatch: source field has %lld points, weights expect %lld",
+                  (long long)a->npts, (long long)s->source_nnodes);
+    if (b->npts != s->m)
+      throw_error(SG_DOMAIN_ERROR, "ShapeMismatch: target field has %lld points, weights cover %lld",
+                  (long long)b->npts, (long long)s->m);
+    if (a->levels != b->levels) throw_error(SG_DOMAIN_ERROR, "ShapeMismatch: level counts differ");
+    SG_REQUIRE(a->itemsize == 8 && b->itemsize == 8, "apply_remap on device needs real64 fields");
+    SG_REQUIRE(a->device == s->device && b->device == s->device, "fields and stencil live on different devices");
+    if (p.levels < 0) p.levels = a->levels;
+    SG_REQUIRE(a->levels == p.levels, "all field pairs of one call must have equal levels");
+  }
+  return p;
+}
+
+ApplyArgs make_args(const Stencil* s, const FieldPairs& p, int f0, int64_t t0, int64_t t1) {
+  ApplyArgs a{};
+  a.idx = s->idx.as<int4>();
+  a.w = s->w.as<double4>();
+  a.t0 = t0;
+  a.t1 = t1;
+  a.levels = p.levels;
+  a.nfields = std::min<int>(kMaxFields, (int)p.src.size() - f0);
+  for (int f = 0; f < a.nfields; ++f) {
+    a.src[f] = p.src[f0 + f]->buf.as<double>();
+    a.dst[f] = p.dst[f0 + f]->buf.as<double>();
+    a.src_pitch[f] = p.src[f0 + f]->pitch;
+    a.dst_pitch[f] = p.dst[f0 + f]->pitch;
+  }
+  return a;
+}
+
+// ---- host pipeline plan (per stencil, built on first use) -----------------------------------
+struct HostPlan {
+  int nchunks = 0;
+  std::vector<int64_t> t_end;                                  // chunk c: targets [t_end[c-1], t_end[c])
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> runs;  // chunk c: referenced source rows
+  int64_t rows_copied = 0;
+  cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_cmp;
+};
+
+std::mutex g_plan_mu;
+
+HostPlan* host_plan(Stencil* s, int nchunks) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  auto* hp = static_cast<HostPlan*>(s->host_plan);
+  if (hp && hp->nchunks == nchunks) return hp;
+  s->destroy_host_plan();
+  auto owned = std::make_unique<HostPlan>();
+  hp = owned.get();
+  hp->nchunks = nchunks;
+  const int64_t m = s->m, n = s->source_nnodes;
+  std::vector<int4> idx((size_t)m);
+  if (m) SG_CUDA(cudaMemcpy(idx.data(), s->idx.ptr, (size_t)m * sizeof(int4), cudaMemcpyDeviceToHost));
+  std::vector<unsigned char> mark((size_t)n, 0);
+  std::vector<int64_t> pmax((size_t)m);
+  int64_t run_max = -1;
+  for (int64_t t = 0; t < m; ++t) {
+    const int4 id = idx[t];
+    mark[id.x] = mark[id.y] = mark[id.z] = 1;
+    run_max = std::max<int64_t>(run_max, std::max(id.x, std::max(id.y, id.z)));
+    pmax[t] = run_max;  // monotone: targets [0, t] need source rows <= pmax[t]
+  }
+  int64_t tprev = 0, rprev = 0;
+  hp->t_end.resize(nchunks);
+  hp->runs.resize(nchunks);
+  for (int c = 0; c < nchunks; ++c) {
+    const int64_t rb = (c + 1 == nchunks) ? n : n * (c + 1) / nchunks;  // source rows [rprev, rb)
+    int64_t te = (c + 1 == nchunks) ? m : (int64_t)(std::lower_bound(pmax.begin(), pmax.end(), rb) - pmax.begin());
+    te = std::max(te, tprev);
+    hp->t_end[c] = te;
+    // referenced runs of [rprev, rb); unreferenced gaps shorter than 64 rows are copied through
+    int64_t i = rprev;
+    while (i < rb) {
+      while (i < rb && !mark[i]) ++i;
+      if (i >= rb) break;
+      int64_t j = i;
+      for (;;) {
+        while (j < rb && mark[j]) ++j;
+        int64_t g = j;
+        while (g < rb && !mark[g] && g - j < 64) ++g;
+        if (g < rb && mark[g]) j = g;  // short gap: merge
+        else break;
+      }
+      hp->runs[c].emplace_back(i, j);
+      hp->rows_copied += j - i;
+      i = j;
+    }
+    tprev = te;
+    rprev = rb;
+  }
+  SG_CUDA(cudaStreamCreateWithFlags(&hp->s_in, cudaStreamNonBlocking));
+  SG_CUDA(cudaStreamCreateWithFlags(&hp->s_cmp, cudaStreamNonBlocking));
+  SG_CUDA(cudaStreamCreateWithFlags(&hp->s_out, cudaStreamNonBlocking));
+  hp->ev_in.resize(nchunks);
+  hp->ev_cmp.resize(nchunks);
+  for (int c = 0; c < nchunks; ++c) {
+    SG_CUDA(cudaEventCreateWithFlags(&hp->ev_in[c], cudaEventDisableTiming));
+    SG_CUDA(cudaEventCreateWithFlags(&hp->ev_cmp[c], cudaEventDisableTiming));
+  }
+  s->host_plan = owned.release();
+  return hp;
+}
 
 }  // namespace
+
+void Stencil::destroy_host_plan() {
+  auto* hp = static_cast<HostPlan*>(host_plan);
+  if (!hp) return;
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != device) cudaSetDevice(device);
+  for (auto e : hp->ev_in) cudaEventDestroy(e);
+  for (auto e : hp->ev_cmp) cudaEventDestroy(e);
+  if (hp->s_in) cudaStreamDestroy(hp->s_in);
+  if (hp->s_cmp) cudaStreamDestroy(hp->s_cmp);
+  if (hp->s_out) cudaStreamDestroy(hp->s_out);
+  if (cur != device && cur >= 0) cudaSetDevice(cur);
+  delete hp;
+  host_plan = nullptr;
+}
 
 void stencil_finalize(Stencil* s, const int32_t* d_idx3, const double* d_w3, cudaStream_t st) {
   s->idx.alloc(s->device, (size_t)std::max<int64_t>(s->m, 1) * sizeof(int4));
   s->w.alloc(s->device, (size_t)std::max<int64_t>(s->m, 1) * sizeof(double4));
   if (s->m > 0) {
-    pack_stencil<<<(unsigned)((s->m + 255) / 256), 256, 0, st>>>(d_idx3, d_w3, s->m,
-                                                                 s->idx.as<int4>(), s->w.as<double4>());
+    pack_stencil<<<(unsigned)((s->m + 255) / 256), 256, 0, st>>>(d_idx3, d_w3, s->m, s->idx.as<int4>(),
+                                                                 s->w.as<double4>());
     SG_CUDA_LAUNCH();
   }
   DevBuf mark, cnt;
@@ -296,11 +518,9 @@ void stencil_finalize(Stencil* s, const int32_t* d_idx3, const double* d_w3, cud
   SG_CUDA(cudaMemsetAsync(mark.ptr, 0, mark.bytes, st));
   SG_CUDA(cudaMemsetAsync(cnt.ptr, 0, cnt.bytes, st));
   if (s->m > 0) {
-    mark_sources<<<(unsigned)((s->m + 255) / 256), 256, 0, st>>>(s->idx.as<int4>(), s->m,
-                                                                 mark.as<unsigned char>());
+    mark_sources<<<(unsigned)((s->m + 255) / 256), 256, 0, st>>>(s->idx.as<int4>(), s->m, mark.as<unsigned char>());
     SG_CUDA_LAUNCH();
-    count_marks<<<1024, 256, 0, st>>>(mark.as<unsigned char>(), s->source_nnodes,
-                                      cnt.as<unsigned long long>());
+    count_marks<<<1024, 256, 0, st>>>(mark.as<unsigned char>(), s->source_nnodes, cnt.as<unsigned long long>());
     SG_CUDA_LAUNCH();
   }
   unsigned long long u = 0;
@@ -355,86 +575,69 @@ int32_t sg_stencil_info(uint64_t stencil, int64_t* out_m, int64_t* out_source_nn
   SG_API_END
 }
 
-int32_t sg_remap_apply(uint64_t stencil, const uint64_t* src_fields, const uint64_t* dst_fields,
-                       int32_t nfields, int32_t variant, uint64_t stream) {
+int32_t sg_remap_apply(uint64_t stencil, const uint64_t* src_fields, const uint64_t* dst_fields, int32_t nfields,
+                       int32_t variant, uint64_t stream) {
   SG_API_BEGIN
   Stencil* s = get<Stencil>(stencil, ObjKind::Stencil);
-  SG_REQUIRE(nfields >= 1, "nfields must be >= 1");
-  SG_REQUIRE(src_fields && dst_fields, "null field arrays");
+  FieldPairs p = check_pairs(s, src_fields, dst_fields, nfields);
   DeviceScope ds(s->device);
-  cudaStream_t st = as_stream(stream);
-  int32_t levels = -1;
-  std::vector<Field*> src(nfields), dst(nfields);
-  bool even_pitch = true;
+  for (int f0 = 0; f0 < nfields; f0 += kMaxFields) launch_apply(make_args(s, p, f0, 0, s->m), variant, as_stream(stream));
+  SG_API_END
+}
+
+int32_t sg_remap_apply_range(uint64_t stencil, const uint64_t* src_fields, const uint64_t* dst_fields,
+                             int32_t nfields, int64_t t0, int64_t t1, int32_t variant, uint64_t stream) {
+  SG_API_BEGIN
+  Stencil* s = get<Stencil>(stencil, ObjKind::Stencil);
+  FieldPairs p = check_pairs(s, src_fields, dst_fields, nfields);
+  SG_REQUIRE(0 <= t0 && t0 <= t1 && t1 <= s->m, "target range [%lld, %lld) outside [0, %lld)", (long long)t0,
+             (long long)t1, (long long)s->m);
+  DeviceScope ds(s->device);
+  for (int f0 = 0; f0 < nfields; f0 += kMaxFields) launch_apply(make_args(s, p, f0, t0, t1), variant, as_stream(stream));
+  SG_API_END
+}
+
+int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, const uint64_t* dst_fields,
+                              int32_t nfields, const uint64_t* host_src, const uint64_t* host_dst, int32_t nchunks,
+                              int32_t variant, int64_t* out_rows_copied) {
+  SG_API_BEGIN
+  Stencil* s = get<Stencil>(stencil, ObjKind::Stencil);
+  FieldPairs p = check_pairs(s, src_fields, dst_fields, nfields);
+  SG_REQUIRE(host_src && host_dst, "null host arrays");
   for (int f = 0; f < nfields; ++f) {
-    src[f] = get<Field>(src_fields[f], ObjKind::Field);
-    dst[f] = get<Field>(dst_fields[f], ObjKind::Field);
-    // exact reference messages, interp.py:208-217
-    if (src[f]->npts != s->source_nnodes)
-      throw_error(SG_DOMAIN_ERROR, "ShapeMismatch: source field has %lld points, weights expect %lld",
-                  (long long)src[f]->npts, (long long)s->source_nnodes);
-    if (dst[f]->npts != s->m)
-      throw_error(SG_DOMAIN_ERROR, "ShapeMismatch: target field has %lld points, weights cover %lld",
-                  (long long)dst[f]->npts, (long long)s->m);
-    if (src[f]->levels != dst[f]->levels) throw_error(SG_DOMAIN_ERROR, "ShapeMismatch: level counts differ");
-    SG_REQUIRE(src[f]->itemsize == 8 && dst[f]->itemsize == 8, "apply_remap on device needs real64 fields");
-    SG_REQUIRE(src[f]->device == s->device && dst[f]->device == s->device,
-               "fields and stencil live on different devices");
-    if (levels < 0) levels = src[f]->levels;
-    SG_REQUIRE(src[f]->levels == levels, "all field pairs of one call must have equal levels");
-    even_pitch = even_pitch && (src[f]->pitch % 2 == 0) && (dst[f]->pitch % 2 == 0);
+    SG_REQUIRE(host_src[f] && host_dst[f], "null host array for field %d", f);
+    SG_REQUIRE(p.src[f]->pitch == p.levels && p.dst[f]->pitch == p.levels, "execute_host needs dense fields");
   }
-  if (s->m == 0) return SG_OK;
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  for (int f0 = 0; f0 < nfields; f0 += kMaxFields) {
-    ApplyArgs a{};
-    a.idx = s->idx.as<int4>();
-    a.w = s->w.as<double4>();
-    a.m = s->m;
-    a.levels = levels;
-    a.nfields = std::min(kMaxFields, nfields - f0);
-    for (int f = 0; f < a.nfields; ++f) {
-      a.src[f] = src[f0 + f]->buf.as<double>();
-      a.dst[f] = dst[f0 + f]->buf.as<double>();
-      a.src_pitch[f] = src[f0 + f]->pitch;
-      a.dst_pitch[f] = dst[f0 + f]->pitch;
+  SG_REQUIRE(nchunks >= 1 && nchunks <= 1024, "nchunks must be in [1, 1024]");
+  DeviceScope ds(s->device);
+  HostPlan* hp = host_plan(s, nchunks);
+  const size_t row = (size_t)p.levels * 8;
+  int64_t tprev = 0;
+  for (int c = 0; c < nchunks; ++c) {
+    for (int f = 0; f < nfields; ++f) {
+      char* dev = p.src[f]->buf.as<char>();
+      const char* host = reinterpret_cast<const char*>(host_src[f]);
+      for (auto& r : hp->runs[c])
+        SG_CUDA(cudaMemcpyAsync(dev + r.first * row, host + r.first * row, (size_t)(r.second - r.first) * row,
+                                cudaMemcpyHostToDevice, hp->s_in));
     }
-    const int nvec = (levels + 1) / 2;
-    const uint32_t row_bytes = (uint32_t)(((int64_t)levels * 8 + 15) / 16 * 16);
-    bool bulk_ok = even_pitch && levels >= 2 && variant == 2;
-    for (int f = 0; f < a.nfields && bulk_ok; ++f) bulk_ok = a.src_pitch[f] * 8 >= (int64_t)row_bytes;
-    if (bulk_ok) {
-      const int row_elems = (int)(row_bytes / 8);
-      const size_t smem = (size_t)kStages * 3 * kTile * row_elems * sizeof(double);
-      SG_REQUIRE(smem <= 200 * 1024, "levels too large for the bulk-copy variant");
-      SG_CUDA(cudaFuncSetAttribute(apply_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      int per_sm = 0;
-      SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_bulk, kV2Threads, smem));
-      per_sm = std::max(per_sm, 1);
-      const int64_t nwork = (s->m + kTile - 1) / kTile * a.nfields;
-      const int64_t grid = std::min<int64_t>((int64_t)g_num_sms * per_sm, nwork);
-      apply_bulk<<<(unsigned)grid, kV2Threads, smem, st>>>(a, row_elems, row_bytes);
-    } else if (levels <= 8) {
-      apply_thread_short<<<(unsigned)((s->m + 255) / 256), 256, 0, st>>>(a);
-    } else if (!even_pitch) {
-      apply_warp_scalar<<<(unsigned)((s->m + 7) / 8), 256, 0, st>>>(a);
-    } else {
-      const unsigned grid = (unsigned)((s->m + 7) / 8);  // 8 warps per block
-      const int iters = (nvec + 31) / 32;
-      switch (iters) {
-        case 1: apply_warp_v2<1><<<grid, 256, 0, st>>>(a); break;
-        case 2: apply_warp_v2<2><<<grid, 256, 0, st>>>(a); break;
-        case 3: apply_warp_v2<3><<<grid, 256, 0, st>>>(a); break;
-        case 4: apply_warp_v2<4><<<grid, 256, 0, st>>>(a); break;
-        default: apply_warp_scalar<<<grid, 256, 0, st>>>(a); break;
-      }
-    }
-    SG_CUDA_LAUNCH();
+    SG_CUDA(cudaEventRecord(hp->ev_in[c], hp->s_in));
+    SG_CUDA(cudaStreamWaitEvent(hp->s_cmp, hp->ev_in[c], 0));
+    const int64_t te = hp->t_end[c];
+    for (int f0 = 0; f0 < nfields; f0 += kMaxFields) launch_apply(make_args(s, p, f0, tprev, te), variant, hp->s_cmp);
+    SG_CUDA(cudaEventRecord(hp->ev_cmp[c], hp->s_cmp));
+    SG_CUDA(cudaStreamWaitEvent(hp->s_out, hp->ev_cmp[c], 0));
+    if (te > tprev)
+      for (int f = 0; f < nfields; ++f)
+        SG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(host_dst[f]) + tprev * row,
+                                p.dst[f]->buf.as<char>() + tprev * row, (size_t)(te - tprev) * row,
+                                cudaMemcpyDeviceToHost, hp->s_out));
+    tprev = te;
   }
+  SG_CUDA(cudaStreamSynchronize(hp->s_out));
+  SG_CUDA(cudaStreamSynchronize(hp->s_cmp));
+  SG_CUDA(cudaStreamSynchronize(hp->s_in));
+  if (out_rows_copied) *out_rows_copied = hp->rows_copied;
   SG_API_END
 }
 

@@ -72,18 +72,11 @@ struct Field : Object {
   DevBuf buf;
 };
 
-// Row pitch policy: rows >= 128 B are padded to a multiple of 128 B (one cache line, a
-// multiple of the 16-B vector / bulk-copy granule); shorter rows to the next power of two.
-inline int64_t field_pitch_elems(int32_t levels, int32_t itemsize) {
-  int64_t row = (int64_t)levels * itemsize;
-  int64_t padded;
-  if (row >= 128) {
-    padded = (row + 127) / 128 * 128;
-  } else {
-    padded = itemsize;
-    while (padded < row) padded *= 2;
-  }
-  return padded / itemsize;
-}
+// Row pitch policy: dense rows (pitch == levels), exactly the reference host layout.
+// Measured (profiles/, round 1): with 128-B padded rows every gathered 1096-B row cost 1152 B
+// of DRAM reads (HBM fetches 64-B granules), 5% over the algorithmic bytes; dense rows let
+// the boundary granule of two neighbouring source points — which neighbouring targets read
+// together — be fetched once, and make h2d/d2h plain contiguous copies at full PCIe rate.
+inline int64_t field_pitch_elems(int32_t levels, int32_t /*itemsize*/) { return levels; }
 
 }  // namespace sg

@@ -1,6 +1,7 @@
-// Device mirror of a reference Field (field.py:77-162): pitched, level-contiguous rows.
-// h2d/d2h move the unpadded host (npts, levels) C-order array (field.py:161) with one
-// cudaMemcpy2DAsync each, so the host layout the reference exposes is unchanged.
+// Device mirror of a reference Field (field.py:77-162): level-contiguous rows with the
+// pitch chosen by field_pitch_elems (dense today).  h2d/d2h move the unpadded host
+// (npts, levels) C-order array (field.py:161): one contiguous copy for dense rows, a
+// cudaMemcpy2DAsync otherwise.
 #include <algorithm>
 
 #include "cuda_util.cuh"
@@ -72,7 +73,13 @@ static void copy_rows(Field* f, int64_t row0, int64_t nrows, const void* src_hos
   size_t row_bytes = (size_t)f->levels * f->itemsize;
   size_t pitch_bytes = (size_t)f->pitch * f->itemsize;
   char* dev = f->buf.as<char>() + (size_t)row0 * pitch_bytes;
-  if (src_host) {
+  if (pitch_bytes == row_bytes) {  // dense rows: one contiguous copy
+    const size_t n = row_bytes * (size_t)nrows;
+    if (src_host)
+      SG_CUDA(cudaMemcpyAsync(dev, src_host, n, cudaMemcpyHostToDevice, as_stream(stream)));
+    else
+      SG_CUDA(cudaMemcpyAsync(dst_host, dev, n, cudaMemcpyDeviceToHost, as_stream(stream)));
+  } else if (src_host) {
     SG_CUDA(cudaMemcpy2DAsync(dev, pitch_bytes, src_host, row_bytes, row_bytes, (size_t)nrows,
                               cudaMemcpyHostToDevice, as_stream(stream)));
   } else {

@@ -5,7 +5,7 @@
 // (halo, gidx) order (functionspace.py:66-72), and each ghost's row on its owner
 // (mesh.py:303-308, node_remote == the owner's send entry for it).
 //
-// Kernels (one warp per row, lanes over the row's 32-bit words; every field kind shares them):
+// Kernels (one warp per row, lanes over the row's items):
 //   pack   — every peer's payload into one device buffer, peers ascending, (n, L) C-order:
 //            byte-equal to f.host[send[peer]].tobytes() (functionspace.py:113-114)
 //   unpack — receive buffer into the ghost rows (functionspace.py:115-117)
@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <mutex>
 #include <numeric>
+#include <type_traits>
 #include <vector>
 
 #include "cuda_util.cuh"
@@ -39,53 +40,48 @@ struct Plan : Object {
   DevBuf sendbuf, recvbuf;                   // NCCL staging (lazily sized)
 };
 
-// Rows are moved as 32-bit words so every field kind (4- or 8-byte) shares the kernels:
-// W words per row, pitches in words.
-__global__ void pack_rows(const uint32_t* __restrict__ f, int64_t pitch_w, int W,
-                          const int32_t* __restrict__ rows, int64_t n, uint32_t* __restrict__ out) {
+// Rows are moved as words of the field's item size (8 B for real64/int64, 4 B otherwise):
+// W words per row, pitches in words.  Dense rows are item-aligned only, so no wider moves.
+template <typename Wd>
+__global__ void pack_rows(const Wd* __restrict__ f, int64_t pitch_w, int W, const int32_t* __restrict__ rows,
+                          int64_t n, Wd* __restrict__ out) {
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= n) return;
-  const uint32_t* src = f + (int64_t)rows[r] * pitch_w;
-  uint32_t* dst = out + r * W;
+  const Wd* src = f + (int64_t)rows[r] * pitch_w;
+  Wd* dst = out + r * W;
   for (int l = lane; l < W; l += 32) dst[l] = src[l];
 }
 
-__global__ void unpack_rows(uint32_t* __restrict__ f, int64_t pitch_w, int W,
-                            const int32_t* __restrict__ rows, int64_t n, const uint32_t* __restrict__ in) {
+template <typename Wd>
+__global__ void unpack_rows(Wd* __restrict__ f, int64_t pitch_w, int W, const int32_t* __restrict__ rows, int64_t n,
+                            const Wd* __restrict__ in) {
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= n) return;
-  uint32_t* dst = f + (int64_t)rows[r] * pitch_w;
-  const uint32_t* src = in + r * W;
+  Wd* dst = f + (int64_t)rows[r] * pitch_w;
+  const Wd* src = in + r * W;
   for (int l = lane; l < W; l += 32) dst[l] = src[l];
 }
 
 struct PeerPtrs {
-  const uint32_t* base[kMaxPeers];
+  const void* base[kMaxPeers];
   int64_t pitch_w[kMaxPeers];
 };
 
 // Fused exchange: ghost row k (peer slot s) <- the owner's row recv_remote[k], read through a
-// peer pointer.  VEC: 16-B moves (rows padded to 16 B on both sides).
-template <bool VEC>
-__global__ void pull_rows(uint32_t* __restrict__ f, int64_t pitch_w, int W,
-                          const int32_t* __restrict__ rows, const int32_t* __restrict__ remote,
-                          const int32_t* __restrict__ slot, int64_t n, PeerPtrs peers) {
+// peer pointer (same device, NVLink P2P or CUDA IPC): pack, transfer and unpack in one pass.
+template <typename Wd>
+__global__ void pull_rows(Wd* __restrict__ f, int64_t pitch_w, int W, const int32_t* __restrict__ rows,
+                          const int32_t* __restrict__ remote, const int32_t* __restrict__ slot, int64_t n,
+                          PeerPtrs peers) {
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= n) return;
   const int s = slot[r];
-  const uint32_t* src = peers.base[s] + (int64_t)remote[r] * peers.pitch_w[s];
-  uint32_t* dst = f + (int64_t)rows[r] * pitch_w;
-  if (VEC) {
-    const int nv = (W + 3) >> 2;
-    const uint4* s4 = reinterpret_cast<const uint4*>(src);
-    uint4* d4 = reinterpret_cast<uint4*>(dst);
-    for (int k = lane; k < nv; k += 32) d4[k] = s4[k];
-  } else {
-    for (int l = lane; l < W; l += 32) dst[l] = src[l];
-  }
+  const Wd* src = static_cast<const Wd*>(peers.base[s]) + (int64_t)remote[r] * peers.pitch_w[s];
+  Wd* dst = f + (int64_t)rows[r] * pitch_w;
+  for (int l = lane; l < W; l += 32) dst[l] = src[l];
 }
 
 inline unsigned warps_grid(int64_t n) { return (unsigned)((n + 7) / 8); }
@@ -96,7 +92,7 @@ typedef struct ncclComm* ncclComm_t;
 struct ncclUniqueId {
   char internal[128];
 };
-enum { ncclUint32 = 3 };
+enum { ncclUint8 = 1 };
 struct Nccl {
   void* lib = nullptr;
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
@@ -150,8 +146,12 @@ struct Comm : Object {
   }
 };
 
-inline int64_t pitch_words(const Field* f) { return f->pitch * f->itemsize / 4; }
-inline int row_words(const Field* f) { return (int)((int64_t)f->levels * f->itemsize / 4); }
+// Dispatch on the field's item size: 8-byte kinds move as uint64, 4-byte kinds as uint32.
+template <class F>
+void by_word(const Field* f, F&& fn) {
+  if (f->itemsize == 8) fn((uint64_t*)nullptr);
+  else fn((uint32_t*)nullptr);
+}
 
 void check_field(const Plan* p, const Field* f) {
   if (f->npts != p->nnodes)
@@ -229,9 +229,12 @@ int32_t sg_halo_pack(uint64_t plan, uint64_t field, void* dev_sendbuf, uint64_t 
   if (n == 0) return SG_OK;
   SG_REQUIRE(dev_sendbuf, "null send buffer");
   DeviceScope ds(p->device);
-  pack_rows<<<warps_grid(n), 256, 0, as_stream(stream)>>>(f->buf.as<uint32_t>(), pitch_words(f), row_words(f),
-                                                          p->send_rows.as<int32_t>(), n,
-                                                          static_cast<uint32_t*>(dev_sendbuf));
+  by_word(f, [&](auto* tag) {
+    using Wd = std::remove_pointer_t<decltype(tag)>;
+    pack_rows<Wd><<<warps_grid(n), 256, 0, as_stream(stream)>>>(f->buf.as<Wd>(), f->pitch, f->levels,
+                                                                p->send_rows.as<int32_t>(), n,
+                                                                static_cast<Wd*>(dev_sendbuf));
+  });
   SG_CUDA_LAUNCH();
   SG_API_END
 }
@@ -245,9 +248,12 @@ int32_t sg_halo_unpack(uint64_t plan, uint64_t field, const void* dev_recvbuf, u
   if (n == 0) return SG_OK;
   SG_REQUIRE(dev_recvbuf, "null receive buffer");
   DeviceScope ds(p->device);
-  unpack_rows<<<warps_grid(n), 256, 0, as_stream(stream)>>>(f->buf.as<uint32_t>(), pitch_words(f), row_words(f),
-                                                            p->recv_rows.as<int32_t>(), n,
-                                                            static_cast<const uint32_t*>(dev_recvbuf));
+  by_word(f, [&](auto* tag) {
+    using Wd = std::remove_pointer_t<decltype(tag)>;
+    unpack_rows<Wd><<<warps_grid(n), 256, 0, as_stream(stream)>>>(f->buf.as<Wd>(), f->pitch, f->levels,
+                                                                  p->recv_rows.as<int32_t>(), n,
+                                                                  static_cast<const Wd*>(dev_recvbuf));
+  });
   SG_CUDA_LAUNCH();
   SG_API_END
 }
@@ -262,24 +268,19 @@ int32_t sg_halo_pull(uint64_t plan, uint64_t field, const uint64_t* peer_ptrs, c
   if (n == 0) return SG_OK;
   SG_REQUIRE(peer_ptrs && peer_pitch_elems, "null peer arrays");
   PeerPtrs pp{};
-  const int64_t wpi = f->itemsize / 4;
-  bool vec = (pitch_words(f) % 4 == 0);
   for (size_t i = 0; i < p->peers.size(); ++i) {
-    pp.base[i] = reinterpret_cast<const uint32_t*>(peer_ptrs[i]);
-    pp.pitch_w[i] = peer_pitch_elems[i] * wpi;
+    pp.base[i] = reinterpret_cast<const void*>(peer_ptrs[i]);
+    pp.pitch_w[i] = peer_pitch_elems[i];
     if (p->recv_off[i + 1] > p->recv_off[i]) SG_REQUIRE(pp.base[i], "null peer pointer for peer %d", p->peers[i]);
-    vec = vec && (pp.pitch_w[i] % 4 == 0) && (peer_ptrs[i] % 16 == 0) && pp.pitch_w[i] >= (row_words(f) + 3) / 4 * 4;
   }
-  vec = vec && pitch_words(f) >= (row_words(f) + 3) / 4 * 4;
   DeviceScope ds(p->device);
-  if (vec)
-    pull_rows<true><<<warps_grid(n), 256, 0, as_stream(stream)>>>(
-        f->buf.as<uint32_t>(), pitch_words(f), row_words(f), p->recv_rows.as<int32_t>(), p->recv_remote.as<int32_t>(),
-        p->recv_peer.as<int32_t>(), n, pp);
-  else
-    pull_rows<false><<<warps_grid(n), 256, 0, as_stream(stream)>>>(
-        f->buf.as<uint32_t>(), pitch_words(f), row_words(f), p->recv_rows.as<int32_t>(), p->recv_remote.as<int32_t>(),
-        p->recv_peer.as<int32_t>(), n, pp);
+  by_word(f, [&](auto* tag) {
+    using Wd = std::remove_pointer_t<decltype(tag)>;
+    pull_rows<Wd><<<warps_grid(n), 256, 0, as_stream(stream)>>>(f->buf.as<Wd>(), f->pitch, f->levels,
+                                                                p->recv_rows.as<int32_t>(),
+                                                                p->recv_remote.as<int32_t>(),
+                                                                p->recv_peer.as<int32_t>(), n, pp);
+  });
   SG_CUDA_LAUNCH();
   SG_API_END
 }
@@ -319,12 +320,15 @@ int32_t sg_halo_exchange_nccl(uint64_t plan, uint64_t field, uint64_t comm, uint
   DeviceScope ds(p->device);
   cudaStream_t st = as_stream(stream);
   const int64_t ns = p->send_off.back(), nr = p->recv_off.back();
-  const size_t W = (size_t)row_words(f);  // payload words per row
-  if ((size_t)ns * W * 4 > p->sendbuf.bytes) p->sendbuf.alloc(p->device, (size_t)ns * W * 4);
-  if ((size_t)nr * W * 4 > p->recvbuf.bytes) p->recvbuf.alloc(p->device, (size_t)nr * W * 4);
+  const size_t row = (size_t)f->levels * f->itemsize;  // payload bytes per row
+  if ((size_t)ns * row > p->sendbuf.bytes) p->sendbuf.alloc(p->device, (size_t)ns * row);
+  if ((size_t)nr * row > p->recvbuf.bytes) p->recvbuf.alloc(p->device, (size_t)nr * row);
   if (ns) {
-    pack_rows<<<warps_grid(ns), 256, 0, st>>>(f->buf.as<uint32_t>(), pitch_words(f), (int)W, p->send_rows.as<int32_t>(),
-                                              ns, p->sendbuf.as<uint32_t>());
+    by_word(f, [&](auto* tag) {
+      using Wd = std::remove_pointer_t<decltype(tag)>;
+      pack_rows<Wd><<<warps_grid(ns), 256, 0, st>>>(f->buf.as<Wd>(), f->pitch, f->levels, p->send_rows.as<int32_t>(),
+                                                    ns, p->sendbuf.as<Wd>());
+    });
     SG_CUDA_LAUNCH();
   }
   Nccl& N = nccl();
@@ -332,13 +336,16 @@ int32_t sg_halo_exchange_nccl(uint64_t plan, uint64_t field, uint64_t comm, uint
   for (size_t i = 0; i < p->peers.size(); ++i) {
     const int64_t s0 = p->send_off[i], s1 = p->send_off[i + 1];
     const int64_t r0 = p->recv_off[i], r1 = p->recv_off[i + 1];
-    if (s1 > s0) SG_NCCL(N.Send(p->sendbuf.as<uint32_t>() + s0 * W, (size_t)(s1 - s0) * W, ncclUint32, p->peers[i], c->comm, st));
-    if (r1 > r0) SG_NCCL(N.Recv(p->recvbuf.as<uint32_t>() + r0 * W, (size_t)(r1 - r0) * W, ncclUint32, p->peers[i], c->comm, st));
+    if (s1 > s0) SG_NCCL(N.Send(p->sendbuf.as<char>() + s0 * row, (size_t)(s1 - s0) * row, ncclUint8, p->peers[i], c->comm, st));
+    if (r1 > r0) SG_NCCL(N.Recv(p->recvbuf.as<char>() + r0 * row, (size_t)(r1 - r0) * row, ncclUint8, p->peers[i], c->comm, st));
   }
   SG_NCCL(N.GroupEnd());
   if (nr) {
-    unpack_rows<<<warps_grid(nr), 256, 0, st>>>(f->buf.as<uint32_t>(), pitch_words(f), (int)W, p->recv_rows.as<int32_t>(),
-                                                nr, p->recvbuf.as<uint32_t>());
+    by_word(f, [&](auto* tag) {
+      using Wd = std::remove_pointer_t<decltype(tag)>;
+      unpack_rows<Wd><<<warps_grid(nr), 256, 0, st>>>(f->buf.as<Wd>(), f->pitch, f->levels, p->recv_rows.as<int32_t>(),
+                                                      nr, p->recvbuf.as<Wd>());
+    });
     SG_CUDA_LAUNCH();
   }
   SG_API_END

@@ -15,6 +15,9 @@ struct Stencil : Object {
   int64_t distinct_sources = 0;  // U: distinct source rows referenced
   DevBuf idx;                    // int4[m]
   DevBuf w;                      // double4[m]
+  void* host_plan = nullptr;     // pipelined host-buffer execute plan (apply.cu)
+  void destroy_host_plan();
+  ~Stencil() override { destroy_host_plan(); }
 };
 
 // Builds the device arrays from device-resident int32 index / fp64 weight triples and

@@ -160,6 +160,15 @@ class InterpolationWeights:
             self.stencil, self.stencil_device = N.Handle(h.value), device
         return self.stencil.handle
 
+    def _staging(self, device: int, src_shape, dst_shape):
+        key = (device, tuple(src_shape), tuple(dst_shape))
+        cache = self.__dict__.setdefault("_staging_cache", {})
+        if key not in cache:
+            cache.clear()
+            cache[key] = (DeviceArray(src_shape[0], src_shape[1], np.float64, device),
+                          DeviceArray(dst_shape[0], dst_shape[1], np.float64, device))
+        return cache[key]
+
     def distinct_sources(self) -> int:
         u = C.c_int64()
         N.call("sg_stencil_info", self.device_stencil(self.stencil_device), None, None, N.ref(u))
@@ -227,6 +236,30 @@ def apply_remap_device(weights: InterpolationWeights, sources: Sequence[DeviceAr
     N.call("sg_remap_apply", sh, N.ptr(s), N.ptr(t), len(s), variant, stream)
 
 
+def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], host_dst: Sequence[np.ndarray],
+                 dev_src: Sequence[DeviceArray], dev_dst: Sequence[DeviceArray], nchunks: int = 0,
+                 variant: int = APPLY_DEFAULT) -> int:
+    """Host buffers in, host buffers out (sg_remap_execute_host): chunked h2d of the referenced
+    source rows, apply, d2h of the target rows, overlapped on three streams.  Host arrays
+    should be pinned (``device.PinnedArray``) for full PCIe rate.  Returns source rows copied."""
+    dev = dev_src[0].device
+    sh = weights.device_stencil(dev)
+    m = len(weights)
+    if nchunks <= 0:
+        nchunks = int(max(1, min(32, m // 32768)))
+    for a, d in zip(list(host_src) + list(host_dst), list(dev_src) + list(dev_dst)):
+        if a.shape != d.shape or a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("host arrays must be C-contiguous float64 of the device arrays' shape")
+    hs = np.array([a.ctypes.data for a in host_src], np.uint64)
+    hd = np.array([a.ctypes.data for a in host_dst], np.uint64)
+    s = np.array([a.handle for a in dev_src], np.uint64)
+    t = np.array([a.handle for a in dev_dst], np.uint64)
+    rows = C.c_int64(0)
+    N.call("sg_remap_execute_host", sh, N.ptr(s), N.ptr(t), len(s), N.ptr(hs), N.ptr(hd), nchunks, variant,
+           N.ref(rows))
+    return rows.value
+
+
 def apply_remap(weights: InterpolationWeights, source_field: Field, target_field: Field) -> None:
     """target[t] = sum_i w_i * source[node_i], every level (interp.py:206-228)."""
     _check_shapes(weights, source_field, target_field)
@@ -240,16 +273,18 @@ def apply_remap(weights: InterpolationWeights, source_field: Field, target_field
         N.call("sg_stream_synchronize", source_field.device.device, 0)
         target_field.mark_device_written()
         return
-    # host-resident fields: reference semantics (reads source.host, writes target.host)
-    src = DeviceArray(source_field.npts, source_field.levels, np.float64, dev)
-    dst = DeviceArray(target_field.npts, target_field.levels, np.float64, dev)
-    src.upload(np.ascontiguousarray(source_field.host, dtype=np.float64))
-    apply_remap_device(weights, [src], [dst])
-    out = np.empty(target_field.shape, np.float64)
-    dst.download(out)
-    target_field.host[:] = out
-    src.close()
-    dst.close()
+    # host-resident fields: reference semantics (reads source.host, writes target.host);
+    # the arithmetic runs on the device through staging buffers cached on the weights
+    src, dst = weights._staging(dev, source_field.shape, target_field.shape)
+    host_src = source_field.host
+    if host_src.dtype != np.float64 or not host_src.flags["C_CONTIGUOUS"]:
+        host_src = np.ascontiguousarray(host_src, dtype=np.float64)
+    th = target_field.host
+    direct = th.dtype == np.float64 and th.flags["C_CONTIGUOUS"] and th.flags["WRITEABLE"]
+    out = th if direct else np.empty(target_field.shape, np.float64)
+    execute_host(weights, [host_src], [out], [src], [dst])
+    if not direct:
+        th[:] = out
     if target_field.state is MemoryState.SYNCED:
         target_field.state = MemoryState.HOST_DIRTY
 

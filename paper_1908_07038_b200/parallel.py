@@ -51,6 +51,8 @@ class _World:
 
     def _stuck(self) -> bool:
         # every unfinished rank waits and nobody's wake-up condition holds (parallel.py:49-64)
+        if self.aborted:
+            return False
         live = self.nranks - len(self.done)
         return live > 0 and len(self.waiting) == live and not any(p() for p in self.waiting.values())
 
@@ -61,10 +63,10 @@ class _World:
                 self.deadlocked = True
                 self.cv.notify_all()
             while not ready():
-                if self.deadlocked:
-                    raise DeadlockDetected(f"rank {rank} blocked with no possible sender")
                 if self.aborted:
                     raise _Abort()
+                if self.deadlocked:
+                    raise DeadlockDetected(f"rank {rank} blocked with no possible sender")
                 self.cv.wait()
         finally:
             self.waiting.pop(rank, None)
@@ -243,6 +245,7 @@ class DistContext:
         self.messages_received = 0
         self._comm = None
         self._pending: Dict[tuple, deque] = {}
+        self._inflight: list = []
 
     def _peer(self, peer: int) -> None:
         if not isinstance(peer, int) or not 0 <= peer < self.nranks:
@@ -256,8 +259,12 @@ class DistContext:
         self._peer(dest)
         data = pickle.dumps((tag, bytes(payload)))
         n = torch.tensor([len(data)], dtype=torch.int64)
-        self._dist.send(n, dest, group=self._group)
-        self._dist.send(torch.frombuffer(bytearray(data), dtype=torch.uint8), dest, group=self._group)
+        body = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+        # non-blocking: the reference protocol sends to every peer before receiving
+        # (functionspace.py:77-93); a blocking gloo send would deadlock it
+        works = [self._dist.isend(n, dest, group=self._group), self._dist.isend(body, dest, group=self._group)]
+        self._inflight.append((works, n, body))
+        self._inflight = [w for w in self._inflight if not all(x.is_completed() for x in w[0])]
         self.messages_sent += 1
         self.bytes_sent += len(payload)
 
@@ -278,7 +285,14 @@ class DistContext:
             self._dist.recv(buf, source, group=self._group)
             q.append(pickle.loads(buf.numpy().tobytes()))
 
+    def flush(self) -> None:
+        for works, _, _ in self._inflight:
+            for w in works:
+                w.wait()
+        self._inflight = []
+
     def barrier(self) -> None:
+        self.flush()
         self._dist.barrier(group=self._group)
 
     def gather_to_root(self, payload: bytes) -> Optional[List[bytes]]:
@@ -296,6 +310,7 @@ class DistContext:
         return data
 
     def share(self, value: Any) -> List[Any]:
+        self.flush()
         out: List[Any] = [None] * self.nranks
         self._dist.all_gather_object(out, value, group=self._group)
         return out

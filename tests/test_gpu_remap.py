@@ -127,7 +127,7 @@ def test_apply_variants_multifield_bitwise(gpu):
         srcs = [DeviceArray(mesh.nb_nodes, L, np.float64) for _ in hosts]
         for d, h in zip(srcs, hosts):
             d.upload(h)
-        for variant in (0, 1, 2):
+        for variant in (0, 2, 3):
             dsts = [DeviceArray(len(w), L, np.float64) for _ in hosts]
             sg.apply_remap_device(w, srcs, dsts, variant=variant)
             for d, h in zip(dsts, hosts):
@@ -199,3 +199,51 @@ def test_constant_field_exact(gpu):
     res = sg.run_ranks(4, prog)
     assert max(r[0] for r in res) <= 1e-14
     assert sum(r[1] for r in res) == 0  # zero messages during build + apply (interp.py:9-11)
+
+
+def test_execute_host_pipeline_bitwise(gpu):
+    """sg_remap_execute_host: chunked h2d of referenced rows / apply / d2h equals the oracle
+    for any chunk count, and copies only referenced source rows."""
+    sg = gpu
+    from paper_1908_07038_b200.device import DeviceArray, PinnedArray
+    from paper_1908_07038_b200.interp import execute_host
+
+    S, T = sg.grid_from_name("O160"), sg.grid_from_name("O80")
+    dist = sg.blocks_partition(S, 1)
+    mesh = sg.generate_mesh(S, dist, 0, halo=2, include_pole=True)
+    w = sg.build_remap(sg.NodeColumns(mesh, None), T, sg.matching_partition(T, S, dist))
+    L = 137
+    hs = PinnedArray((mesh.nb_nodes, L))
+    hs.array[:] = np.random.default_rng(3).normal(size=hs.array.shape)
+    exp = O.apply_remap(w.nodes, w.weights, hs.array)
+    for nchunks in (1, 3, 17):
+        hd = PinnedArray((len(w), L))
+        ds, dd = DeviceArray(mesh.nb_nodes, L, np.float64), DeviceArray(len(w), L, np.float64)
+        rows = execute_host(w, [hs.array], [hd.array], [ds], [dd], nchunks=nchunks)
+        assert np.array_equal(hd.array.view(np.uint64), exp.view(np.uint64)), nchunks
+        assert w.distinct_sources() <= rows <= mesh.nb_nodes
+
+
+def test_apply_range(gpu):
+    sg = gpu
+    import ctypes as C
+
+    import paper_1908_07038_b200._native as N
+    from paper_1908_07038_b200.device import DeviceArray
+
+    S, T = sg.grid_from_name("O32"), sg.grid_from_name("O16")
+    dist = sg.blocks_partition(S, 1)
+    mesh = sg.generate_mesh(S, dist, 0, halo=0, include_pole=True)
+    w = sg.build_remap(sg.NodeColumns(mesh, None), T, sg.matching_partition(T, S, dist))
+    h = np.random.default_rng(9).normal(size=(mesh.nb_nodes, 21))
+    src, dst = DeviceArray(mesh.nb_nodes, 21, np.float64), DeviceArray(len(w), 21, np.float64)
+    src.upload(h)
+    s = np.array([src.handle], np.uint64)
+    d = np.array([dst.handle], np.uint64)
+    sh = w.device_stencil(0)
+    N.call("sg_remap_apply_range", sh, N.ptr(s), N.ptr(d), 1, 100, 700, 0, 0)
+    got = dst.to_numpy()
+    exp = O.apply_remap(w.nodes, w.weights, h)
+    assert np.array_equal(got[100:700].view(np.uint64), exp[100:700].view(np.uint64))
+    assert not got[:100].any() and not got[700:].any()
+    assert N.lib.sg_remap_apply_range(sh, N.ptr(s), N.ptr(d), 1, 5, len(w) + 1, 0, 0) == N.SG_INVALID_ARGUMENT

@@ -1,0 +1,151 @@
+"""Rank runtimes and the exchange-plan protocol on CPU: the thread runtime (run_ranks,
+parallel.py:1-195 contract) and DistContext over torch.distributed/gloo with world_size
+> 1, each building the reference's halo plans (checked against golden fixtures)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_1908_07038_b200 as sg
+from conftest import load_golden
+
+
+def test_send_receive_tags_fifo_and_counters():
+    def prog(ctx):
+        if ctx.rank == 0:
+            ctx.send(1, 7, b"a")
+            ctx.send(1, 8, b"bb")
+            ctx.send(1, 7, b"c")
+            return ctx.messages_sent, ctx.bytes_sent
+        got = [ctx.receive(0, 8), ctx.receive(0, 7), ctx.receive(0, 7)]
+        return got, ctx.messages_received
+
+    r = sg.run_ranks(2, prog)
+    assert r[0] == (3, 4)
+    assert r[1] == ([b"bb", b"a", b"c"], 3)
+
+
+def test_deadlock_detected_and_unconsumed():
+    with pytest.raises(sg.DeadlockDetected):
+        sg.run_ranks(2, lambda ctx: ctx.receive(1 - ctx.rank, 1))
+    with pytest.raises(sg.UnconsumedMessages):
+        sg.run_ranks(2, lambda ctx: ctx.send(1, 3, b"x") if ctx.rank == 0 else None)
+    with pytest.raises(sg.InvalidRank):
+        sg.run_ranks(1, lambda ctx: ctx.send(0, 1, b""))
+
+
+def test_gather_broadcast_barrier_share():
+    def prog(ctx):
+        parts = ctx.gather_to_root(bytes([ctx.rank]))
+        b = ctx.broadcast_from_root(b"root" if ctx.rank == 0 else None)
+        ctx.barrier()
+        s = ctx.share(ctx.rank * 10)
+        return parts, b, s
+
+    r = sg.run_ranks(3, prog)
+    assert r[0][0] == [b"\x00", b"\x01", b"\x02"] and r[1][0] is None
+    assert all(x[1] == b"root" for x in r)
+    assert all(x[2] == [0, 10, 20] for x in r)
+
+
+def test_error_propagates():
+    def prog(ctx):
+        if ctx.rank == 1:
+            raise ValueError("boom")
+        ctx.receive(1, 5)
+
+    with pytest.raises(ValueError):
+        sg.run_ranks(2, prog)
+
+
+@pytest.mark.parametrize("name,src", [("part_O32_O16_p4_h2", "O32"), ("part_F8_F4_p3_h1", "F8")])
+def test_thread_plan_build_matches_reference(name, src):
+    z = load_golden(name)
+    S = sg.grid_with_latitudes(src, z["src_lat"])
+    P, halo = int(z["nparts"]), int(z["halo"])
+
+    def prog(ctx):
+        mesh = sg.generate_mesh(S, sg.blocks_partition(S, ctx.nranks), ctx.rank, halo=halo, include_pole=True)
+        plan = sg.NodeColumns(mesh, ctx).exchange_plan
+        for p in range(ctx.nranks):
+            assert (p in plan.send) == (f"r{ctx.rank}_send_{p}" in z)
+            if p in plan.send:
+                assert np.array_equal(plan.send[p], z[f"r{ctx.rank}_send_{p}"])
+            if p in plan.recv:
+                assert np.array_equal(plan.recv[p], z[f"r{ctx.rank}_recv_{p}"])
+                # pull-kernel source rows: the owner's send list for us, in the same order
+                assert len(plan.recv_remote[p]) == len(plan.recv[p])
+        return plan, ctx.messages_sent
+
+    res = sg.run_ranks(P, prog)
+    for r, (plan, msgs) in enumerate(res):
+        assert msgs == P - 1  # one request per other rank (functionspace.py:77-81)
+        for p, rem in plan.recv_remote.items():
+            assert np.array_equal(rem, res[p][0].send[r])
+
+
+def test_inconsistent_mesh_detected():
+    g = sg.grid_from_name("F8")
+
+    def prog(ctx):
+        mesh = sg.generate_mesh(g, sg.blocks_partition(g, 2), ctx.rank, halo=1, include_pole=True)
+        if ctx.rank == 1:
+            mesh.node_global[mesh.node_ghost] += 1  # ask for ids rank 0 does not own
+            mesh.node_global[-1] = 10**6
+        return sg.NodeColumns(mesh, ctx)
+
+    with pytest.raises(sg.InconsistentMesh):
+        sg.run_ranks(2, prog)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ.setdefault("GLOO_SOCKET_IFNAME", "lo")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        z = load_golden("part_F8_F4_p3_h1")
+        S = sg.grid_with_latitudes("F8", z["src_lat"])
+        ctx = sg.DistContext()
+        mesh = sg.generate_mesh(S, sg.blocks_partition(S, world), rank, halo=int(z["halo"]), include_pole=True)
+        plan = sg.NodeColumns(mesh, ctx).exchange_plan
+        ok = all(np.array_equal(plan.send[p], z[f"r{rank}_send_{p}"]) for p in plan.send)
+        ok &= all(np.array_equal(plan.recv[p], z[f"r{rank}_recv_{p}"]) for p in plan.recv)
+        ok &= set(plan.send) == {p for p in range(world) if f"r{rank}_send_{p}" in z}
+        gathered = ctx.gather_to_root(bytes([rank]))
+        b = ctx.broadcast_from_root(b"xy" if rank == 0 else None)
+        shared = ctx.share(rank + 100)
+        q.put((rank, bool(ok), ctx.messages_sent, gathered, b, shared))
+        ctx.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distcontext_gloo_world3_plan_build():
+    import torch.multiprocessing as mp
+
+    world = 3
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(o[1] for o in out)
+    assert out[0][3] == [b"\x00", b"\x01", b"\x02"]
+    assert all(o[4] == b"xy" for o in out)
+    assert all(o[5] == [100, 101, 102] for o in out)
