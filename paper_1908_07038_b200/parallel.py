@@ -231,9 +231,16 @@ class DistContext:
     Host messages (plan build, gather) travel on a gloo group as uint8 tensors; counters
     mirror the reference.  ``device_exchange`` uses the library's NCCL communicator."""
 
-    def __init__(self, group=None, device: Optional[int] = None):
+    def __init__(self, group=None, device: Optional[int] = None, transport: str = "nccl"):
+        """transport: "nccl" (pack -> grouped ncclSend/ncclRecv -> unpack, stream-ordered) or
+        "ipc" (fused pull kernel over CUDA-IPC mappings of the owners' fields, host barriers
+        around it; works for several processes on one GPU too)."""
         import torch.distributed as dist
 
+        if transport not in ("nccl", "ipc"):
+            raise ValueError(f"unknown transport {transport!r}")
+        self.transport = transport
+        self._ipc: Dict[int, list] = {}
         self._dist = dist
         self.rank = dist.get_rank()
         self.nranks = dist.get_world_size()
@@ -331,6 +338,37 @@ class DistContext:
             self._comm = N.Handle(h.value)
         return self._comm.handle
 
+    def _peer_fields(self, dev_array) -> list:
+        """(ptr, pitch, device) of every rank's copy of this field, via CUDA IPC (cached)."""
+        import ctypes as C
+
+        from . import _native as N
+
+        got = self._ipc.get(dev_array.handle)
+        if got is None:
+            h = (C.c_uint8 * 64)()
+            N.call("sg_ipc_handle", dev_array.handle, N.ref(h), 64)
+            everyone = self.share((bytes(h), dev_array.pitch, dev_array.device))
+            got = []
+            for r, (blob, pitch, dev) in enumerate(everyone):
+                if r == self.rank:
+                    got.append((dev_array.ptr, dev_array.pitch, dev_array.device))
+                    continue
+                p = C.c_uint64(0)
+                hb = (C.c_uint8 * 64).from_buffer_copy(blob)
+                N.call("sg_ipc_open", dev_array.device, N.ref(hb), 64, N.ref(p))
+                got.append((p.value, pitch, dev))
+            self._ipc[dev_array.handle] = got
+        return got
+
     def device_exchange(self, plan, dev_array, stream: int = 0) -> None:
-        plan.exchange_nccl(dev_array, self.nccl_comm(), stream)
+        if self.transport == "nccl":
+            plan.exchange_nccl(dev_array, self.nccl_comm(), stream)
+            D.synchronize(dev_array.device, stream)
+            return
+        peers = self._peer_fields(dev_array)
         D.synchronize(dev_array.device, stream)
+        self.barrier()  # every owner's rows are final
+        plan.pull(dev_array, peers)
+        D.synchronize(dev_array.device, stream)
+        self.barrier()  # nobody overwrites owned rows while a peer still reads them

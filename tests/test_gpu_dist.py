@@ -1,0 +1,69 @@
+"""One process per rank over torch.distributed (gloo host messages) with the device halo
+exchange through CUDA-IPC mappings and the fused pull kernel.  Two processes share the one
+GPU of the test box (IPC works within a device; the exchange is host-barrier synchronised,
+no kernel waits on another)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.setdefault("GLOO_SOCKET_IFNAME", "lo")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1908_07038_b200 as sg
+
+        sg.set_device(0)
+        ctx = sg.DistContext(device=0, transport="ipc")
+        g = sg.grid_from_name("O32")
+        mesh = sg.generate_mesh(g, sg.blocks_partition(g, world), rank, halo=2, include_pole=True)
+        fs = sg.NodeColumns(mesh, ctx)
+        f = fs.create_field("x", 137)
+        owned = fs.owned_row_index()
+        f.host[owned] = mesh.node_global[owned, None] * 1.0 + np.arange(137)[None, :] / 137
+        f.allocate_device()
+        fs.halo_exchange_device(f, ctx)
+        f.update_host()
+        ok = np.array_equal(f.host, mesh.node_global[:, None] * 1.0 + np.arange(137)[None, :] / 137)
+        # host entry point through the same transport (staging copy)
+        h = fs.create_field("y", 3, sg.Kind.INT64)
+        h.host[owned] = mesh.node_global[owned, None]
+        fs.halo_exchange(h, ctx)
+        ok2 = np.array_equal(h.host, np.repeat(mesh.node_global[:, None], 3, axis=1))
+        q.put((rank, bool(ok), bool(ok2), ctx.messages_sent))
+        ctx.barrier()
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, False, False, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ipc_pull_exchange_processes(gpu, world):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(o[1] and o[2] for o in out), out

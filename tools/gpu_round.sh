@@ -8,6 +8,7 @@ echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 300 python bench.py --steps 20 --warmup 5 --variant 2 --no-cpu-baseline > gpurun_out/bench_v2.json 2> gpurun_out/bench_v2.err
+timeout 300 python bench.py --steps 20 --warmup 5 --config cfg2 --no-cpu-baseline > gpurun_out/bench_cfg2.json 2> gpurun_out/bench_cfg2.err
 if [ "${NCU:-1}" = "1" ]; then
   timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
