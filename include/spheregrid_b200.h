@@ -68,6 +68,13 @@ int32_t sg_host_free(uint64_t ptr);
 int32_t sg_event_create(int32_t device, uint64_t* out_event);
 int32_t sg_event_record(uint64_t event, uint64_t stream);
 int32_t sg_event_elapsed_ms(uint64_t start, uint64_t end, float* out_ms);
+/* streams (non-blocking; released with sg_release), cross-stream waits on events, and CUDA
+ * graphs of a captured steady-state step (the multi-GPU exchange + apply). */
+int32_t sg_stream_create(int32_t device, uint64_t* out_handle, uint64_t* out_stream);
+int32_t sg_stream_wait_event(uint64_t stream, uint64_t event);
+int32_t sg_graph_begin(int32_t device, uint64_t stream);
+int32_t sg_graph_end(int32_t device, uint64_t stream, uint64_t* out_graph);
+int32_t sg_graph_launch(uint64_t graph, uint64_t stream);
 int32_t sg_field_info(uint64_t field, int32_t* out_device, int64_t* out_npts,
                       int32_t* out_levels, int64_t* out_pitch_elems, uint64_t* out_devptr);
 

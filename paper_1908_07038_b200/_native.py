@@ -42,6 +42,11 @@ _SIGS = {
     "sg_event_create": [i32, vp],
     "sg_event_record": [u64, u64],
     "sg_event_elapsed_ms": [u64, u64, vp],
+    "sg_stream_create": [i32, vp, vp],
+    "sg_stream_wait_event": [u64, u64],
+    "sg_graph_begin": [i32, u64],
+    "sg_graph_end": [i32, u64, vp],
+    "sg_graph_launch": [u64, u64],
     "sg_locator_create": [i32, vp, i64, vp, vp, i64, vp],
     "sg_locator_stats": [u64, vp, vp, vp, vp],
     "sg_locator_locate": [u64, vp, i64, vp, vp],

@@ -133,6 +133,13 @@ struct Event : Object {
 };
 }  // namespace
 
+}  // extern "C"
+
+// raw event of a registry handle (runtime.cu: cross-stream waits)
+cudaEvent_t sg_event_raw(uint64_t h) { return get<Event>(h, ObjKind::Event)->ev; }
+
+extern "C" {
+
 int32_t sg_host_alloc(size_t bytes, uint64_t* out_ptr) {
   SG_API_BEGIN
   SG_REQUIRE(out_ptr, "null out pointer");

@@ -135,3 +135,43 @@ class Event(N.Handle):
         ms = C.c_float(0)
         N.call("sg_event_elapsed_ms", start.handle, end.handle, N.ref(ms))
         return float(ms.value)
+
+
+class Stream(N.Handle):
+    """A non-blocking CUDA stream owned by the library; ``.stream`` is the raw handle every
+    sg_* call accepts."""
+
+    __slots__ = ("device", "stream")
+
+    def __init__(self, device: int = None):
+        dev = current_device() if device is None else device
+        h, s = C.c_uint64(0), C.c_uint64(0)
+        N.call("sg_stream_create", dev, N.ref(h), N.ref(s))
+        super().__init__(h.value)
+        self.device, self.stream = dev, s.value
+
+    def wait(self, event: "Event") -> None:
+        N.call("sg_stream_wait_event", self.stream, event.handle)
+
+    def synchronize(self) -> None:
+        synchronize(self.device, self.stream)
+
+
+class Graph(N.Handle):
+    """A captured sequence of stream work (cudaStreamBeginCapture ... EndCapture),
+    instantiated once and replayed with ``launch``."""
+
+    __slots__ = ("device",)
+
+    def __init__(self, device: int, stream: int, body):
+        N.call("sg_graph_begin", device, stream)
+        try:
+            body()
+        finally:
+            h = C.c_uint64(0)
+            N.call("sg_graph_end", device, stream, N.ref(h))
+        super().__init__(h.value)
+        self.device = device
+
+    def launch(self, stream: int) -> None:
+        N.call("sg_graph_launch", self.handle, stream)

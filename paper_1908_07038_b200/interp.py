@@ -236,6 +236,16 @@ def apply_remap_device(weights: InterpolationWeights, sources: Sequence[DeviceAr
     N.call("sg_remap_apply", sh, N.ptr(s), N.ptr(t), len(s), variant, stream)
 
 
+def apply_remap_range(weights: InterpolationWeights, sources: Sequence[DeviceArray], targets: Sequence[DeviceArray],
+                      t0: int, t1: int, variant: int = APPLY_DEFAULT, stream: int = 0) -> None:
+    """apply_remap_device restricted to targets [t0, t1) (sg_remap_apply_range)."""
+    dev = sources[0].device
+    sh = weights.device_stencil(dev)
+    s = np.array([a.handle for a in sources], np.uint64)
+    t = np.array([a.handle for a in targets], np.uint64)
+    N.call("sg_remap_apply_range", sh, N.ptr(s), N.ptr(t), len(s), t0, t1, variant, stream)
+
+
 def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], host_dst: Sequence[np.ndarray],
                  dev_src: Sequence[DeviceArray], dev_dst: Sequence[DeviceArray], nchunks: int = 0,
                  variant: int = APPLY_DEFAULT) -> int:

@@ -247,3 +247,39 @@ def test_apply_range(gpu):
     assert np.array_equal(got[100:700].view(np.uint64), exp[100:700].view(np.uint64))
     assert not got[:100].any() and not got[700:].any()
     assert N.lib.sg_remap_apply_range(sh, N.ptr(s), N.ptr(d), 1, 5, len(w) + 1, 0, 0) == N.SG_INVALID_ARGUMENT
+
+
+def test_distributed_remap_ranges_and_graph(gpu):
+    """execute.DistributedRemap on one rank of a P=4 decomposition: interior block + boundary
+    ranges, eager and replayed from a captured CUDA graph, equal the oracle bitwise."""
+    sg = gpu
+    from paper_1908_07038_b200.device import DeviceArray
+    from paper_1908_07038_b200.execute import DistributedRemap, interior_block
+
+    S, T = sg.grid_from_name("O64"), sg.grid_from_name("O32")
+    dist = sg.blocks_partition(S, 4)
+    td = sg.matching_partition(T, S, dist)
+    mesh = sg.generate_mesh(S, dist, 1, halo=2, include_pole=True)
+    fs = sg.NodeColumns(mesh, None)
+    w = sg.build_remap(fs, T, td)
+    b0, b1 = interior_block(w, mesh.nb_owned_nodes)
+    assert 0 < b0 < b1 < len(w)
+    assert (w.nodes[b0:b1] < mesh.nb_owned_nodes).all()
+    h = np.random.default_rng(11).normal(size=(mesh.nb_nodes, 137))
+    src, dst = DeviceArray(mesh.nb_nodes, 137, np.float64), DeviceArray(len(w), 137, np.float64)
+    src.upload(h)
+    exp = O.apply_remap(w.nodes, w.weights, h)
+    run = DistributedRemap(fs, w, None, src, dst)
+    run.step()
+    run.synchronize()
+    assert np.array_equal(dst.to_numpy().view(np.uint64), exp.view(np.uint64))
+    dst2 = DeviceArray(len(w), 137, np.float64)
+    run2 = DistributedRemap(fs, w, None, src, dst2)
+    run2.step()
+    run2.synchronize()
+    run2.capture()
+    for _ in range(3):
+        run2.step()
+    run2.synchronize()
+    assert np.array_equal(dst2.to_numpy().view(np.uint64), exp.view(np.uint64))
+    assert run2.launches_per_step == 3
