@@ -34,11 +34,25 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    # name: (source, target, levels, fields)
+    # name: (source, target, levels, fields[, method])
     "cfg3": ("O1280", "O640", 137, 1),
     "cfg2": ("O320", "O160", 137, 4),
     "cfg1": ("O32", "O16", 10, 1),
+    # structured bilinear: no reference method (parity vs oracle.bilinear_stencil only)
+    "cfg5": ("O2560", "O1280", 137, 1, "bilinear"),
 }
+
+
+def metric_name(source, target, method, L):
+    if (source, target, method, L) == ("O1280", "O640", "fe", 137):
+        return METRIC
+    kind = "structured-bilinear" if method == "bilinear" else "FE"
+    return f"Gpts·lev/s {source}→{target} {kind} interp, {L} lev fp64"
+
+
+def config(name):
+    c = CONFIGS[name]
+    return c[0], c[1], c[2], c[3], (c[4] if len(c) > 4 else "fe")
 METRIC = "Gpts·lev/s O1280→O640 FE interp, 137 lev fp64"
 
 
@@ -128,13 +142,16 @@ def fill_smooth(out: np.ndarray, xyz: np.ndarray, field_index: int, rows=None) -
         out[r] = basis[:, cols] * fac
 
 
-def setup_remap(sg, source, target, nparts, rank, ctx):
+def setup_remap(sg, source, target, nparts, rank, ctx, method="fe"):
     S, T = sg.grid_from_name(source), sg.grid_from_name(target)
     dist = sg.blocks_partition(S, nparts)
     mesh = sg.generate_mesh(S, dist, rank, halo=2, include_pole=True)  # cli.py:131
     fs = sg.NodeColumns(mesh, ctx)
     tdist = sg.matching_partition(T, S, dist)
-    w = sg.build_remap(fs, T, tdist, ctx)
+    if method == "bilinear":
+        w = sg.build_bilinear(fs, T, tdist, ctx)
+    else:
+        w = sg.build_remap(fs, T, tdist, ctx)
     return S, T, mesh, fs, tdist, w
 
 
@@ -150,7 +167,7 @@ def cpu_apply(nodes, weights, src, out, nthreads):
 
     def job(s):
         sl = slice(s, min(s + chunk, m))
-        out[sl] = O.apply_remap(nodes[sl], weights[sl], src)
+        out[sl] = O.apply_remap_k(nodes[sl], weights[sl], src)
 
     if nthreads <= 1:
         for s in range(0, m, chunk):
@@ -160,9 +177,9 @@ def cpu_apply(nodes, weights, src, out, nthreads):
         list(ex.map(job, range(0, m, chunk)))
 
 
-def algorithmic_bytes(U, m, L, F):
-    """F·(U·L·8 + m·L·8) + m·(3·4 + 3·8)."""
-    return F * (U * L * 8 + m * L * 8) + m * 36
+def algorithmic_bytes(U, m, L, F, k=3):
+    """F·(U·L·8 + m·L·8) + m·k·(4 + 8), k = stencil points."""
+    return F * (U * L * 8 + m * L * 8) + m * k * 12
 
 
 # ------------------------------------------------------------------------------------------
@@ -173,12 +190,12 @@ def run_reference(args):
         return
     import paper_1908_07038_b200 as sg
 
-    source, target, L, F = CONFIGS[args.config]
+    source, target, L, F, method = config(args.config)
     sg.set_device(0)
     t0 = time.time()
     # stencils: built once on the GPU (untimed setup; at cfg3 the CPU apply
     # runs on the new build's stencils, verified bit-exact against the reference's locate)
-    S, T, mesh, fs, tdist, w = setup_remap(sg, source, target, 1, 0, None)
+    S, T, mesh, fs, tdist, w = setup_remap(sg, source, target, 1, 0, None, method)
     nodes, weights = w.nodes, w.weights
     srcs = []
     for f in range(F):
@@ -201,11 +218,12 @@ def run_reference(args):
     ms = 1e3 * sum(times) / len(times)
     value = units / (ms * 1e-3) / 1e9
     line = {
-        "metric": METRIC, "value": value, "unit": "Gpts·lev/s", "n_gpus": args.gpus, "steps": args.steps,
+        "metric": metric_name(source, target, method, L), "value": value, "unit": "Gpts·lev/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
         "impl": "reference",
-        "config": {"workload": f"{source}->{target} FE remap apply, {L} levels x {F} field(s), P=1",
+        "config": {"workload": f"{source}->{target} {'structured-bilinear' if method == 'bilinear' else 'FE'} remap "
+                               f"apply, {L} levels x {F} field(s), P=1",
                    "levels": L, "fields": F, "targets": len(w), "source_nodes": mesh.nb_nodes},
         "cpu_baseline": {"value": value, "unit": "Gpts·lev/s", "cores": nthreads, "kind": "port",
                          "sample": f"full {source}->{target} apply per step (oracle port of interp.py:219-223, "
@@ -220,11 +238,11 @@ def run_single(args):
     import paper_1908_07038_b200 as sg
     from paper_1908_07038_b200.device import DeviceArray, Event, PinnedArray
 
-    source, target, L, F = CONFIGS[args.config]
+    source, target, L, F, method = config(args.config)
     dev = 0
     sg.set_device(dev)
     t0 = time.time()
-    S, T, mesh, fs, tdist, w = setup_remap(sg, source, target, 1, 0, None)
+    S, T, mesh, fs, tdist, w = setup_remap(sg, source, target, 1, 0, None, method)
     m, n = len(w), mesh.nb_nodes
     U = w.distinct_sources()
     log(f"setup {time.time() - t0:.1f}s: {n} source nodes, {m} targets, U={U}")
@@ -263,7 +281,7 @@ def run_single(args):
 
     samp = np.random.default_rng(7).choice(m, size=min(m, 4096), replace=False)
     got = ddst[0].to_numpy()[samp]
-    exp = O.apply_remap(w.nodes[samp], w.weights[samp], hsrc[0].array)
+    exp = O.apply_remap_k(w.nodes[samp], w.weights[samp], hsrc[0].array)
     bitwise = bool(np.array_equal(got.view(np.uint64), exp.view(np.uint64)))
 
     # ---- e2e through the public API: host fields in pinned memory -------------------------
@@ -297,14 +315,15 @@ def run_single(args):
                          f"interp.py:219-223, single-threaded like the reference)"}
 
     peak, peak_src = measured_peak()
-    B = algorithmic_bytes(U, m, L, F)
+    B = algorithmic_bytes(U, m, L, F, w.nodes.shape[1])
     kern_ms = statistics.mean(launch_ms)
     achieved = B / (kern_ms * 1e-3) / 1e9
     line = {
-        "metric": METRIC, "value": value, "unit": "Gpts·lev/s", "n_gpus": 1, "steps": args.steps,
+        "metric": metric_name(source, target, method, L), "value": value, "unit": "Gpts·lev/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
-        "config": {"workload": f"{source}->{target} FE remap apply, {L} levels x {F} field(s), P=1",
+        "config": {"workload": f"{source}->{target} {'structured-bilinear' if method == 'bilinear' else 'FE'} remap "
+                               f"apply, {L} levels x {F} field(s), P=1",
                    "levels": L, "fields": F, "targets": m, "source_nodes": n, "distinct_sources": U,
                    "parallelism": "single GPU", "l2": "inputs 7.3 GB > 126 MB L2 (no flush needed)",
                    "variant": args.variant},
@@ -340,9 +359,9 @@ def run_multi(args):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     sg.set_device(local)
     ctx = sg.DistContext(device=local, transport="nccl")
-    source, target, L, F = CONFIGS[args.config]
+    source, target, L, F, method = config(args.config)
     t0 = time.time()
-    S, T, mesh, fs, tdist, w = setup_remap(sg, source, target, world, rank, ctx)
+    S, T, mesh, fs, tdist, w = setup_remap(sg, source, target, world, rank, ctx, method)
     m, n = len(w), mesh.nb_nodes
     n_owned = mesh.nb_owned_nodes
     hsrc = PinnedArray((n, L))
@@ -422,7 +441,7 @@ def run_multi(args):
         units = msum * L
         value = units / (ms * 1e-3) / 1e9
         line = {
-            "metric": METRIC, "value": value, "unit": "Gpts·lev/s", "n_gpus": world, "steps": args.steps,
+            "metric": metric_name(source, target, method, L), "value": value, "unit": "Gpts·lev/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
             "config": {"workload": f"{source}->{target} FE remap, {L} levels, blocks_partition P={world}, halo 2; "

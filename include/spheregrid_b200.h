@@ -110,6 +110,20 @@ int32_t sg_remap_build(uint64_t locator, const double* target_xyz, int64_t m,
                        uint8_t* out_fallback, uint8_t* out_status, int64_t* out_first_bad);
 int32_t sg_stencil_create(int32_t device, const int64_t* nodes, const double* weights,
                           int64_t m, int64_t source_nnodes, uint64_t* out_stencil);
+/* k-point stencils: k = 3 (FE) or 4 (structured bilinear); nodes/weights are [m][k]. */
+int32_t sg_stencil_create_k(int32_t device, const int64_t* nodes, const double* weights,
+                            int64_t m, int32_t k, int64_t source_nnodes, uint64_t* out_stencil);
+/* Structured-bilinear stencils (BASELINE configs[4]; no reference counterpart — defined in
+ * csrc/bilinear.cu and restated in oracle/oracle.py:bilinear_stencil, parity unpinned vs
+ * the reference): bracketing rows of the source grid, linear in longitude per row, linear
+ * in latitude, polar caps through the pole nodes.  node_global: the local mesh's global ids
+ * (mesh.py node_global) so the 4 nodes come back as local rows; target_lonlat (m, 2) in
+ * degrees.  NotLocated (status 1, *out_first_bad) if a node is not in the local mesh. */
+int32_t sg_bilinear_build(int32_t device, int32_t nrows, const double* lat_deg,
+                          const int64_t* nlons, int32_t has_poles, const int64_t* node_global,
+                          int64_t n_nodes, const double* target_lonlat, int64_t m,
+                          uint64_t* out_stencil, int64_t* out_nodes, double* out_weights,
+                          uint8_t* out_status, int64_t* out_first_bad);
 int32_t sg_stencil_info(uint64_t stencil, int64_t* out_m, int64_t* out_source_nnodes,
                         int64_t* out_distinct_sources);
 

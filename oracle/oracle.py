@@ -148,3 +148,57 @@ def gaussian_latitudes(n: int) -> np.ndarray:
         out.append(min(cands, key=lambda c: abs(legendre_p(m, math.sin(math.radians(c))))))
     north = np.array(out)
     return np.concatenate([north, -north[::-1]])
+
+
+def apply_remap_k(nodes: np.ndarray, weights: np.ndarray, src: np.ndarray) -> np.ndarray:
+    """k-point apply, summed left to right: ((w0*s0 + w1*s1) + w2*s2) [+ w3*s3]."""
+    out = weights[:, 0:1] * src[nodes[:, 0]] + weights[:, 1:2] * src[nodes[:, 1]]
+    for k in range(2, nodes.shape[1]):
+        out = out + weights[:, k:k + 1] * src[nodes[:, k]]
+    return out
+
+
+def bilinear_stencil(lat: np.ndarray, nlons: np.ndarray, lonlat: np.ndarray, has_poles: bool):
+    """Structured-bilinear stencils — NOT a reference function (the reference has no bilinear
+    method; parity unpinned).  CPU restatement of the definition in
+    paper_1908_07038_b200/csrc/bilinear.cu: returns (global nodes (m, 4), weights (m, 4),
+    located (m,))."""
+    lat = np.asarray(lat, float)
+    nlons = np.asarray(nlons, np.int64)
+    off = np.concatenate([[0], np.cumsum(nlons)])
+    npts = int(off[-1])
+    lam, phi = lonlat[:, 0], lonlat[:, 1]
+    m = len(lonlat)
+    nodes = np.zeros((m, 4), np.int64)
+    w = np.zeros((m, 4))
+    ok = np.ones(m, bool)
+
+    def row_pair(j, lam_):
+        n = nlons[j]
+        x = (lam_ * n.astype(float)) / 360.0
+        i = np.clip(np.floor(x).astype(np.int64), 0, n - 1)
+        a = x - i.astype(float)
+        return off[j] + i, off[j] + (i + 1) % n, a
+
+    north, south = phi > lat[0], phi < lat[-1]
+    inner = ~(north | south)
+    j = np.searchsorted(-lat, -phi[inner], side="right") - 1
+    j = np.minimum(j, len(lat) - 2)
+    beta = (lat[j] - phi[inner]) / (lat[j] - lat[j + 1])
+    ia, ib, a0 = row_pair(j, lam[inner])
+    ic, id_, a1 = row_pair(j + 1, lam[inner])
+    ob = 1.0 - beta
+    nodes[inner] = np.stack([ia, ib, ic, id_], 1)
+    w[inner] = np.stack([ob * (1.0 - a0), ob * a0, beta * (1.0 - a1), beta * a1], 1)
+    for cap, jj, pole in ((north, 0, npts), (south, len(lat) - 1, npts + 1)):
+        if not cap.any():
+            continue
+        if not has_poles:
+            ok[cap] = False
+            continue
+        p = phi[cap]
+        beta = (90.0 - p) / (90.0 - lat[0]) if jj == 0 else (p + 90.0) / (lat[jj] + 90.0)
+        ia, ib, a = row_pair(np.full(cap.sum(), jj), lam[cap])
+        nodes[cap] = np.stack([np.full(cap.sum(), pole), ia, ib, np.full(cap.sum(), pole)], 1)
+        w[cap] = np.stack([1.0 - beta, beta * (1.0 - a), beta * a, np.zeros(cap.sum())], 1)
+    return nodes, w, ok

@@ -53,6 +53,8 @@ _SIGS = {
     "sg_remap_build": [u64, vp, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp],
     "sg_stencil_create": [i32, vp, vp, i64, i64, vp],
     "sg_stencil_info": [u64, vp, vp, vp],
+    "sg_stencil_create_k": [i32, vp, vp, i64, i32, i64, vp],
+    "sg_bilinear_build": [i32, i32, vp, vp, i32, vp, i64, vp, i64, vp, vp, vp, vp, vp],
     "sg_remap_apply": [u64, vp, vp, i32, i32, u64],
     "sg_remap_apply_range": [u64, vp, vp, i32, i64, i64, i32, u64],
     "sg_remap_execute_host": [u64, vp, vp, i32, vp, vp, i32, i32, vp],

@@ -35,6 +35,7 @@ struct ApplyArgs {
   const int4* idx;
   const double4* w;
   int64_t t0, t1;  // target range
+  int32_t k;       // stencil points: 3 (FE triangles) or 4 (structured bilinear)
   int32_t levels;
   int32_t nfields;
   const double* src[kMaxFields];
@@ -61,6 +62,10 @@ __device__ __forceinline__ double4 ldg_w4(const double4* p) {
 __device__ __forceinline__ double combine(double w0, double w1, double w2, double a, double b, double c) {
   // numpy: (w0*a + w1*b) + w2*c, each op rounded (interp.py:219-223)
   return __dadd_rn(__dadd_rn(__dmul_rn(w0, a), __dmul_rn(w1, b)), __dmul_rn(w2, c));
+}
+// 4-point stencils (structured bilinear): ((w0*a + w1*b) + w2*c) + w3*d, left to right
+__device__ __forceinline__ double combine4(double4 w, double a, double b, double c, double d) {
+  return __dadd_rn(combine(w.x, w.y, w.z, a, b, c), __dmul_rn(w.w, d));
 }
 
 // ---- warp per target, 16-B loads (even pitch) ------------------------------------------------
@@ -132,6 +137,45 @@ __global__ void __launch_bounds__(256) apply_warp_v1(ApplyArgs a) {
     for (int i = 0; i < ITERS; ++i) {
       const int k = lane + 32 * i;
       if (k < L) __stcs(outp + k, combine(wt.x, wt.y, wt.z, v0[i], v1[i], v2[i]));
+    }
+  }
+}
+
+// ---- 4-point stencils (structured bilinear, bilinear.cu): warp per target, 8-B loads -------
+template <int ITERS>
+__global__ void __launch_bounds__(256) apply4_warp(ApplyArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (t >= a.t1) return;
+  const int4 id = __ldg(a.idx + t);
+  const double4 wt = ldg_w4(a.w + t);
+  const int L = a.levels;
+  for (int f = 0; f < a.nfields; ++f) {
+    const double* r0 = a.src[f] + (int64_t)id.x * a.src_pitch[f];
+    const double* r1 = a.src[f] + (int64_t)id.y * a.src_pitch[f];
+    const double* r2 = a.src[f] + (int64_t)id.z * a.src_pitch[f];
+    const double* r3 = a.src[f] + (int64_t)id.w * a.src_pitch[f];
+    double* outp = a.dst[f] + t * a.dst_pitch[f];
+    if (ITERS > 0) {
+      double v0[ITERS > 0 ? ITERS : 1], v1[ITERS > 0 ? ITERS : 1], v2[ITERS > 0 ? ITERS : 1], v3[ITERS > 0 ? ITERS : 1];
+#pragma unroll
+      for (int i = 0; i < ITERS; ++i) {
+        const int k = lane + 32 * i;
+        if (k < L) {
+          v0[i] = ldg_stream1(r0 + k);
+          v1[i] = ldg_stream1(r1 + k);
+          v2[i] = ldg_stream1(r2 + k);
+          v3[i] = ldg_stream1(r3 + k);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < ITERS; ++i) {
+        const int k = lane + 32 * i;
+        if (k < L) __stcs(outp + k, combine4(wt, v0[i], v1[i], v2[i], v3[i]));
+      }
+    } else {
+      for (int l = lane; l < L; l += 32)
+        __stcs(outp + l, combine4(wt, ldg_stream1(r0 + l), ldg_stream1(r1 + l), ldg_stream1(r2 + l), ldg_stream1(r3 + l)));
     }
   }
 }
@@ -282,13 +326,14 @@ __global__ void __launch_bounds__(kBulkThreads) apply_bulk(ApplyArgs a, int slot
   }
 }
 
-__global__ void mark_sources(const int4* idx, int64_t m, unsigned char* mark) {
+__global__ void mark_sources(const int4* idx, int64_t m, int k, unsigned char* mark) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= m) return;
   const int4 id = idx[t];
   mark[id.x] = 1;
   mark[id.y] = 1;
   mark[id.z] = 1;
+  if (k == 4) mark[id.w] = 1;
 }
 
 __global__ void count_marks(const unsigned char* mark, int64_t n, unsigned long long* out) {
@@ -299,11 +344,13 @@ __global__ void count_marks(const unsigned char* mark, int64_t n, unsigned long 
   if ((threadIdx.x & 31) == 0) atomicAdd(out, c);
 }
 
-__global__ void pack_stencil(const int32_t* idx3, const double* w3, int64_t m, int4* idx, double4* w) {
+__global__ void pack_stencil(const int32_t* idxk, const double* wk, int64_t m, int k, int4* idx, double4* w) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= m) return;
-  idx[t] = make_int4(idx3[3 * t], idx3[3 * t + 1], idx3[3 * t + 2], 0);
-  w[t] = make_double4(w3[3 * t], w3[3 * t + 1], w3[3 * t + 2], 0.0);
+  const int32_t* i = idxk + k * t;
+  const double* x = wk + k * t;
+  idx[t] = make_int4(i[0], i[1], i[2], k == 4 ? i[3] : 0);
+  w[t] = make_double4(x[0], x[1], x[2], k == 4 ? x[3] : 0.0);
 }
 
 int num_sms() {
@@ -321,9 +368,23 @@ void launch_apply(ApplyArgs a, int variant, cudaStream_t st) {
   const int64_t m = a.t1 - a.t0;
   if (m <= 0) return;
   const int L = a.levels;
+  if (a.k == 4) {
+    const unsigned grid = (unsigned)((m + 7) / 8);
+    switch ((L + 31) / 32) {
+      case 1: apply4_warp<1><<<grid, 256, 0, st>>>(a); break;
+      case 2: apply4_warp<2><<<grid, 256, 0, st>>>(a); break;
+      case 3: apply4_warp<3><<<grid, 256, 0, st>>>(a); break;
+      case 4: apply4_warp<4><<<grid, 256, 0, st>>>(a); break;
+      case 5: apply4_warp<5><<<grid, 256, 0, st>>>(a); break;
+      case 6: apply4_warp<6><<<grid, 256, 0, st>>>(a); break;
+      default: apply4_warp<0><<<grid, 256, 0, st>>>(a); break;
+    }
+    SG_CUDA_LAUNCH();
+    return;
+  }
   bool even = true;
   for (int f = 0; f < a.nfields; ++f) even = even && a.src_pitch[f] % 2 == 0 && a.dst_pitch[f] % 2 == 0;
-  if (variant == 2 && L >= 2) {
+  if (variant == 2 && L >= 2 && a.k == 3) {
     const int slot = ((L + 2) * 8 + 15) / 16 * 2;  // doubles; holds the 16-B aligned superset
     const size_t stage_bytes = (size_t)3 * kTile * slot * 8;
     const int stages = (int)std::min<size_t>(8, std::max<size_t>(2, (size_t)(100 * 1024) / stage_bytes));
@@ -402,6 +463,7 @@ ApplyArgs make_args(const Stencil* s, const FieldPairs& p, int f0, int64_t t0, i
   a.w = s->w.as<double4>();
   a.t0 = t0;
   a.t1 = t1;
+  a.k = s->k;
   a.levels = p.levels;
   a.nfields = std::min<int>(kMaxFields, (int)p.src.size() - f0);
   for (int f = 0; f < a.nfields; ++f) {
@@ -443,6 +505,10 @@ HostPlan* host_plan(Stencil* s, int nchunks) {
     const int4 id = idx[t];
     mark[id.x] = mark[id.y] = mark[id.z] = 1;
     run_max = std::max<int64_t>(run_max, std::max(id.x, std::max(id.y, id.z)));
+    if (s->k == 4) {
+      mark[id.w] = 1;
+      run_max = std::max<int64_t>(run_max, id.w);
+    }
     pmax[t] = run_max;  // monotone: targets [0, t] need source rows <= pmax[t]
   }
   int64_t tprev = 0, rprev = 0;
@@ -508,7 +574,7 @@ void stencil_finalize(Stencil* s, const int32_t* d_idx3, const double* d_w3, cud
   s->idx.alloc(s->device, (size_t)std::max<int64_t>(s->m, 1) * sizeof(int4));
   s->w.alloc(s->device, (size_t)std::max<int64_t>(s->m, 1) * sizeof(double4));
   if (s->m > 0) {
-    pack_stencil<<<(unsigned)((s->m + 255) / 256), 256, 0, st>>>(d_idx3, d_w3, s->m, s->idx.as<int4>(),
+    pack_stencil<<<(unsigned)((s->m + 255) / 256), 256, 0, st>>>(d_idx3, d_w3, s->m, s->k, s->idx.as<int4>(),
                                                                  s->w.as<double4>());
     SG_CUDA_LAUNCH();
   }
@@ -518,7 +584,8 @@ void stencil_finalize(Stencil* s, const int32_t* d_idx3, const double* d_w3, cud
   SG_CUDA(cudaMemsetAsync(mark.ptr, 0, mark.bytes, st));
   SG_CUDA(cudaMemsetAsync(cnt.ptr, 0, cnt.bytes, st));
   if (s->m > 0) {
-    mark_sources<<<(unsigned)((s->m + 255) / 256), 256, 0, st>>>(s->idx.as<int4>(), s->m, mark.as<unsigned char>());
+    mark_sources<<<(unsigned)((s->m + 255) / 256), 256, 0, st>>>(s->idx.as<int4>(), s->m, s->k,
+                                                                 mark.as<unsigned char>());
     SG_CUDA_LAUNCH();
     count_marks<<<1024, 256, 0, st>>>(mark.as<unsigned char>(), s->source_nnodes, cnt.as<unsigned long long>());
     SG_CUDA_LAUNCH();
@@ -535,34 +602,41 @@ using namespace sg;
 
 extern "C" {
 
-int32_t sg_stencil_create(int32_t device, const int64_t* nodes, const double* weights, int64_t m,
-                          int64_t source_nnodes, uint64_t* out_stencil) {
+int32_t sg_stencil_create_k(int32_t device, const int64_t* nodes, const double* weights, int64_t m, int32_t k,
+                            int64_t source_nnodes, uint64_t* out_stencil) {
   SG_API_BEGIN
   SG_REQUIRE(out_stencil, "null out pointer");
+  SG_REQUIRE(k == 3 || k == 4, "stencils have 3 or 4 points, got %d", k);
   SG_REQUIRE(m >= 0 && source_nnodes >= 0, "negative size");
   SG_REQUIRE(m == 0 || (nodes && weights), "null stencil arrays");
   SG_REQUIRE(source_nnodes < (int64_t)INT32_MAX, "source mesh too large for int32 indices");
-  std::vector<int32_t> idx3((size_t)m * 3);
-  for (int64_t i = 0; i < m * 3; ++i) {
+  std::vector<int32_t> idxk((size_t)m * k);
+  for (int64_t i = 0; i < m * k; ++i) {
     SG_REQUIRE(nodes[i] >= 0 && nodes[i] < source_nnodes, "stencil node %lld out of range [0, %lld)",
                (long long)nodes[i], (long long)source_nnodes);
-    idx3[i] = (int32_t)nodes[i];
+    idxk[i] = (int32_t)nodes[i];
   }
   DeviceScope ds(device);
   auto s = std::make_unique<Stencil>();
   s->device = device;
   s->m = m;
+  s->k = k;
   s->source_nnodes = source_nnodes;
   DevBuf di, dw;
-  di.alloc(device, std::max<size_t>(idx3.size(), 1) * sizeof(int32_t));
-  dw.alloc(device, std::max<size_t>((size_t)m * 3, 1) * sizeof(double));
+  di.alloc(device, std::max<size_t>(idxk.size(), 1) * sizeof(int32_t));
+  dw.alloc(device, std::max<size_t>((size_t)m * k, 1) * sizeof(double));
   if (m) {
-    SG_CUDA(cudaMemcpy(di.ptr, idx3.data(), idx3.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-    SG_CUDA(cudaMemcpy(dw.ptr, weights, (size_t)m * 3 * sizeof(double), cudaMemcpyHostToDevice));
+    SG_CUDA(cudaMemcpy(di.ptr, idxk.data(), idxk.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    SG_CUDA(cudaMemcpy(dw.ptr, weights, (size_t)m * k * sizeof(double), cudaMemcpyHostToDevice));
   }
   stencil_finalize(s.get(), di.as<int32_t>(), dw.as<double>(), 0);
   *out_stencil = registry_put(s.release());
   SG_API_END
+}
+
+int32_t sg_stencil_create(int32_t device, const int64_t* nodes, const double* weights, int64_t m,
+                          int64_t source_nnodes, uint64_t* out_stencil) {
+  return sg_stencil_create_k(device, nodes, weights, m, 3, source_nnodes, out_stencil);
 }
 
 int32_t sg_stencil_info(uint64_t stencil, int64_t* out_m, int64_t* out_source_nnodes,

@@ -11,6 +11,7 @@ struct Stencil : Object {
   Stencil() : Object(ObjKind::Stencil) {}
   int device = 0;
   int64_t m = 0;
+  int32_t k = 3;                 // points per target: 3 (FE) or 4 (structured bilinear)
   int64_t source_nnodes = 0;
   int64_t distinct_sources = 0;  // U: distinct source rows referenced
   DevBuf idx;                    // int4[m]
@@ -20,8 +21,8 @@ struct Stencil : Object {
   ~Stencil() override { destroy_host_plan(); }
 };
 
-// Builds the device arrays from device-resident int32 index / fp64 weight triples and
-// counts distinct referenced source rows.  idx3/w3 are [m][3] on the device.
+// Builds the device arrays from device-resident int32 index / fp64 weight k-tuples
+// (idx/w are [m][s->k] on the device) and counts distinct referenced source rows.
 void stencil_finalize(Stencil* s, const int32_t* d_idx3, const double* d_w3, cudaStream_t st);
 
 }  // namespace sg

@@ -156,7 +156,8 @@ class InterpolationWeights:
             nodes = np.ascontiguousarray(self.nodes, dtype=np.int64)
             w = np.ascontiguousarray(self.weights, dtype=np.float64)
             h = C.c_uint64(0)
-            N.call("sg_stencil_create", device, N.ptr(nodes), N.ptr(w), len(self), self.source_nnodes, N.ref(h))
+            N.call("sg_stencil_create_k", device, N.ptr(nodes), N.ptr(w), len(self), nodes.shape[1],
+                   self.source_nnodes, N.ref(h))
             self.stencil, self.stencil_device = N.Handle(h.value), device
         return self.stencil.handle
 
@@ -306,13 +307,57 @@ def export_weights(weights: InterpolationWeights, stream) -> None:
         stream.write(json.dumps(row) + "\n")
 
 
+def build_bilinear(source_fs: NodeColumns, target: Grid, target_dist: Distribution, ctx=None
+                   ) -> InterpolationWeights:
+    """Structured-bilinear weights (4 nodes per target) onto this partition's owned target
+    points — BASELINE configs[4].  The reference has no such method; the definition is in
+    csrc/bilinear.cu and oracle/oracle.py:bilinear_stencil (parity unpinned vs the
+    reference).  Zero communication; NotLocated if a bracketing node is outside the local
+    (owned + halo) mesh."""
+    mesh = source_fs.mesh
+    grid = mesh.grid
+    owned = np.flatnonzero(target_dist.part_of == mesh.partition_id).astype(np.int64)
+    ll = np.ascontiguousarray(target.lonlats()[owned])
+    m = len(owned)
+    nodes = np.zeros((m, 4), np.int64)
+    weights = np.zeros((m, 4))
+    status = np.zeros(m, np.uint8)
+    lat = np.ascontiguousarray(grid.latitudes, dtype=np.float64)
+    nl = np.ascontiguousarray(grid.nlons, dtype=np.int64)
+    ng = np.ascontiguousarray(mesh.node_global, dtype=np.int64)
+    h = C.c_uint64(0)
+    bad = C.c_int64(-1)
+    dev = current_device()
+    rc = N.lib.sg_bilinear_build(dev, grid.nrows, N.ptr(lat), N.ptr(nl), int(mesh.include_pole), N.ptr(ng),
+                                 mesh.nb_nodes, N.ptr(ll), m, N.ref(h), N.ptr(nodes), N.ptr(weights),
+                                 N.ptr(status), N.ref(bad))
+    if rc != N.SG_OK:
+        msg = N.last_error()
+        if bad.value >= 0:
+            t = int(owned[bad.value])
+            raise NotLocated(f"target point {t} not located in local source elements; increase the source mesh "
+                             "halo depth", target_global_index=t)
+        N.check(rc)
+    return InterpolationWeights(
+        target_global=owned, nodes=nodes, weights=weights, fallback=np.zeros(m, bool),
+        source_nnodes=mesh.nb_nodes, source_global=mesh.node_global, scale=np.ones(m),
+        stencil=N.Handle(h.value), stencil_device=dev,
+    )
+
+
 class Interpolation:
     """Atlas-style operator: ``Interpolation(source_fs, target, target_dist, ctx).execute(src,
-    tgt)`` builds the stencil once and applies it per call."""
+    tgt)`` builds the stencil once and applies it per call.  ``method``:
+    "finite-element" (the reference's gnomonic triangles) or "structured-bilinear"."""
 
     def __init__(self, source_fs: NodeColumns, target: Grid, target_dist: Distribution, ctx=None,
-                 allow_fallback: bool = False):
-        self.weights = build_remap(source_fs, target, target_dist, ctx, allow_fallback)
+                 allow_fallback: bool = False, method: str = "finite-element"):
+        if method == "finite-element":
+            self.weights = build_remap(source_fs, target, target_dist, ctx, allow_fallback)
+        elif method == "structured-bilinear":
+            self.weights = build_bilinear(source_fs, target, target_dist, ctx)
+        else:
+            raise ValueError(f"unknown interpolation method {method!r}")
 
     def execute(self, source_field: Field, target_field: Field) -> None:
         apply_remap(self.weights, source_field, target_field)

@@ -263,7 +263,8 @@ def test_distributed_remap_ranges_and_graph(gpu):
     fs = sg.NodeColumns(mesh, None)
     w = sg.build_remap(fs, T, td)
     b0, b1 = interior_block(w, mesh.nb_owned_nodes)
-    assert 0 < b0 < b1 < len(w)
+    assert 0 <= b0 < b1 <= len(w) and (b0 > 0 or b1 < len(w))
+    assert b1 - b0 > len(w) // 2
     assert (w.nodes[b0:b1] < mesh.nb_owned_nodes).all()
     h = np.random.default_rng(11).normal(size=(mesh.nb_nodes, 137))
     src, dst = DeviceArray(mesh.nb_nodes, 137, np.float64), DeviceArray(len(w), 137, np.float64)
@@ -282,4 +283,4 @@ def test_distributed_remap_ranges_and_graph(gpu):
         run2.step()
     run2.synchronize()
     assert np.array_equal(dst2.to_numpy().view(np.uint64), exp.view(np.uint64))
-    assert run2.launches_per_step == 3
+    assert run2.launches_per_step == 1 + (b0 > 0) + (b1 < len(w))

@@ -2,13 +2,17 @@
 # One GPU session: tests, bench (both arms), launch list, full ncu capture of the apply kernel.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
+free -g > gpurun_out/free.txt
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
+if [ "${REF:-1}" = "1" ]; then
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-timeout 300 python bench.py --steps 20 --warmup 5 --variant 2 --no-cpu-baseline > gpurun_out/bench_v2.json 2> gpurun_out/bench_v2.err
-timeout 300 python bench.py --steps 20 --warmup 5 --config cfg2 --no-cpu-baseline > gpurun_out/bench_cfg2.json 2> gpurun_out/bench_cfg2.err
+fi
+for extra in ${EXTRA:-}; do
+  timeout 900 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --config $extra > gpurun_out/bench_$extra.json 2> gpurun_out/bench_$extra.err
+done
 if [ "${NCU:-1}" = "1" ]; then
   timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
