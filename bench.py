@@ -325,7 +325,7 @@ def run_single(args):
         "config": {"workload": f"{source}->{target} {'structured-bilinear' if method == 'bilinear' else 'FE'} remap "
                                f"apply, {L} levels x {F} field(s), P=1",
                    "levels": L, "fields": F, "targets": m, "source_nodes": n, "distinct_sources": U,
-                   "parallelism": "single GPU", "l2": "inputs 7.3 GB > 126 MB L2 (no flush needed)",
+                   "parallelism": "single GPU", "l2": f"inputs {(n + m) * L * 8 * F / 1e9:.1f} GB > 126 MB L2 (no flush needed)",
                    "variant": args.variant},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(args.config), "algorithmic_bytes_per_launch": B,
