@@ -184,6 +184,12 @@ int32_t sg_comm_create(int32_t device, int32_t nranks, int32_t rank, const uint8
 int32_t sg_halo_exchange_nccl(uint64_t plan, uint64_t field, uint64_t comm,
                               uint64_t stream);
 
+/* Partition-invariant digest of owned rows [row0, row0+nrows) whose global ids are gids
+ * (functionspace.py:233-254): the wrapping u64 sum of splitmix64(gid*G + (level+1)*Lv ^ bits);
+ * the caller sums the partials over ranks (gather_to_root + broadcast, as the reference). */
+int32_t sg_field_checksum(uint64_t field, int64_t row0, int64_t nrows, const int64_t* gids,
+                          uint64_t* out_partial);
+
 /* CUDA IPC for the multi-process pull path (one process per GPU). */
 int32_t sg_ipc_handle(uint64_t field, uint8_t* out_handle, size_t n);
 int32_t sg_ipc_open(int32_t device, const uint8_t* handle, size_t n, uint64_t* out_ptr);

@@ -66,6 +66,7 @@ _SIGS = {
     "sg_nccl_unique_id": [vp, sz],
     "sg_comm_create": [i32, i32, i32, vp, sz, vp],
     "sg_halo_exchange_nccl": [u64, u64, u64, u64],
+    "sg_field_checksum": [u64, i64, i64, vp, vp],
     "sg_ipc_handle": [u64, vp, sz],
     "sg_ipc_open": [i32, vp, sz, vp],
     "sg_ipc_close": [i32, u64],

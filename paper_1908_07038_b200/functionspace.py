@@ -256,3 +256,101 @@ class StructuredColumns:
         f = create_field(name, (len(self.local_points), levels), kind)
         f.functionspace_tag = f"structured:{self.grid.name}:p{self.part}"
         return f
+
+
+# -- output / verification plumbing (functionspace.py:185-258) ---------------------------------
+_TAG_SCATTER = 104  # functionspace.py:27
+
+
+def _owned_device_rows(fs, f: Field):
+    """(DeviceArray, row0, nrows) holding the current owned values of ``f``: the field's own
+    mirror when it is current and the owned rows are contiguous, else a staging upload."""
+    rows = fs.owned_row_index()
+    contiguous = len(rows) == 0 or (rows[0] == 0 and rows[-1] == len(rows) - 1)
+    if f.device is not None and f.state in (MemoryState.SYNCED, MemoryState.DEVICE_DIRTY) and contiguous:
+        return f.device, 0, len(rows)
+    if f.state is MemoryState.DEVICE_DIRTY:
+        f.update_host()
+    host = np.ascontiguousarray(f.host[rows])
+    st = DeviceArray(max(len(rows), 1), f.levels, f.host.dtype, current_device())
+    if len(rows):
+        st.upload_rows(0, host)
+    return st, 0, len(rows)
+
+
+def checksum(fs, f: Field, ctx) -> int:
+    """Partition-invariant 64-bit digest of the owned values (functionspace.py:233-254),
+    computed by a device kernel (sg_field_checksum); ranks combine partials exactly like the
+    reference (gather_to_root + broadcast_from_root).  A DEVICE_DIRTY field is digested from
+    its (current) device mirror."""
+    dev, row0, n = _owned_device_rows(fs, f)
+    gids = np.ascontiguousarray(fs.owned_global, dtype=np.int64)
+    part = C.c_uint64(0)
+    N.call("sg_field_checksum", dev.handle, row0, n, N.ptr(gids), N.ref(part))
+    partial = np.uint64(part.value)
+    if ctx is None or ctx.nranks == 1:
+        return int(partial)
+    parts = ctx.gather_to_root(partial.tobytes())
+    digest = None
+    if ctx.rank == 0:
+        total = np.uint64(0)
+        with np.errstate(over="ignore"):
+            for blob in parts:
+                total += np.frombuffer(blob, dtype=np.uint64)[0]
+        digest = total.tobytes()
+    return int(np.frombuffer(ctx.broadcast_from_root(digest), dtype=np.uint64)[0])
+
+
+def format_checksum(digest: int) -> str:
+    return f"{digest:016x}"
+
+
+def _owned_values(fs, f: Field) -> np.ndarray:
+    if f.state is MemoryState.DEVICE_DIRTY:
+        rows = fs.owned_row_index()
+        if len(rows) and rows[0] == 0 and rows[-1] == len(rows) - 1:
+            return f.device.download_rows(0, len(rows))
+        f.update_host()
+    return fs.owned_rows(f)
+
+
+def gather_field(fs, f: Field, ctx) -> Optional[np.ndarray]:
+    """Owned values of every rank assembled on rank 0 in global order (functionspace.py:185-204);
+    device-dirty fields are read from HBM."""
+    owned = np.ascontiguousarray(_owned_values(fs, f))
+    gids = fs.owned_global
+    if ctx is None or ctx.nranks == 1:
+        out = np.zeros((fs.global_size, f.levels), dtype=f.host.dtype)
+        out[gids] = owned
+        return out
+    parts = ctx.gather_to_root(np.asarray(gids, np.int64).tobytes() + owned.tobytes())
+    if ctx.rank != 0:
+        return None
+    out = np.zeros((fs.global_size, f.levels), dtype=f.host.dtype)
+    row = 8 + f.host.dtype.itemsize * f.levels
+    for blob in parts:
+        n = len(blob) // row
+        g = np.frombuffer(blob[: 8 * n], dtype=np.int64)
+        out[g] = np.frombuffer(blob[8 * n:], dtype=f.host.dtype).reshape(n, f.levels)
+    return out
+
+
+def scatter_field(fs, f: Field, ctx, global_values: Optional[np.ndarray]) -> None:
+    """Rank 0's global array into every rank's owned rows (functionspace.py:207-224)."""
+    if f.state is MemoryState.DEVICE_DIRTY:
+        raise StaleHost(f"field {f.name!r} is device-dirty; update_host before scattering")
+    rows = fs.owned_row_index()
+    if ctx is None or ctx.nranks == 1:
+        f.host[rows] = global_values[fs.owned_global]
+    elif ctx.rank == 0:
+        gid_parts = ctx.gather_to_root(np.asarray(fs.owned_global, np.int64).tobytes())
+        for peer in range(1, ctx.nranks):
+            g = np.frombuffer(gid_parts[peer], dtype=np.int64)
+            ctx.send(peer, _TAG_SCATTER, np.ascontiguousarray(global_values[g]).tobytes())
+        f.host[rows] = global_values[fs.owned_global]
+    else:
+        ctx.gather_to_root(np.asarray(fs.owned_global, np.int64).tobytes())
+        data = np.frombuffer(ctx.receive(0, _TAG_SCATTER), dtype=f.host.dtype)
+        f.host[rows] = data.reshape(len(rows), f.levels)
+    if f.state is MemoryState.SYNCED:
+        f.state = MemoryState.HOST_DIRTY

@@ -186,7 +186,40 @@ def o1280_sample(n_random=5000):
          src_lat=S.latitudes, tgt_lat=T.latitudes)
 
 
+def checksums():
+    """checksum (functionspace.py:233-254) of fields scattered over P ranks: the digest is
+    partition-invariant; also the NodeColumns (mesh halo 1) variant."""
+    out = {}
+    for name, kind, levels in [("O32", R.Kind.REAL64, 3), ("F8", R.Kind.INT64, 2), ("O16", R.Kind.REAL32, 5)]:
+        g = R.grid_from_name(name)
+        rng = np.random.default_rng(77)
+        vals = rng.normal(size=(g.npts, levels))
+        if kind is R.Kind.INT64:
+            vals = rng.integers(-10**12, 10**12, size=(g.npts, levels))
+        vals = vals.astype(kind.dtype)
+        for P in (1, 2, 4):
+            def program(ctx):
+                dist = R.blocks_partition(g, ctx.nranks)
+                fs = R.StructuredColumns(g, dist, ctx.rank)
+                f = fs.create_field("x", levels, kind)
+                c = ctx if ctx.nranks > 1 else None
+                R.scatter_field(fs, f, c, vals if ctx.rank == 0 else None)
+                d1 = R.checksum(fs, f, c)
+                mesh = R.generate_mesh(g, dist, ctx.rank, halo=1, include_pole=False)
+                nfs = R.NodeColumns(mesh, c)
+                nf = nfs.create_field("y", levels, kind)
+                own = nfs.owned_row_index()
+                nf.host[own] = vals[mesh.node_global[own]]
+                d2 = R.checksum(nfs, nf, c)
+                return d1, d2
+            res = R.run_ranks(P, program)
+            out[f"{name}_p{P}"] = np.array([res[0][0], res[0][1]], dtype=np.uint64)
+        out[f"{name}_values"] = vals
+    save("checksum", **out)
+
+
 JOBS = {
+    "checksum": checksums,
     "latitudes": latitudes,
     "cfg1": lambda: serial_remap("O32", "O16", 10, "cfg1_O32_O16"),
     "f8": lambda: serial_remap("F8", "F4", 2, "serial_F8_F4"),
