@@ -45,11 +45,16 @@ class DistributedRemap:
         self.ev_fork, self.ev_halo = Event(dev), Event(dev)
         self.graph: Optional[Graph] = None
         self.multi = ctx is not None and getattr(ctx, "nranks", 1) > 1
-        self.comm = ctx.nccl_comm() if self.multi else None
+        # NCCL: stream-ordered exchange, overlappable and graph-capturable.  Otherwise
+        # (in-process ranks, CUDA-IPC pull) the exchange is host-synchronised: no overlap.
+        self.stream_ordered = self.multi and getattr(ctx, "transport", None) == "nccl"
+        self.comm = ctx.nccl_comm() if self.stream_ordered else None
 
     @property
     def launches_per_step(self) -> int:
         n = 0
+        if self.multi and not self.stream_ordered:
+            return 1 + int(sum(len(v) for v in self.plan.recv.values()) > 0)  # pull + apply
         if self.multi:
             n += int(sum(len(v) for v in self.plan.send.values()) > 0)  # pack
             n += int(sum(len(v) for v in self.plan.recv.values()) > 0)  # unpack
@@ -58,6 +63,11 @@ class DistributedRemap:
 
     def _enqueue(self) -> None:
         main = self.main.stream
+        if self.multi and not self.stream_ordered:
+            self.main.synchronize()
+            self.ctx.device_exchange(self.plan, self.src)
+            apply_remap_range(self.w, [self.src], [self.dst], 0, self.m, self.variant, main)
+            return
         if self.multi:
             self.ev_fork.record(main)
             self.halo.wait(self.ev_fork)
@@ -73,7 +83,9 @@ class DistributedRemap:
 
     def capture(self) -> None:
         """Record one step into a CUDA graph (call after one eager step so every buffer
-        exists)."""
+        exists).  Only stream-ordered steps can be captured."""
+        if self.multi and not self.stream_ordered:
+            raise RuntimeError("a host-synchronised exchange cannot be captured")
         self.graph = Graph(self.src.device, self.main.stream, self._enqueue)
 
     def step(self) -> None:
