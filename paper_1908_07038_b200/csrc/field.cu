@@ -43,7 +43,9 @@ int32_t sg_field_alloc(int32_t device, int64_t npts, int32_t levels, int32_t ite
   f->levels = levels;
   f->itemsize = itemsize;
   f->pitch = field_pitch_elems(levels, itemsize);
-  size_t bytes = (size_t)std::max<int64_t>(npts, 1) * f->pitch * itemsize;
+  // +16 B slack: the bulk-copy apply reads the 16-B aligned superset of a row, which can
+  // reach 8 B past the last dense row
+  size_t bytes = (size_t)std::max<int64_t>(npts, 1) * f->pitch * itemsize + 16;
   f->buf.alloc(device, bytes);
   SG_CUDA(cudaMemset(f->buf.ptr, 0, bytes));
   if (out_pitch_elems) *out_pitch_elems = f->pitch;
