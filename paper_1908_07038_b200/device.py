@@ -90,6 +90,84 @@ class DeviceArray(N.Handle):
         self.download(out)
         return out
 
+    # -- numpy-compatible access (the reference's Field.device was an ndarray, field.py:102) --
+    # Element access moves data over PCIe; it exists so code written against the reference's
+    # device mirror keeps working.  Kernels and torch/cupy use __cuda_array_interface__.
+    @property
+    def ndim(self) -> int:
+        return 2
+
+    @property
+    def size(self) -> int:
+        return self.shape[0] * self.shape[1]
+
+    def __len__(self) -> int:
+        return self.shape[0]
+
+    def __array__(self, dtype=None, copy=None):
+        a = self.to_numpy()
+        return a if dtype is None else a.astype(dtype)
+
+    def tobytes(self) -> bytes:
+        return self.to_numpy().tobytes()
+
+    def __getitem__(self, key):
+        return self.to_numpy()[key]
+
+    def __setitem__(self, key, value):
+        if isinstance(key, slice) and key == slice(None):
+            full = np.empty(self.shape, dtype=self.dtype)
+            full[...] = np.asarray(value)
+        else:
+            full = self.to_numpy()
+            full[key] = np.asarray(value)
+        self.upload(np.ascontiguousarray(full))
+
+    def _np(self, other):
+        return np.asarray(other) if isinstance(other, DeviceArray) else other
+
+    def __eq__(self, other):
+        return self.to_numpy() == self._np(other)
+
+    def __ne__(self, other):
+        return self.to_numpy() != self._np(other)
+
+    def __lt__(self, other):
+        return self.to_numpy() < self._np(other)
+
+    def __le__(self, other):
+        return self.to_numpy() <= self._np(other)
+
+    def __gt__(self, other):
+        return self.to_numpy() > self._np(other)
+
+    def __ge__(self, other):
+        return self.to_numpy() >= self._np(other)
+
+    def __add__(self, other):
+        return self.to_numpy() + self._np(other)
+
+    __radd__ = __add__
+
+    def __sub__(self, other):
+        return self.to_numpy() - self._np(other)
+
+    def __rsub__(self, other):
+        return self._np(other) - self.to_numpy()
+
+    def __mul__(self, other):
+        return self.to_numpy() * self._np(other)
+
+    __rmul__ = __mul__
+
+    def __truediv__(self, other):
+        return self.to_numpy() / self._np(other)
+
+    def __neg__(self):
+        return -self.to_numpy()
+
+    __hash__ = N.Handle.__hash__
+
 
 class PinnedArray:
     """Page-locked host array (cudaHostAlloc) for full-rate asynchronous copies."""

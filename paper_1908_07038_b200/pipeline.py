@@ -1,0 +1,54 @@
+"""The end-to-end distributed remap driver — ``run_remap_pipeline`` (cli.py:119-154 of the
+reference), on the device path.
+
+Per rank (one thread per rank, GPUs round-robin): blocks-decompose the source grid, build
+the rank's mesh with poles and a halo, slave the target grid to the decomposition, fill the
+owned source rows from an analytic spec, halo-exchange, build the stencils and apply them
+on the GPU, gather the target field on rank 0.  Returns (gathered target values, analytic
+target values, per-rank message counts during build + apply) like the reference.
+"""
+
+from __future__ import annotations
+
+from typing import List, Optional
+
+import numpy as np
+
+from .analytic import FieldSpec
+from .functionspace import NodeColumns, StructuredColumns, gather_field
+from .grid import grid_from_name
+from .interp import apply_remap, build_bilinear, build_remap
+from .mesh import generate_mesh
+from .parallel import run_ranks
+from .partition import blocks_partition, matching_partition
+
+
+def run_remap_pipeline(source_name: str, target_name: str, nparts: int, field_spec: str, halo: int = 2,
+                       method: str = "finite-element", devices: Optional[List[int]] = None):
+    source, target = grid_from_name(source_name), grid_from_name(target_name)
+    spec = FieldSpec(field_spec)
+
+    def rank_program(ctx):
+        comm = ctx if ctx.nranks > 1 else None
+        dist = blocks_partition(source, ctx.nranks)
+        mesh = generate_mesh(source, dist, ctx.rank, halo=halo, include_pole=True)
+        fs = NodeColumns(mesh, comm)
+        tdist = matching_partition(target, source, dist)
+        src = fs.create_field("src")
+        rows = fs.owned_row_index()
+        src.host[rows, 0] = spec(mesh.node_xyz[rows])
+        fs.halo_exchange(src, comm)
+        before = ctx.messages_sent
+        if method == "structured-bilinear":
+            weights = build_bilinear(fs, target, tdist, ctx)
+        else:
+            weights = build_remap(fs, target, tdist, ctx)
+        tfs = StructuredColumns(target, tdist, ctx.rank)
+        dst = tfs.create_field("dst")
+        apply_remap(weights, src, dst)
+        sent = ctx.messages_sent - before
+        return gather_field(tfs, dst, comm), sent
+
+    out = run_ranks(nparts, rank_program, devices)
+    gathered = out[0][0][:, 0]
+    return gathered, spec(target.xyz()), [r[1] for r in out]
