@@ -178,6 +178,14 @@ int32_t sg_halo_unpack(uint64_t plan, uint64_t field, const void* dev_recvbuf,
 int32_t sg_halo_pull(uint64_t plan, uint64_t field, const uint64_t* peer_ptrs,
                      const int64_t* peer_pitch_elems, uint64_t stream);
 
+/* Fused exchange + apply: applies targets [t0, t1) reading every ghost stencil row straight
+ * from its owner's field (peer_ptrs/peer_pitch_elems by plan peer slot) — the halo exchange
+ * of functionspace.py:107-118 and the apply of interp.py:206-228 in one kernel, no ghost
+ * copy.  Caller guarantees the owners' rows are final (barrier) while it runs. */
+int32_t sg_remap_apply_fused(uint64_t stencil, uint64_t plan, uint64_t src_field,
+                             uint64_t dst_field, int64_t t0, int64_t t1,
+                             const uint64_t* peer_ptrs, const int64_t* peer_pitch_elems,
+                             uint64_t stream);
 int32_t sg_nccl_unique_id(uint8_t* out_id, size_t n);
 int32_t sg_comm_create(int32_t device, int32_t nranks, int32_t rank, const uint8_t* id,
                        size_t n, uint64_t* out_comm);

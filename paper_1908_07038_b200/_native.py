@@ -63,6 +63,7 @@ _SIGS = {
     "sg_halo_pack": [u64, u64, vp, u64],
     "sg_halo_unpack": [u64, u64, vp, u64],
     "sg_halo_pull": [u64, u64, vp, vp, u64],
+    "sg_remap_apply_fused": [u64, u64, u64, u64, i64, i64, vp, vp, u64],
     "sg_nccl_unique_id": [vp, sz],
     "sg_comm_create": [i32, i32, i32, vp, sz, vp],
     "sg_halo_exchange_nccl": [u64, u64, u64, u64],
@@ -101,6 +102,19 @@ def _load() -> C.CDLL:
 
 
 lib = _load()
+_shutting_down = False
+
+
+def _mark_shutdown() -> None:
+    # registered after the CUDA runtime's own exit handlers, so it runs first: from here on
+    # handles are leaked to the OS instead of released into a runtime being torn down
+    global _shutting_down
+    _shutting_down = True
+
+
+import atexit  # noqa: E402
+
+atexit.register(_mark_shutdown)
 _PREFIX = re.compile(r"^([A-Za-z]+): (.*)$", re.S)
 
 
@@ -182,7 +196,7 @@ class Handle:
 
     def close(self) -> None:
         h, self.handle = self.handle, 0
-        if h:
+        if h and not _shutting_down:
             lib.sg_release(h)
 
     def __del__(self):

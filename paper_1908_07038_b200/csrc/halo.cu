@@ -22,23 +22,10 @@
 #include <type_traits>
 #include <vector>
 
-#include "cuda_util.cuh"
+#include "plan.cuh"
 
 namespace sg {
 namespace {
-
-constexpr int kMaxPeers = 64;
-
-struct Plan : Object {
-  Plan() : Object(ObjKind::Plan) {}
-  int device = 0;
-  int64_t nnodes = 0;
-  std::vector<int32_t> peers;
-  std::vector<int64_t> send_off, recv_off;  // per peer, npeers+1
-  DevBuf send_rows, recv_rows, recv_remote;  // int32
-  DevBuf recv_peer;                          // int32 plan-peer slot of every ghost row
-  DevBuf sendbuf, recvbuf;                   // NCCL staging (lazily sized)
-};
 
 // Rows are moved as words of the field's item size (8 B for real64/int64, 4 B otherwise):
 // W words per row, pitches in words.  Dense rows are item-aligned only, so no wider moves.
@@ -208,6 +195,19 @@ int32_t sg_halo_plan_create(int32_t device, int64_t nnodes, int32_t npeers, cons
   upload_i32(p->recv_rows, device, rrows);
   upload_i32(p->recv_remote, device, rremote);
   upload_i32(p->recv_peer, device, rslot);
+  // dense ghost map over [ghost_lo, nnodes): owner slot and owner row of every received row
+  if (!rrows.empty()) {
+    p->ghost_lo = *std::min_element(rrows.begin(), rrows.end());
+    std::vector<int32_t> gs((size_t)(nnodes - p->ghost_lo), -1), gr((size_t)(nnodes - p->ghost_lo), -1);
+    for (size_t k = 0; k < rrows.size(); ++k) {
+      gs[rrows[k] - p->ghost_lo] = rslot[k];
+      gr[rrows[k] - p->ghost_lo] = rremote[k];
+    }
+    upload_i32(p->ghost_slot, device, gs);
+    upload_i32(p->ghost_row, device, gr);
+  } else {
+    p->ghost_lo = nnodes;
+  }
   *out_plan = registry_put(p.release());
   SG_API_END
 }

@@ -179,12 +179,14 @@ class PinnedArray:
         N.call("sg_host_alloc", nbytes, N.ref(p))
         self._ptr = p.value
         buf = (C.c_char * max(nbytes, 1)).from_address(self._ptr)
+        buf._sg_owner = self  # any view of .array keeps the pinned allocation alive
         self.array = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
 
     def free(self) -> None:
         if self._ptr:
             self.array = None
-            N.call("sg_host_free", self._ptr)
+            if not N._shutting_down:
+                N.call("sg_host_free", self._ptr)
             self._ptr = 0
 
     def __del__(self):

@@ -15,7 +15,7 @@ from typing import Optional
 import numpy as np
 
 from .device import DeviceArray, Event, Graph, Stream
-from .interp import APPLY_DEFAULT, InterpolationWeights, apply_remap_range
+from .interp import APPLY_DEFAULT, InterpolationWeights, apply_remap_fused, apply_remap_range
 
 
 def interior_block(weights: InterpolationWeights, n_owned: int):
@@ -31,7 +31,10 @@ def interior_block(weights: InterpolationWeights, n_owned: int):
 
 class DistributedRemap:
     def __init__(self, fs, weights: InterpolationWeights, ctx, src: DeviceArray, dst: DeviceArray,
-                 variant: int = APPLY_DEFAULT, overlap: bool = True):
+                 variant: int = APPLY_DEFAULT, overlap: bool = True, fused: bool = False):
+        """fused: skip the ghost copy — boundary targets read ghost rows straight from the
+        owners' fields (sg_remap_apply_fused; peer memory: in-process ranks or CUDA IPC).
+        The source field's ghost rows are then left untouched."""
         self.fs, self.w, self.ctx = fs, weights, ctx
         self.src, self.dst = src, dst
         self.variant = variant
@@ -48,11 +51,17 @@ class DistributedRemap:
         # NCCL: stream-ordered exchange, overlappable and graph-capturable.  Otherwise
         # (in-process ranks, CUDA-IPC pull) the exchange is host-synchronised: no overlap.
         self.stream_ordered = self.multi and getattr(ctx, "transport", None) == "nccl"
+        self.fused = bool(fused) and self.multi
+        if self.fused:
+            self.stream_ordered = False
         self.comm = ctx.nccl_comm() if self.stream_ordered else None
+        self.peer_info = ctx.peer_fields(src) if self.fused else None
 
     @property
     def launches_per_step(self) -> int:
         n = 0
+        if self.fused:
+            return sum(1 for a, b in ((self.b0, self.b1), (0, self.b0), (self.b1, self.m)) if b > a)
         if self.multi and not self.stream_ordered:
             return 1 + int(sum(len(v) for v in self.plan.recv.values()) > 0)  # pull + apply
         if self.multi:
@@ -63,6 +72,17 @@ class DistributedRemap:
 
     def _enqueue(self) -> None:
         main = self.main.stream
+        if self.fused:
+            self.main.synchronize()
+            self.ctx.barrier()  # every owner's rows are final
+            if self.b1 > self.b0:
+                apply_remap_range(self.w, [self.src], [self.dst], self.b0, self.b1, self.variant, main)
+            for a, b in ((0, self.b0), (self.b1, self.m)):
+                if b > a:
+                    apply_remap_fused(self.w, self.plan, self.src, self.dst, a, b, self.peer_info, main)
+            self.main.synchronize()
+            self.ctx.barrier()  # nobody overwrites owned rows while a peer still reads them
+            return
         if self.multi and not self.stream_ordered:
             self.main.synchronize()
             self.ctx.device_exchange(self.plan, self.src)

@@ -247,6 +247,19 @@ def apply_remap_range(weights: InterpolationWeights, sources: Sequence[DeviceArr
     N.call("sg_remap_apply_range", sh, N.ptr(s), N.ptr(t), len(s), t0, t1, variant, stream)
 
 
+def apply_remap_fused(weights: InterpolationWeights, plan, source: DeviceArray, target: DeviceArray, t0: int,
+                      t1: int, peer_info, stream: int = 0) -> None:
+    """Targets [t0, t1) with ghost stencil rows read straight from their owners' fields
+    (sg_remap_apply_fused): halo exchange + apply in one kernel.  peer_info[r] = (ptr,
+    pitch, device) of rank r's source field (ctx.peer_fields); owners' rows must be final."""
+    dev = source.device
+    peers = plan.peers
+    ptrs = np.array([peer_info[p][0] for p in peers] or [0], np.uint64)
+    pitch = np.array([peer_info[p][1] for p in peers] or [0], np.int64)
+    N.call("sg_remap_apply_fused", weights.device_stencil(dev), plan.native(dev), source.handle, target.handle,
+           t0, t1, N.ptr(ptrs), N.ptr(pitch), stream)
+
+
 def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], host_dst: Sequence[np.ndarray],
                  dev_src: Sequence[DeviceArray], dev_dst: Sequence[DeviceArray], nchunks: int = 0,
                  variant: int = APPLY_DEFAULT) -> int:

@@ -165,10 +165,20 @@ class RankContext:
             w.board.pop((key, self.rank), None)
         return out
 
-    def device_exchange(self, plan, dev_array) -> None:
+    def peer_fields(self, dev_array) -> list:
+        """(ptr, pitch, device) of every rank's instance of a field (collective; cached per
+        field): ranks of one process address each other's HBM directly."""
+        cache = self.__dict__.setdefault("_peer_cache", {})
+        got = cache.get(dev_array.handle)
+        if got is None:
+            got = cache[dev_array.handle] = self.share((dev_array.ptr, dev_array.pitch, dev_array.device))
+        return got
+
+    def device_exchange(self, plan, dev_array, stream: int = 0) -> None:
         """Fused device halo exchange over peer memory: one pull kernel per rank."""
-        D.synchronize(dev_array.device)
-        ptrs = self.share((dev_array.ptr, dev_array.pitch, dev_array.device))
+        ptrs = self.peer_fields(dev_array)
+        D.synchronize(dev_array.device, stream)
+        self.barrier()
         plan.pull(dev_array, ptrs)
         D.synchronize(dev_array.device)
         self.barrier()
@@ -338,7 +348,7 @@ class DistContext:
             self._comm = N.Handle(h.value)
         return self._comm.handle
 
-    def _peer_fields(self, dev_array) -> list:
+    def peer_fields(self, dev_array) -> list:
         """(ptr, pitch, device) of every rank's copy of this field, via CUDA IPC (cached)."""
         import ctypes as C
 
@@ -366,7 +376,7 @@ class DistContext:
             plan.exchange_nccl(dev_array, self.nccl_comm(), stream)
             D.synchronize(dev_array.device, stream)
             return
-        peers = self._peer_fields(dev_array)
+        peers = self.peer_fields(dev_array)
         D.synchronize(dev_array.device, stream)
         self.barrier()  # every owner's rows are final
         plan.pull(dev_array, peers)

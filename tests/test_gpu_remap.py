@@ -284,3 +284,40 @@ def test_distributed_remap_ranges_and_graph(gpu):
     run2.synchronize()
     assert np.array_equal(dst2.to_numpy().view(np.uint64), exp.view(np.uint64))
     assert run2.launches_per_step == 1 + (b0 > 0) + (b1 < len(w))
+
+
+def test_empty_and_tiny_cases(gpu):
+    """Edge cases: a rank that owns no target, zero-point fields, one-level fields."""
+    sg = gpu
+    from paper_1908_07038_b200.device import DeviceArray
+
+    S, T = sg.grid_from_name("O16"), sg.grid_from_name("F2")  # 32 targets over 16 ranks' bands
+    dist = sg.blocks_partition(S, 16)
+    td = sg.matching_partition(T, S, dist)
+    empty_ranks = [r for r in range(16) if not (td.part_of == r).any()]
+    assert empty_ranks
+    r = empty_ranks[0]
+    mesh = sg.generate_mesh(S, dist, r, halo=1, include_pole=True)
+    fs = sg.NodeColumns(mesh, None)
+    w = sg.build_remap(fs, T, td)
+    assert len(w) == 0 and w.nodes.shape == (0, 3)
+    f = fs.create_field("s", 5)
+    tf = sg.StructuredColumns(T, td, r).create_field("t", 5)
+    sg.apply_remap(w, f, tf)  # host path, nothing to do
+    f.allocate_device()
+    tf.allocate_device()
+    sg.apply_remap(w, f, tf)  # device path
+    assert tf.state is sg.MemoryState.DEVICE_DIRTY
+    z = sg.create_field("z", (0, 4)).allocate_device()
+    z.update_host()
+    assert z.device.to_numpy().shape == (0, 4)
+    # one level, odd pitch path
+    S1, T1 = sg.grid_from_name("O32"), sg.grid_from_name("O16")
+    d1 = sg.blocks_partition(S1, 1)
+    m1 = sg.generate_mesh(S1, d1, 0, halo=0, include_pole=True)
+    w1 = sg.build_remap(sg.NodeColumns(m1, None), T1, sg.matching_partition(T1, S1, d1))
+    h = np.random.default_rng(1).normal(size=(m1.nb_nodes, 1))
+    src, dst = DeviceArray(m1.nb_nodes, 1, np.float64), DeviceArray(len(w1), 1, np.float64)
+    src.upload(h)
+    sg.apply_remap_device(w1, [src], [dst])
+    assert np.array_equal(dst.to_numpy().view(np.uint64), O.apply_remap(w1.nodes, w1.weights, h).view(np.uint64))
