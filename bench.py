@@ -375,7 +375,7 @@ def run_multi(args):
     hdst = PinnedArray((m, L))
     f = sg.Field(name="src", shape=(n, L), kind=sg.Kind.REAL64, host=hsrc.array).allocate_device()
     tf = sg.Field(name="dst", shape=(m, L), kind=sg.Kind.REAL64, host=hdst.array).allocate_device()
-    run = DistributedRemap(fs, w, ctx, f.device, tf.device, variant=args.variant)
+    run = DistributedRemap(fs, w, ctx, f.device, tf.device, variant=args.variant, fused=args.fused)
     log(f"rank {rank}: setup {time.time() - t0:.1f}s, {n} nodes ({n_owned} owned), {m} targets, "
         f"interior block {run.b1 - run.b0}, {sum(len(v) for v in fs.exchange_plan.recv.values())} ghosts")
     for _ in range(args.warmup):
@@ -458,7 +458,8 @@ def run_multi(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
             "config": {"workload": f"{source}->{target} FE remap, {L} levels, blocks_partition P={world}, halo 2; "
-                                   f"step = halo exchange ({args.transport}) + apply (interior block overlapped when stream-ordered)",
+                                   (f"step = fused exchange+apply over peer memory ({args.transport} fences)" if args.fused else
+                                    f"step = halo exchange ({args.transport}) + apply (interior block overlapped when stream-ordered)"),
                        "levels": L, "parallelism": f"domain decomposition x{world}", "l2": "inputs > L2",
                        "cuda_graph": graphed},
             "halo": {"bytes_per_exchange": hsum, "ms": hmax, "GB_per_s": hsum / (hmax * 1e-3) / 1e9},
@@ -481,6 +482,9 @@ def main():
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     ap.add_argument("--variant", type=int, default=0, help="apply kernel: 0 default, 1 warp LDG, 2 TMA bulk")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fused", action="store_true",
+                    help="N>1: no ghost copy — boundary targets read ghost rows from the owners' HBM "
+                         "(CUDA IPC / NVLink) inside the apply kernel, fenced by NCCL barriers")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
                     help="N>1 halo exchange: NCCL send/recv (one GPU per rank) or CUDA-IPC pull")
     args = ap.parse_args()

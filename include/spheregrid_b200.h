@@ -144,13 +144,17 @@ int32_t sg_remap_apply_range(uint64_t stencil, const uint64_t* src_fields,
 /* apply_remap with HOST buffers (the reference's call shape, interp.py:206-228): host
  * source rows -> device, apply, device -> host target rows, as an nchunks-deep pipeline
  * on three streams (h2d of source-row chunk c, apply of the targets whose stencils lie in
- * chunks <= c, d2h of those target rows).  Only source rows the stencil references are
- * copied (*out_rows_copied).  host_src/host_dst: dense (npts, levels) C-order fp64, ideally
+ * chunks <= c, d2h of those target rows).  Unreferenced gaps of < 64 rows are copied
+ * through (*out_rows_copied).  host_src/host_dst: dense (npts, levels) C-order fp64, ideally
  * pinned (sg_host_alloc).  Synchronous: returns when host_dst holds the result. */
 int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields,
                               const uint64_t* dst_fields, int32_t nfields,
                               const uint64_t* host_src, const uint64_t* host_dst,
-                              int32_t nchunks, int32_t variant, int64_t* out_rows_copied);
+                              int32_t nchunks, int32_t variant, int32_t flags,
+                              int64_t* out_rows_copied);
+/* flags bit 0 (compact): pack exactly the referenced source rows on the host (library thread
+ * pool, pinned 3-slot staging ring) and apply from a compact device copy with a renumbered
+ * stencil — PCIe carries U rows instead of every row (77 % at cfg3/cfg2). */
 
 /* ---- halo exchange (functionspace.py:58-118) ---------------------------------------------
  * sg_halo_plan_create <- HaloExchangePlan (functionspace.py:47-55): per peer (ascending),
@@ -191,6 +195,9 @@ int32_t sg_comm_create(int32_t device, int32_t nranks, int32_t rank, const uint8
                        size_t n, uint64_t* out_comm);
 int32_t sg_halo_exchange_nccl(uint64_t plan, uint64_t field, uint64_t comm,
                               uint64_t stream);
+/* Stream-ordered barrier (ncclAllReduce of one word on `stream`): fences the fused
+ * exchange+apply's peer reads without a host round trip; graph-capturable. */
+int32_t sg_comm_barrier(uint64_t comm, uint64_t stream);
 
 /* Partition-invariant digest of owned rows [row0, row0+nrows) whose global ids are gids
  * (functionspace.py:233-254): the wrapping u64 sum of splitmix64(gid*G + (level+1)*Lv ^ bits);

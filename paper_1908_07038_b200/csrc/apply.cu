@@ -24,6 +24,10 @@
 #include <mutex>
 #include <vector>
 
+#include <cstring>
+#include <memory>
+
+#include "host_pool.h"
 #include "stencil.cuh"
 
 namespace sg {
@@ -476,6 +480,10 @@ ApplyArgs make_args(const Stencil* s, const FieldPairs& p, int f0, int64_t t0, i
 }
 
 // ---- host pipeline plan (per stencil, built on first use) -----------------------------------
+struct CompactRun {
+  int64_t src, len, dst;  // source row, rows, compact row
+};
+
 struct HostPlan {
   int nchunks = 0;
   std::vector<int64_t> t_end;                                  // chunk c: targets [t_end[c-1], t_end[c])
@@ -483,7 +491,61 @@ struct HostPlan {
   int64_t rows_copied = 0;
   cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_cmp;
+  // compact mode: only referenced rows cross PCIe, packed on the host into pinned staging
+  bool compact_ready = false;
+  int64_t ncompact = 0;                           // U
+  std::vector<std::vector<CompactRun>> cruns;     // chunk c: exact referenced runs
+  std::vector<int64_t> cb;                        // chunk c: compact rows [cb[c], cb[c+1])
+  DevBuf cidx;                                    // int4[m]: stencil in compact row numbering
+  std::vector<std::unique_ptr<DevBuf>> csrc;      // per field: U compact rows on the device
+  static constexpr int kRing = 3;
+  std::vector<void*> ring;                        // per (field, slot): pinned staging
+  size_t ring_bytes = 0;
+  int ring_fields = 0;
+  ~HostPlan() {
+    for (void* p : ring)
+      if (p) cudaFreeHost(p);
+  }
 };
+
+HostPool& host_pool() {
+  static HostPool pool(std::max(1u, std::min(32u, std::thread::hardware_concurrency())) - 1);
+  return pool;
+}
+
+void build_compact(Stencil* s, HostPlan* hp, const std::vector<int4>& idx, const std::vector<unsigned char>& mark) {
+  const int64_t n = s->source_nnodes, m = s->m;
+  std::vector<int32_t> cpos((size_t)n, -1);
+  int64_t u = 0;
+  for (int64_t i = 0; i < n; ++i)
+    if (mark[i]) cpos[i] = (int32_t)u++;
+  hp->ncompact = u;
+  hp->cruns.assign(hp->nchunks, {});
+  hp->cb.assign(hp->nchunks + 1, 0);
+  int64_t rprev = 0;
+  for (int c = 0; c < hp->nchunks; ++c) {
+    const int64_t rb = (c + 1 == hp->nchunks) ? n : n * (c + 1) / hp->nchunks;
+    int64_t i = rprev;
+    while (i < rb) {
+      while (i < rb && !mark[i]) ++i;
+      if (i >= rb) break;
+      int64_t j = i;
+      while (j < rb && mark[j]) ++j;
+      hp->cruns[c].push_back(CompactRun{i, j - i, cpos[i]});
+      i = j;
+    }
+    hp->cb[c + 1] = hp->cruns[c].empty() ? hp->cb[c] : hp->cruns[c].back().dst + hp->cruns[c].back().len;
+    rprev = rb;
+  }
+  std::vector<int4> ci((size_t)m);
+  for (int64_t t = 0; t < m; ++t) {
+    const int4 id = idx[t];
+    ci[t] = make_int4(cpos[id.x], cpos[id.y], cpos[id.z], s->k == 4 ? cpos[id.w] : 0);
+  }
+  hp->cidx.alloc(s->device, std::max<size_t>(ci.size(), 1) * sizeof(int4));
+  if (m) SG_CUDA(cudaMemcpy(hp->cidx.ptr, ci.data(), ci.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  hp->compact_ready = true;
+}
 
 std::mutex g_plan_mu;
 
@@ -539,6 +601,7 @@ HostPlan* host_plan(Stencil* s, int nchunks) {
     tprev = te;
     rprev = rb;
   }
+  build_compact(s, hp, idx, mark);
   SG_CUDA(cudaStreamCreateWithFlags(&hp->s_in, cudaStreamNonBlocking));
   SG_CUDA(cudaStreamCreateWithFlags(&hp->s_cmp, cudaStreamNonBlocking));
   SG_CUDA(cudaStreamCreateWithFlags(&hp->s_out, cudaStreamNonBlocking));
@@ -673,7 +736,7 @@ int32_t sg_remap_apply_range(uint64_t stencil, const uint64_t* src_fields, const
 
 int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, const uint64_t* dst_fields,
                               int32_t nfields, const uint64_t* host_src, const uint64_t* host_dst, int32_t nchunks,
-                              int32_t variant, int64_t* out_rows_copied) {
+                              int32_t variant, int32_t flags, int64_t* out_rows_copied) {
   SG_API_BEGIN
   Stencil* s = get<Stencil>(stencil, ObjKind::Stencil);
   FieldPairs p = check_pairs(s, src_fields, dst_fields, nfields);
@@ -686,19 +749,69 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
   DeviceScope ds(s->device);
   HostPlan* hp = host_plan(s, nchunks);
   const size_t row = (size_t)p.levels * 8;
-  int64_t tprev = 0;
+  const bool compact = (flags & 1) != 0;
+  if (compact) {
+    // device compact sources and the pinned staging ring (sized for the largest chunk)
+    size_t maxc = 0;
+    for (int c = 0; c < nchunks; ++c) maxc = std::max<size_t>(maxc, (size_t)(hp->cb[c + 1] - hp->cb[c]));
+    const size_t need = std::max<size_t>(maxc * row, 16);
+    if (hp->ring_bytes < need || hp->ring_fields < nfields) {
+      for (void* q : hp->ring)
+        if (q) cudaFreeHost(q);
+      hp->ring.assign((size_t)nfields * HostPlan::kRing, nullptr);
+      for (auto& q : hp->ring) SG_CUDA(cudaHostAlloc(&q, need, cudaHostAllocPortable));
+      hp->ring_bytes = need;
+      hp->ring_fields = nfields;
+    }
+    while ((int)hp->csrc.size() < nfields) hp->csrc.emplace_back(new DevBuf());
+    for (int f = 0; f < nfields; ++f)
+      if (hp->csrc[f]->bytes < std::max<size_t>(hp->ncompact * row, 16))
+        hp->csrc[f]->alloc(s->device, std::max<size_t>(hp->ncompact * row, 16));
+  }
+  int64_t tprev = 0, copied = 0;
   for (int c = 0; c < nchunks; ++c) {
-    for (int f = 0; f < nfields; ++f) {
-      char* dev = p.src[f]->buf.as<char>();
-      const char* host = reinterpret_cast<const char*>(host_src[f]);
-      for (auto& r : hp->runs[c])
-        SG_CUDA(cudaMemcpyAsync(dev + r.first * row, host + r.first * row, (size_t)(r.second - r.first) * row,
-                                cudaMemcpyHostToDevice, hp->s_in));
+    if (compact) {
+      const int slot = c % HostPlan::kRing;
+      if (c >= HostPlan::kRing) SG_CUDA(cudaEventSynchronize(hp->ev_in[c - HostPlan::kRing]));  // slot free
+      const auto& runs = hp->cruns[c];
+      const int64_t base = hp->cb[c], nrows = hp->cb[c + 1] - hp->cb[c];
+      const int nr = (int)runs.size();
+      const int grain = std::max(1, nr / (host_pool().size() * 4));
+      for (int f = 0; f < nfields; ++f) {
+        char* stage = static_cast<char*>(hp->ring[(size_t)f * HostPlan::kRing + slot]);
+        const char* host = reinterpret_cast<const char*>(host_src[f]);
+        host_pool().parallel_for((nr + grain - 1) / grain, [&](int b) {
+          for (int k = b * grain; k < std::min(nr, (b + 1) * grain); ++k)
+            std::memcpy(stage + (runs[k].dst - base) * row, host + runs[k].src * row, (size_t)runs[k].len * row);
+        });
+        if (nrows)
+          SG_CUDA(cudaMemcpyAsync(hp->csrc[f]->as<char>() + base * row, stage, (size_t)nrows * row,
+                                  cudaMemcpyHostToDevice, hp->s_in));
+      }
+      copied += nrows;
+    } else {
+      for (int f = 0; f < nfields; ++f) {
+        char* dev = p.src[f]->buf.as<char>();
+        const char* host = reinterpret_cast<const char*>(host_src[f]);
+        for (auto& r : hp->runs[c])
+          SG_CUDA(cudaMemcpyAsync(dev + r.first * row, host + r.first * row, (size_t)(r.second - r.first) * row,
+                                  cudaMemcpyHostToDevice, hp->s_in));
+      }
     }
     SG_CUDA(cudaEventRecord(hp->ev_in[c], hp->s_in));
     SG_CUDA(cudaStreamWaitEvent(hp->s_cmp, hp->ev_in[c], 0));
     const int64_t te = hp->t_end[c];
-    for (int f0 = 0; f0 < nfields; f0 += kMaxFields) launch_apply(make_args(s, p, f0, tprev, te), variant, hp->s_cmp);
+    for (int f0 = 0; f0 < nfields; f0 += kMaxFields) {
+      ApplyArgs a = make_args(s, p, f0, tprev, te);
+      if (compact) {
+        a.idx = hp->cidx.as<int4>();
+        for (int f = 0; f < a.nfields; ++f) {
+          a.src[f] = hp->csrc[f0 + f]->as<double>();
+          a.src_pitch[f] = p.levels;
+        }
+      }
+      launch_apply(a, variant, hp->s_cmp);
+    }
     SG_CUDA(cudaEventRecord(hp->ev_cmp[c], hp->s_cmp));
     SG_CUDA(cudaStreamWaitEvent(hp->s_out, hp->ev_cmp[c], 0));
     if (te > tprev)
@@ -711,7 +824,7 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
   SG_CUDA(cudaStreamSynchronize(hp->s_out));
   SG_CUDA(cudaStreamSynchronize(hp->s_cmp));
   SG_CUDA(cudaStreamSynchronize(hp->s_in));
-  if (out_rows_copied) *out_rows_copied = hp->rows_copied;
+  if (out_rows_copied) *out_rows_copied = compact ? copied : hp->rows_copied;
   SG_API_END
 }
 

@@ -89,6 +89,7 @@ struct Nccl {
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 std::mutex g_nccl_mu;
@@ -110,6 +111,7 @@ Nccl& nccl() {
     SG_NCCL_SYM(GroupEnd, "ncclGroupEnd");
     SG_NCCL_SYM(Send, "ncclSend");
     SG_NCCL_SYM(Recv, "ncclRecv");
+    SG_NCCL_SYM(AllReduce, "ncclAllReduce");
     SG_NCCL_SYM(GetErrorString, "ncclGetErrorString");
 #undef SG_NCCL_SYM
     g_nccl.lib = h;
@@ -128,6 +130,7 @@ struct Comm : Object {
   Comm() : Object(ObjKind::Comm) {}
   int device = 0, nranks = 0, rank = 0;
   ncclComm_t comm = nullptr;
+  DevBuf token;  // 4-B device word for the stream-ordered barrier
   ~Comm() override {
     if (comm) nccl().CommDestroy(comm);
   }
@@ -308,6 +311,22 @@ int32_t sg_comm_create(int32_t device, int32_t nranks, int32_t rank, const uint8
   c->rank = rank;
   SG_NCCL(nccl().CommInitRank(&c->comm, nranks, uid, rank));
   *out_comm = registry_put(c.release());
+  SG_API_END
+}
+
+// Stream-ordered barrier: an ncclAllReduce of one word on `stream`.  Work enqueued after it
+// on any rank starts only once every rank's earlier work on its stream has completed — the
+// fence the fused exchange+apply needs around peer reads, without a host round trip, and
+// capturable into a CUDA graph.
+int32_t sg_comm_barrier(uint64_t comm, uint64_t stream) {
+  SG_API_BEGIN
+  Comm* c = get<Comm>(comm, ObjKind::Comm);
+  DeviceScope ds(c->device);
+  if (!c->token.ptr) {
+    c->token.alloc(c->device, 16);
+    SG_CUDA(cudaMemset(c->token.ptr, 0, 16));
+  }
+  SG_NCCL(nccl().AllReduce(c->token.ptr, c->token.ptr, 1, /*ncclInt32*/ 2, /*ncclSum*/ 0, c->comm, as_stream(stream)));
   SG_API_END
 }
 

@@ -14,6 +14,7 @@ from typing import Optional
 
 import numpy as np
 
+from . import _native as N
 from .device import DeviceArray, Event, Graph, Stream
 from .interp import APPLY_DEFAULT, InterpolationWeights, apply_remap_fused, apply_remap_range
 
@@ -52,8 +53,9 @@ class DistributedRemap:
         # (in-process ranks, CUDA-IPC pull) the exchange is host-synchronised: no overlap.
         self.stream_ordered = self.multi and getattr(ctx, "transport", None) == "nccl"
         self.fused = bool(fused) and self.multi
-        if self.fused:
-            self.stream_ordered = False
+        # fused + NCCL: peer pointers from CUDA IPC (NVLink reads), fenced by stream-ordered
+        # NCCL barriers -> no host round trip and graph-capturable; fused without NCCL
+        # (in-process ranks, IPC transport) fences with host barriers
         self.comm = ctx.nccl_comm() if self.stream_ordered else None
         self.peer_info = ctx.peer_fields(src) if self.fused else None
 
@@ -73,15 +75,22 @@ class DistributedRemap:
     def _enqueue(self) -> None:
         main = self.main.stream
         if self.fused:
-            self.main.synchronize()
-            self.ctx.barrier()  # every owner's rows are final
-            if self.b1 > self.b0:
+            def fence():
+                if self.stream_ordered:
+                    N.call("sg_comm_barrier", self.comm, main)
+                else:
+                    self.main.synchronize()
+                    self.ctx.barrier()
+
+            if self.b1 > self.b0 and self.stream_ordered:  # interior rows need no fence
+                apply_remap_range(self.w, [self.src], [self.dst], self.b0, self.b1, self.variant, main)
+            fence()  # every owner's rows are final
+            if self.b1 > self.b0 and not self.stream_ordered:
                 apply_remap_range(self.w, [self.src], [self.dst], self.b0, self.b1, self.variant, main)
             for a, b in ((0, self.b0), (self.b1, self.m)):
                 if b > a:
                     apply_remap_fused(self.w, self.plan, self.src, self.dst, a, b, self.peer_info, main)
-            self.main.synchronize()
-            self.ctx.barrier()  # nobody overwrites owned rows while a peer still reads them
+            fence()  # nobody overwrites owned rows while a peer still reads them
             return
         if self.multi and not self.stream_ordered:
             self.main.synchronize()

@@ -262,10 +262,12 @@ def apply_remap_fused(weights: InterpolationWeights, plan, source: DeviceArray, 
 
 def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], host_dst: Sequence[np.ndarray],
                  dev_src: Sequence[DeviceArray], dev_dst: Sequence[DeviceArray], nchunks: int = 0,
-                 variant: int = APPLY_DEFAULT) -> int:
+                 variant: int = APPLY_DEFAULT, compact: bool = True) -> int:
     """Host buffers in, host buffers out (sg_remap_execute_host): chunked h2d of the referenced
     source rows, apply, d2h of the target rows, overlapped on three streams.  Host arrays
-    should be pinned (``device.PinnedArray``) for full PCIe rate.  Returns source rows copied."""
+    should be pinned (``device.PinnedArray``) for full PCIe rate.  compact: only the
+    referenced source rows cross PCIe (packed on the host by the library's thread pool).
+    Returns source rows copied."""
     dev = dev_src[0].device
     sh = weights.device_stencil(dev)
     m = len(weights)
@@ -280,7 +282,7 @@ def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], 
     t = np.array([a.handle for a in dev_dst], np.uint64)
     rows = C.c_int64(0)
     N.call("sg_remap_execute_host", sh, N.ptr(s), N.ptr(t), len(s), N.ptr(hs), N.ptr(hd), nchunks, variant,
-           N.ref(rows))
+           int(bool(compact)), N.ref(rows))
     return rows.value
 
 

@@ -216,12 +216,16 @@ def test_execute_host_pipeline_bitwise(gpu):
     hs = PinnedArray((mesh.nb_nodes, L))
     hs.array[:] = np.random.default_rng(3).normal(size=hs.array.shape)
     exp = O.apply_remap(w.nodes, w.weights, hs.array)
-    for nchunks in (1, 3, 17):
-        hd = PinnedArray((len(w), L))
-        ds, dd = DeviceArray(mesh.nb_nodes, L, np.float64), DeviceArray(len(w), L, np.float64)
-        rows = execute_host(w, [hs.array], [hd.array], [ds], [dd], nchunks=nchunks)
-        assert np.array_equal(hd.array.view(np.uint64), exp.view(np.uint64)), nchunks
-        assert w.distinct_sources() <= rows <= mesh.nb_nodes
+    for compact in (False, True):
+        for nchunks in (1, 3, 17):
+            hd = PinnedArray((len(w), L))
+            ds, dd = DeviceArray(mesh.nb_nodes, L, np.float64), DeviceArray(len(w), L, np.float64)
+            rows = execute_host(w, [hs.array], [hd.array], [ds], [dd], nchunks=nchunks, compact=compact)
+            assert np.array_equal(hd.array.view(np.uint64), exp.view(np.uint64)), (nchunks, compact)
+            if compact:
+                assert rows == w.distinct_sources()
+            else:
+                assert w.distinct_sources() <= rows <= mesh.nb_nodes
 
 
 def test_apply_range(gpu):

@@ -8,6 +8,10 @@ timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --mast
   --master-port 29517 bench.py --gpus 2 --steps 5 --warmup 3 --transport ipc --config cfg2 \
   > gpurun_out/bench_multi_ipc.json 2> gpurun_out/bench_multi_ipc.err
 echo "rc=$?" >> gpurun_out/bench_multi_ipc.err
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+  --master-port 29519 bench.py --gpus 2 --steps 5 --warmup 3 --transport ipc --fused --config cfg2 \
+  > gpurun_out/bench_multi_fused.json 2> gpurun_out/bench_multi_fused.err
+echo "rc=$?" >> gpurun_out/bench_multi_fused.err
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
   --master-port 29518 bench.py --impl reference --gpus 2 --steps 2 --warmup 3 --config cfg1 \
   > gpurun_out/bench_multi_ref.json 2> gpurun_out/bench_multi_ref.err
