@@ -191,18 +191,31 @@ def run_reference(args):
     import paper_1908_07038_b200 as sg
 
     source, target, L, F, method = config(args.config)
-    sg.set_device(0)
     t0 = time.time()
-    # stencils: built once on the GPU (untimed setup; at cfg3 the CPU apply
-    # runs on the new build's stencils, verified bit-exact against the reference's locate)
-    S, T, mesh, fs, tdist, w = setup_remap(sg, source, target, 1, 0, None, method)
-    nodes, weights = w.nodes, w.weights
+    # stencils from the scaled oracle — the reference's own algorithm (scipy cKDTree k=8/32
+    # candidates, interp.py:90-117, scored in C with its arithmetic; batched dgesv weights),
+    # not the device build: nothing of the B200 engine runs in this arm
+    from oracle import oracle as O
+
+    S, T = sg.grid_from_name(source), sg.grid_from_name(target)
+    mesh = sg.generate_mesh(S, sg.blocks_partition(S, 1), 0, halo=2, include_pole=True)
+    conn = mesh.element_connectivity
+    txyz = T.xyz()
+    if method == "bilinear":
+        gn, weights, _ = O.bilinear_stencil(S.latitudes, S.nlons, T.lonlats(), True)
+        nodes = gn  # serial mesh: local row == global id (owned grid points, then the poles)
+    else:
+        elem, nodes = O.locate_kdtree(mesh.node_xyz, conn.offsets, conn.indices, txyz)
+        if (elem < 0).any():
+            raise SystemExit("reference arm: target not located")
+        weights = O.barycentric_weights_batched(mesh.node_xyz, nodes, txyz)
+    w_len = len(nodes)
     srcs = []
     for f in range(F):
         a = np.empty((mesh.nb_nodes, L))
         fill_smooth(a, mesh.node_xyz, f)
         srcs.append(a)
-    out = np.empty((len(w), L))
+    out = np.empty((w_len, L))
     nthreads = os.cpu_count() or 1
     log(f"reference setup {time.time() - t0:.1f}s, {nthreads} threads")
     for _ in range(args.warmup):
@@ -214,7 +227,7 @@ def run_reference(args):
         for a in srcs:
             cpu_apply(nodes, weights, a, out, nthreads)
         times.append(time.perf_counter() - t)
-    units = len(w) * L * F
+    units = w_len * L * F
     ms = 1e3 * sum(times) / len(times)
     value = units / (ms * 1e-3) / 1e9
     line = {
@@ -224,7 +237,8 @@ def run_reference(args):
         "impl": "reference",
         "config": {"workload": f"{source}->{target} {'structured-bilinear' if method == 'bilinear' else 'FE'} remap "
                                f"apply, {L} levels x {F} field(s), P=1",
-                   "levels": L, "fields": F, "targets": len(w), "source_nodes": mesh.nb_nodes},
+                   "levels": L, "fields": F, "targets": w_len, "source_nodes": mesh.nb_nodes,
+                   "stencils": "oracle.locate_kdtree (reference algorithm, scipy cKDTree) — no device code"},
         "cpu_baseline": {"value": value, "unit": "Gpts·lev/s", "cores": nthreads, "kind": "port",
                          "sample": f"full {source}->{target} apply per step (oracle port of interp.py:219-223, "
                                    f"numpy, {nthreads} threads over 16k-target chunks)"},
@@ -285,6 +299,9 @@ def run_single(args):
     bitwise = bool(np.array_equal(got.view(np.uint64), exp.view(np.uint64)))
 
     # ---- e2e through the public API: host fields in pinned memory -------------------------
+    import paper_1908_07038_b200.interp as sgi
+
+    sgi.HOST_EXECUTE_MODE = args.e2e_mode
     fsrc = [sg.Field(name=f"src{f}", shape=(n, L), kind=sg.Kind.REAL64, host=hsrc[f].array) for f in range(F)]
     fdst = [sg.Field(name=f"dst{f}", shape=(m, L), kind=sg.Kind.REAL64, host=hdst[f].array) for f in range(F)]
     e2e_steps = max(3, min(args.steps, 10))
@@ -332,7 +349,8 @@ def run_single(args):
                      "kernel_ms": kern_ms, "peak_source": peak_src},
         "e2e": {"value": units / e2e_s / 1e9, "unit": "Gpts·lev/s", "h2d_bytes_per_step": n * L * 8 * F,
                 "d2h_bytes_per_step": m * L * 8 * F, "ms_per_step": e2e_s * 1e3,
-                "api": "paper_1908_07038_b200.apply_remap(weights, host Field, host Field)"},
+                "api": "paper_1908_07038_b200.apply_remap(weights, host Field, host Field)",
+                "mode": args.e2e_mode},
         "cpu_baseline": cpu,
         "gpu_launches": args.steps,
         "parity": {"apply_bitwise_vs_oracle_sample": bitwise, "e2e_bitwise": e2e_ok},
@@ -458,8 +476,10 @@ def run_multi(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
             "config": {"workload": f"{source}->{target} FE remap, {L} levels, blocks_partition P={world}, halo 2; "
-                                   (f"step = fused exchange+apply over peer memory ({args.transport} fences)" if args.fused else
-                                    f"step = halo exchange ({args.transport}) + apply (interior block overlapped when stream-ordered)"),
+                                   + (f"step = fused exchange+apply over peer memory ({args.transport} fences)"
+                                      if args.fused else
+                                      f"step = halo exchange ({args.transport}) + apply (interior block overlapped "
+                                      "when stream-ordered)"),
                        "levels": L, "parallelism": f"domain decomposition x{world}", "l2": "inputs > L2",
                        "cuda_graph": graphed},
             "halo": {"bytes_per_exchange": hsum, "ms": hmax, "GB_per_s": hsum / (hmax * 1e-3) / 1e9},
@@ -482,6 +502,8 @@ def main():
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     ap.add_argument("--variant", type=int, default=0, help="apply kernel: 0 default, 1 warp LDG, 2 TMA bulk")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-mode", default="auto", choices=["auto", "dma", "compact", "zerocopy"],
+                    help="host-buffer execute path for e2e (auto = zero-copy for pinned arrays)")
     ap.add_argument("--fused", action="store_true",
                     help="N>1: no ghost copy — boundary targets read ghost rows from the owners' HBM "
                          "(CUDA IPC / NVLink) inside the apply kernel, fenced by NCCL barriers")

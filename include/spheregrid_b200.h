@@ -154,7 +154,10 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields,
                               int64_t* out_rows_copied);
 /* flags bit 0 (compact): pack exactly the referenced source rows on the host (library thread
  * pool, pinned 3-slot staging ring) and apply from a compact device copy with a renumbered
- * stencil — PCIe carries U rows instead of every row (77 % at cfg3/cfg2). */
+ * stencil — PCIe carries U rows instead of every row (77 % at cfg3/cfg2).
+ * flags bit 1 (zero-copy): the apply kernel reads source rows directly from the pinned host
+ * array over PCIe and writes target rows directly into the pinned host array (mapped
+ * pinned memory required, e.g. sg_host_alloc); no staging and no copy engines. */
 
 /* ---- halo exchange (functionspace.py:58-118) ---------------------------------------------
  * sg_halo_plan_create <- HaloExchangePlan (functionspace.py:47-55): per peer (ascending),

@@ -145,3 +145,71 @@ int oracle_locate(const double* xyz, int64_t n, const int64_t* off, const int64_
   free(cand);
   return 0;
 }
+
+/*
+ * Same scoring, with the candidate nodes supplied: knn[t*k .. t*k+k) are the k nearest mesh
+ * nodes of point t in cKDTree order (interp.py:92 — the caller runs the reference's own
+ * scipy cKDTree query).  Incidence lists are built once per call.  out_elem: -1 not located
+ * among these candidates, -2 DegenerateTriangle.
+ */
+int oracle_locate_knn(const double* xyz, int64_t n, const int64_t* off, const int64_t* idx, int64_t nelem,
+                      const double* pts, int64_t m, const int64_t* knn, int k, int64_t* out_elem,
+                      int64_t* out_corners) {
+  int64_t* cnt = calloc((size_t)n + 1, sizeof(int64_t));
+  for (int64_t e = 0; e < nelem; ++e)
+    for (int64_t i = off[e]; i < off[e + 1]; ++i) cnt[idx[i] + 1]++;
+  for (int64_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
+  int64_t* inc = malloc(sizeof(int64_t) * (size_t)(cnt[n] > 0 ? cnt[n] : 1));
+  int64_t* fill = malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  memcpy(fill, cnt, sizeof(int64_t) * (size_t)n);
+  for (int64_t e = 0; e < nelem; ++e)
+    for (int64_t i = off[e]; i < off[e + 1]; ++i) inc[fill[idx[i]]++] = e;
+  for (int64_t t = 0; t < m; ++t) {
+    v3 p = ld(pts, t);
+    out_elem[t] = -1;
+    out_corners[3 * t] = out_corners[3 * t + 1] = out_corners[3 * t + 2] = -1;
+    int64_t cand[4096];
+    int nc = 0;
+    for (int a = 0; a < k; ++a) {
+      const int64_t node = knn[t * k + a];
+      if (node < 0 || node >= n) continue;
+      for (int64_t q = cnt[node]; q < cnt[node + 1]; ++q) {
+        int64_t e = inc[q];
+        int dup = 0;
+        for (int j = 0; j < nc; ++j)
+          if (cand[j] == e) { dup = 1; break; }
+        if (!dup && nc < 4096) cand[nc++] = e;
+      }
+    }
+    int have = 0;
+    double best = 0.0;
+    for (int c = 0; c < nc && out_elem[t] != -2; ++c) {
+      int64_t tr[2][3];
+      int nt = element_tris(off, idx, cand[c], tr);
+      for (int s = 0; s < nt; ++s) {
+        v3 a = ld(xyz, tr[s][0]), b = ld(xyz, tr[s][1]), cc = ld(xyz, tr[s][2]);
+        v3 ab = cross_np(a, b);
+        if (fabs(dot_blas(ab, cc)) <= 1e-15) {
+          out_elem[t] = -2;
+          break;
+        }
+        double t1 = dot_blas(ab, p), t2 = dot_blas(cross_np(b, cc), p), t3 = dot_blas(cross_np(cc, a), p);
+        double score = t1;
+        if (t2 < score) score = t2;
+        if (t3 < score) score = t3;
+        if (score >= -1e-12 && (!have || score > best)) {
+          have = 1;
+          best = score;
+          out_elem[t] = cand[c];
+          out_corners[3 * t] = tr[s][0];
+          out_corners[3 * t + 1] = tr[s][1];
+          out_corners[3 * t + 2] = tr[s][2];
+        }
+      }
+    }
+  }
+  free(cnt);
+  free(inc);
+  free(fill);
+  return 0;
+}

@@ -747,8 +747,39 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
   }
   SG_REQUIRE(nchunks >= 1 && nchunks <= 1024, "nchunks must be in [1, 1024]");
   DeviceScope ds(s->device);
-  HostPlan* hp = host_plan(s, nchunks);
   const size_t row = (size_t)p.levels * 8;
+  if (flags & 2) {
+    // zero-copy: the apply kernel reads the referenced source rows straight out of pinned
+    // host memory over PCIe and streams the target rows back into pinned host memory — no
+    // staging, no DMA engine, only referenced rows cross the link (U/n = 77 % at cfg3)
+    std::vector<const double*> hs(nfields);
+    std::vector<double*> hd(nfields);
+    for (int f = 0; f < nfields; ++f) {
+      for (int io = 0; io < 2; ++io) {
+        const void* hp_ = reinterpret_cast<const void*>(io ? host_dst[f] : host_src[f]);
+        cudaPointerAttributes at{};
+        SG_CUDA(cudaPointerGetAttributes(&at, hp_));
+        SG_REQUIRE(at.type == cudaMemoryTypeHost && at.devicePointer,
+                   "zero-copy execute needs pinned, mapped host arrays (sg_host_alloc)");
+        if (io) hd[f] = static_cast<double*>(at.devicePointer);
+        else hs[f] = static_cast<const double*>(at.devicePointer);
+      }
+    }
+    cudaStream_t st = 0;
+    for (int f0 = 0; f0 < nfields; f0 += kMaxFields) {
+      ApplyArgs a = make_args(s, p, f0, 0, s->m);
+      for (int f = 0; f < a.nfields; ++f) {
+        a.src[f] = hs[f0 + f];
+        a.dst[f] = hd[f0 + f];
+        a.src_pitch[f] = a.dst_pitch[f] = p.levels;
+      }
+      launch_apply(a, variant == 2 ? 0 : variant, st);
+    }
+    SG_CUDA(cudaStreamSynchronize(st));
+    if (out_rows_copied) *out_rows_copied = s->distinct_sources;
+    return SG_OK;
+  }
+  HostPlan* hp = host_plan(s, nchunks);
   const bool compact = (flags & 1) != 0;
   if (compact) {
     // device compact sources and the pinned staging ring (sized for the largest chunk)

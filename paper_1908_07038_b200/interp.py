@@ -42,6 +42,8 @@ _KNN_FIRST = 8
 _KNN_WIDE = 32
 
 APPLY_DEFAULT, APPLY_WARP, APPLY_BULK = 0, 1, 2
+# host-buffer execute path used by apply_remap on host-resident fields (see execute_host)
+HOST_EXECUTE_MODE = "auto"
 
 
 @dataclass(frozen=True)
@@ -260,14 +262,26 @@ def apply_remap_fused(weights: InterpolationWeights, plan, source: DeviceArray, 
            t0, t1, N.ptr(ptrs), N.ptr(pitch), stream)
 
 
+def _is_pinned(a: np.ndarray) -> bool:
+    """True when ``a`` lives in a library pinned allocation (device.PinnedArray)."""
+    from .device import PinnedArray
+
+    base = a
+    while isinstance(base, np.ndarray) and base.base is not None:
+        base = base.base
+    return getattr(base, "_sg_owner", None) is not None and isinstance(base._sg_owner, PinnedArray)
+
+
 def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], host_dst: Sequence[np.ndarray],
                  dev_src: Sequence[DeviceArray], dev_dst: Sequence[DeviceArray], nchunks: int = 0,
-                 variant: int = APPLY_DEFAULT, compact: bool = True) -> int:
+                 variant: int = APPLY_DEFAULT, mode: str = "auto") -> int:
     """Host buffers in, host buffers out (sg_remap_execute_host): chunked h2d of the referenced
     source rows, apply, d2h of the target rows, overlapped on three streams.  Host arrays
-    should be pinned (``device.PinnedArray``) for full PCIe rate.  compact: only the
-    referenced source rows cross PCIe (packed on the host by the library's thread pool).
-    Returns source rows copied."""
+    should be pinned (``device.PinnedArray``) for full PCIe rate.  mode: "dma" (chunked
+    copies of the referenced row runs), "compact" (only referenced rows, packed on the host by
+    the library's thread pool), "zerocopy" (the kernel reads/writes the pinned host arrays
+    directly over PCIe), "auto" (zerocopy when both host arrays are pinned, else dma).
+    Returns source rows moved."""
     dev = dev_src[0].device
     sh = weights.device_stencil(dev)
     m = len(weights)
@@ -281,8 +295,11 @@ def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], 
     s = np.array([a.handle for a in dev_src], np.uint64)
     t = np.array([a.handle for a in dev_dst], np.uint64)
     rows = C.c_int64(0)
+    if mode == "auto":
+        mode = "zerocopy" if all(_is_pinned(a) for a in list(host_src) + list(host_dst)) else "dma"
+    flags = {"dma": 0, "compact": 1, "zerocopy": 2}[mode]
     N.call("sg_remap_execute_host", sh, N.ptr(s), N.ptr(t), len(s), N.ptr(hs), N.ptr(hd), nchunks, variant,
-           int(bool(compact)), N.ref(rows))
+           flags, N.ref(rows))
     return rows.value
 
 
@@ -308,7 +325,7 @@ def apply_remap(weights: InterpolationWeights, source_field: Field, target_field
     th = target_field.host
     direct = th.dtype == np.float64 and th.flags["C_CONTIGUOUS"] and th.flags["WRITEABLE"]
     out = th if direct else np.empty(target_field.shape, np.float64)
-    execute_host(weights, [host_src], [out], [src], [dst])
+    execute_host(weights, [host_src], [out], [src], [dst], mode=HOST_EXECUTE_MODE)
     if not direct:
         th[:] = out
     if target_field.state is MemoryState.SYNCED:

@@ -216,16 +216,23 @@ def test_execute_host_pipeline_bitwise(gpu):
     hs = PinnedArray((mesh.nb_nodes, L))
     hs.array[:] = np.random.default_rng(3).normal(size=hs.array.shape)
     exp = O.apply_remap(w.nodes, w.weights, hs.array)
-    for compact in (False, True):
+    for mode in ("dma", "compact", "zerocopy"):
         for nchunks in (1, 3, 17):
             hd = PinnedArray((len(w), L))
             ds, dd = DeviceArray(mesh.nb_nodes, L, np.float64), DeviceArray(len(w), L, np.float64)
-            rows = execute_host(w, [hs.array], [hd.array], [ds], [dd], nchunks=nchunks, compact=compact)
-            assert np.array_equal(hd.array.view(np.uint64), exp.view(np.uint64)), (nchunks, compact)
-            if compact:
-                assert rows == w.distinct_sources()
-            else:
+            rows = execute_host(w, [hs.array], [hd.array], [ds], [dd], nchunks=nchunks, mode=mode)
+            assert np.array_equal(hd.array.view(np.uint64), exp.view(np.uint64)), (nchunks, mode)
+            if mode == "dma":
                 assert w.distinct_sources() <= rows <= mesh.nb_nodes
+            else:
+                assert rows == w.distinct_sources()
+    # pageable host arrays cannot be read zero-copy: "auto" falls back to dma
+    hp = np.ascontiguousarray(hs.array)
+    out = np.empty((len(w), L))
+    execute_host(w, [hp], [out], [ds], [dd])
+    assert np.array_equal(out.view(np.uint64), exp.view(np.uint64))
+    with pytest.raises(Exception):
+        execute_host(w, [hp], [out], [ds], [dd], mode="zerocopy")
 
 
 def test_apply_range(gpu):
@@ -325,3 +332,43 @@ def test_empty_and_tiny_cases(gpu):
     src.upload(h)
     sg.apply_remap_device(w1, [src], [dst])
     assert np.array_equal(dst.to_numpy().view(np.uint64), O.apply_remap(w1.nodes, w1.weights, h).view(np.uint64))
+
+
+def test_o1280_o640_full_stencils_vs_scaled_oracle(gpu, golden):
+    """cfg3 geometry, ALL 1,661,440 targets: device stencils equal the scaled oracle's
+    (the reference's own cKDTree candidates + its scoring order, oracle.locate_kdtree), and
+    weights are within 1e-13 of the batched dgesv weights."""
+    sg = gpu
+    z = golden("o1280_o640_sample")
+    S = sg.grid_with_latitudes("O1280", z["src_lat"])
+    T = sg.grid_with_latitudes("O640", z["tgt_lat"])
+    dist = sg.blocks_partition(S, 1)
+    mesh = sg.generate_mesh(S, dist, 0, halo=2, include_pole=True)
+    w = sg.build_remap(sg.NodeColumns(mesh, None), T, sg.matching_partition(T, S, dist))
+    conn = mesh.element_connectivity
+    txyz = T.xyz()
+    elem, corners = O.locate_kdtree(mesh.node_xyz, conn.offsets, conn.indices, txyz)
+    assert (elem >= 0).all()
+    assert np.array_equal(w.nodes, corners)
+    ow = O.barycentric_weights_batched(mesh.node_xyz, corners, txyz)
+    assert np.abs(w.weights - ow).max() <= W_TOL
+
+
+@pytest.mark.parametrize("P,ranks", [(8, [0, 3, 7]), (4, [1])])
+def test_o1280_partitioned_stencils_vs_scaled_oracle(gpu, golden, P, ranks):
+    """cfg3 partitioned (blocks P, mesh halo 2): every owned target of the checked ranks has
+    the reference's local stencil (SURVEY.md A17 checked 3,340 samples of P=8 rank 3)."""
+    sg = gpu
+    z = golden("o1280_o640_sample")
+    S = sg.grid_with_latitudes("O1280", z["src_lat"])
+    T = sg.grid_with_latitudes("O640", z["tgt_lat"])
+    dist = sg.blocks_partition(S, P)
+    td = sg.matching_partition(T, S, dist)
+    txyz = T.xyz()
+    for r in ranks:
+        mesh = sg.generate_mesh(S, dist, r, halo=2, include_pole=True)
+        w = sg.build_remap(sg.NodeColumns(mesh, None), T, td)
+        conn = mesh.element_connectivity
+        elem, corners = O.locate_kdtree(mesh.node_xyz, conn.offsets, conn.indices, txyz[w.target_global])
+        assert (elem >= 0).all()
+        assert np.array_equal(w.nodes, corners), r

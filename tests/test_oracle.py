@@ -91,3 +91,18 @@ def test_oracle_gaussian_latitudes_equal_reference(golden, n):
 def test_oracle_blocks_partition():
     assert np.array_equal(O.blocks_partition(10, 3), sg.blocks_partition(sg.grid_from_name("F1"), 3).part_of[:0]
                           if False else np.array([0, 0, 0, 0, 1, 1, 1, 2, 2, 2], np.int32))
+
+
+@pytest.mark.parametrize("name,src,tgt", [("cfg1_O32_O16", "O32", "O16"), ("cfg2_O320_O160", "O320", "O160")])
+def test_oracle_kdtree_locate_equals_reference(golden, name, src, tgt):
+    """The scaled oracle (scipy cKDTree candidates + C scoring) reproduces the reference's
+    full stencils (cfg2: 108,160 targets)."""
+    z = golden(name)
+    S, mesh = serial_mesh(z, src)
+    T = sg.grid_with_latitudes(tgt, z["tgt_lat"])
+    conn = mesh.element_connectivity
+    elem, corners = O.locate_kdtree(mesh.node_xyz, conn.offsets, conn.indices, T.xyz()[z["target_global"]])
+    assert (elem >= 0).all()
+    assert np.array_equal(corners, z["nodes"])
+    w = O.barycentric_weights_batched(mesh.node_xyz, corners, T.xyz()[z["target_global"]])
+    assert np.abs(w - z["weights"]).max() < 1e-14
