@@ -1,0 +1,49 @@
+"""The NCCL plumbing on one GPU (a single-rank communicator): dlopen + symbol resolution,
+unique id, communicator creation, grouped send/recv of an exchange with no peers, the
+stream-ordered barrier, and capture of barrier + exchange + apply into a CUDA graph.  The
+multi-rank exchange needs one GPU per rank (NCCL refuses two ranks on one device)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_single_rank_nccl_comm_barrier_and_graph(gpu):
+    sg = gpu
+    import paper_1908_07038_b200._native as N
+    from oracle import oracle as O
+    from paper_1908_07038_b200.device import DeviceArray, Graph, Stream
+
+    uid = (C.c_uint8 * 128)()
+    N.call("sg_nccl_unique_id", N.ref(uid), 128)
+    h = C.c_uint64(0)
+    N.call("sg_comm_create", 0, 1, 0, N.ref(uid), 128, N.ref(h))
+    comm = N.Handle(h.value)
+    g, t = sg.grid_from_name("O32"), sg.grid_from_name("O16")
+    dist = sg.blocks_partition(g, 1)
+    mesh = sg.generate_mesh(g, dist, 0, halo=0, include_pole=True)
+    fs = sg.NodeColumns(mesh, None)
+    w = sg.build_remap(fs, t, sg.matching_partition(t, g, dist))
+    hsrc = np.random.default_rng(2).normal(size=(mesh.nb_nodes, 7))
+    src, dst = DeviceArray(mesh.nb_nodes, 7, np.float64), DeviceArray(len(w), 7, np.float64)
+    src.upload(hsrc)
+    st = Stream(0)
+    plan = fs.exchange_plan
+    plan.exchange_nccl(src, comm.handle, st.stream)  # no peers: pack/unpack skipped, empty group
+    N.call("sg_comm_barrier", comm.handle, st.stream)
+    st.synchronize()
+
+    def body():
+        N.call("sg_comm_barrier", comm.handle, st.stream)
+        plan.exchange_nccl(src, comm.handle, st.stream)
+        sg.apply_remap_device(w, [src], [dst], stream=st.stream)
+        N.call("sg_comm_barrier", comm.handle, st.stream)
+
+    graph = Graph(0, st.stream, body)
+    for _ in range(3):
+        graph.launch(st.stream)
+    st.synchronize()
+    exp = O.apply_remap(w.nodes, w.weights, hsrc)
+    assert np.array_equal(dst.to_numpy().view(np.uint64), exp.view(np.uint64))
