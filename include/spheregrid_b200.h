@@ -92,7 +92,7 @@ int32_t sg_field_info(uint64_t field, int32_t* out_device, int64_t* out_npts,
  *   (interp.py:179-190).  Returns a device stencil handle for sg_remap_apply and copies the
  *   InterpolationWeights arrays (interp.py:120-133) to the caller's host buffers.
  *   out_status[k]: 0 located, 1 not located (fallback row if allow_fallback),
- *   2 degenerate candidate triangle, 3 singular / zero-sum weights.
+ *   2 degenerate candidate triangle, 3 singular vertex matrix, 4 zero weight sum.
  *   On status SG_DOMAIN_ERROR *out_first_bad is the first (ascending) offending row and
  *   the message carries the reference exception class (NotLocated / DegenerateTriangle).
  * sg_stencil_create: device stencil from host arrays (an InterpolationWeights built

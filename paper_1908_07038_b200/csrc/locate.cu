@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(128) locate_kernel(LocView v, const double* pt
       } else {
         const double s = __dadd_rn(__dadd_rn(x[0], x[1]), x[2]);  // w.sum()
         if (s == 0.0) {
-          st = 3;
+          st = 4;  // interp.py:69-70
         } else {
           w[0] = x[0] / s; w[1] = x[1] / s; w[2] = x[2] / s;
           const V3 vproj = V3{__fma_rn(w[2], c.x, __fma_rn(w[1], b.x, __dmul_rn(w[0], a.x))),
@@ -690,6 +690,9 @@ int32_t sg_remap_build(uint64_t locator, const double* target_xyz, int64_t m, in
                       (long long)first_bad);
     if (bad_kind == 2)
       sg::throw_error(SG_DOMAIN_ERROR, "DegenerateTriangle: degenerate candidate triangle for target row %lld",
+                      (long long)first_bad);
+    if (bad_kind == 4)
+      sg::throw_error(SG_DOMAIN_ERROR, "DegenerateTriangle: projection plane through the origin (target row %lld)",
                       (long long)first_bad);
     sg::throw_error(SG_DOMAIN_ERROR, "DegenerateTriangle: singular vertex matrix for target row %lld",
                     (long long)first_bad);

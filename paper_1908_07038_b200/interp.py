@@ -207,7 +207,9 @@ def build_remap(source_fs: NodeColumns, target: Grid, target_dist: Distribution,
                     target_global_index=t,
                 )
             if "singular" in msg:
-                raise DegenerateTriangle("singular vertex matrix")
+                raise DegenerateTriangle("singular vertex matrix")  # interp.py:66-67
+            if "origin" in msg:
+                raise DegenerateTriangle("projection plane through the origin")  # interp.py:69-70
             raise DegenerateTriangle(f"degenerate candidate triangle near target point {t}")
         N.check(rc)
     return InterpolationWeights(

@@ -47,3 +47,51 @@ def test_single_rank_nccl_comm_barrier_and_graph(gpu):
     st.synchronize()
     exp = O.apply_remap(w.nodes, w.weights, hsrc)
     assert np.array_equal(dst.to_numpy().view(np.uint64), exp.view(np.uint64))
+
+
+def test_fork_join_capture_with_single_rank_nccl(gpu):
+    """The multi-GPU step's graph shape: fork a second stream from the main stream with an
+    event, run the (NCCL) exchange there while the main stream applies, join with a second
+    event, then finish on the main stream — captured once and replayed."""
+    sg = gpu
+    import paper_1908_07038_b200._native as N
+    from oracle import oracle as O
+    from paper_1908_07038_b200.device import DeviceArray, Event, Graph, Stream
+    from paper_1908_07038_b200.interp import apply_remap_range
+
+    uid = (C.c_uint8 * 128)()
+    N.call("sg_nccl_unique_id", N.ref(uid), 128)
+    h = C.c_uint64(0)
+    N.call("sg_comm_create", 0, 1, 0, N.ref(uid), 128, N.ref(h))
+    comm = N.Handle(h.value)
+    g, t = sg.grid_from_name("O64"), sg.grid_from_name("O32")
+    dist = sg.blocks_partition(g, 1)
+    mesh = sg.generate_mesh(g, dist, 0, halo=0, include_pole=True)
+    fs = sg.NodeColumns(mesh, None)
+    w = sg.build_remap(fs, t, sg.matching_partition(t, g, dist))
+    m = len(w)
+    hsrc = np.random.default_rng(5).normal(size=(mesh.nb_nodes, 33))
+    src, dst = DeviceArray(mesh.nb_nodes, 33, np.float64), DeviceArray(m, 33, np.float64)
+    src.upload(hsrc)
+    main, side = Stream(0), Stream(0)
+    fork, join = Event(0), Event(0)
+    fs.exchange_plan.exchange_nccl(src, comm.handle, side.stream)  # warm: buffers exist
+    side.synchronize()
+
+    def body():
+        fork.record(main.stream)
+        side.wait(fork)
+        fs.exchange_plan.exchange_nccl(src, comm.handle, side.stream)
+        N.call("sg_comm_barrier", comm.handle, side.stream)
+        apply_remap_range(w, [src], [dst], 0, m // 3, 0, side.stream)
+        join.record(side.stream)
+        apply_remap_range(w, [src], [dst], m // 3, 2 * m // 3, 0, main.stream)
+        main.wait(join)
+        apply_remap_range(w, [src], [dst], 2 * m // 3, m, 0, main.stream)
+
+    graph = Graph(0, main.stream, body)
+    for _ in range(2):
+        graph.launch(main.stream)
+    main.synchronize()
+    exp = O.apply_remap(w.nodes, w.weights, hsrc)
+    assert np.array_equal(dst.to_numpy().view(np.uint64), exp.view(np.uint64))
