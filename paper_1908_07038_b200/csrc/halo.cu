@@ -310,6 +310,8 @@ int32_t sg_comm_create(int32_t device, int32_t nranks, int32_t rank, const uint8
   c->nranks = nranks;
   c->rank = rank;
   SG_NCCL(nccl().CommInitRank(&c->comm, nranks, uid, rank));
+  c->token.alloc(device, 16);  // barrier word: allocated here, never inside a graph capture
+  SG_CUDA(cudaMemset(c->token.ptr, 0, 16));
   *out_comm = registry_put(c.release());
   SG_API_END
 }
@@ -322,10 +324,6 @@ int32_t sg_comm_barrier(uint64_t comm, uint64_t stream) {
   SG_API_BEGIN
   Comm* c = get<Comm>(comm, ObjKind::Comm);
   DeviceScope ds(c->device);
-  if (!c->token.ptr) {
-    c->token.alloc(c->device, 16);
-    SG_CUDA(cudaMemset(c->token.ptr, 0, 16));
-  }
   SG_NCCL(nccl().AllReduce(c->token.ptr, c->token.ptr, 1, /*ncclInt32*/ 2, /*ncclSum*/ 0, c->comm, as_stream(stream)));
   SG_API_END
 }

@@ -106,3 +106,37 @@ def test_oracle_kdtree_locate_equals_reference(golden, name, src, tgt):
     assert np.array_equal(corners, z["nodes"])
     w = O.barycentric_weights_batched(mesh.node_xyz, corners, T.xyz()[z["target_global"]])
     assert np.abs(w - z["weights"]).max() < 1e-14
+
+
+def test_bilinear_restatement_properties():
+    """The structured-bilinear definition (no reference counterpart): weights form a partition
+    of unity, stencil nodes lie in the bracketing rows, and a grid remapped onto itself is the
+    identity to rounding (every target sits on a node)."""
+    S = sg.grid_from_name("O32")
+    gn, w, ok = O.bilinear_stencil(S.latitudes, S.nlons, S.lonlats(), True)
+    assert ok.all()
+    assert np.abs(w.sum(axis=1) - 1.0).max() < 1e-15
+    vals = np.random.default_rng(0).normal(size=(S.npts + 2, 2))
+    out = O.apply_remap_k(gn, w, vals)
+    assert np.abs(out - vals[: S.npts]).max() < 1e-12  # alpha = (360 i / n) n / 360 - i is 0 up to rounding
+    T = sg.grid_from_name("F8")
+    gn, w, ok = O.bilinear_stencil(S.latitudes, S.nlons, T.lonlats(), True)
+    rows = np.searchsorted(S.row_offset, gn, side="right") - 1
+    assert (np.abs(rows[:, 2] - rows[:, 0]) <= 1).all()
+
+
+def test_bench_reference_arm_runs_on_cpu():
+    """bench.py --impl reference (the reference's apply on host threads, stencils from the
+    scaled oracle) prints one JSON line with the contract's keys."""
+    import json
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "cfg1", "--steps", "2",
+                          "--warmup", "3"], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
