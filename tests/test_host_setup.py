@@ -74,3 +74,20 @@ def test_serial_mesh_counts():
 def test_split_quad_lowest_local_index():
     tri = sg.split_quad(np.array([7, 3, 9, 5]))
     assert [t.tolist() for t in tri] == [[3, 9, 5], [3, 5, 7]]
+
+
+def test_dump_field_format():
+    """field.py:190-202 format (the reference's own expected layout, test_field.py:250)."""
+    import io
+
+    f = sg.create_field("t", (2, 2))
+    f.host[:] = [[1.5, 2.0], [1e-300, -3.25]]
+    buf = io.StringIO()
+    sg.dump_field(f, np.array([7, 9]), buf)
+    assert buf.getvalue().splitlines() == ["# field: t", "# shape: 2 2", "# kind: real64", "7 0 1.5", "7 1 2",
+                                           "9 0 1e-300", "9 1 -3.25"]
+
+
+def test_distribution_to_dict():
+    d = sg.blocks_partition(sg.grid_from_name("F1"), 2)
+    assert d.to_dict() == {"nparts": 2, "counts": [4, 4], "part_of": [0, 0, 0, 0, 1, 1, 1, 1]}
