@@ -58,6 +58,18 @@ __device__ __forceinline__ double ldg_stream1(const double* p) {
   asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
+// HINT: L2 prefetch size qualifier (0 none, 1 128B, 2 256B)
+template <int HINT>
+__device__ __forceinline__ double ldg_hint(const double* p) {
+  double v;
+  if (HINT == 2)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  else if (HINT == 1)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::128B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  else
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ double4 ldg_w4(const double4* p) {
   const double2* q = reinterpret_cast<const double2*>(p);
   const double2 a = __ldg(q), b = __ldg(q + 1);
@@ -114,7 +126,7 @@ __global__ void __launch_bounds__(256) apply_warp_v2(ApplyArgs a) {
 }
 
 // ---- warp per target, 8-B loads (any pitch; dense odd rows) ----------------------------------
-template <int ITERS>
+template <int ITERS, int HINT = 0>
 __global__ void __launch_bounds__(256) apply_warp_v1(ApplyArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t t = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
@@ -132,9 +144,9 @@ __global__ void __launch_bounds__(256) apply_warp_v1(ApplyArgs a) {
     for (int i = 0; i < ITERS; ++i) {
       const int k = lane + 32 * i;
       if (k < L) {
-        v0[i] = ldg_stream1(r0 + k);
-        v1[i] = ldg_stream1(r1 + k);
-        v2[i] = ldg_stream1(r2 + k);
+        v0[i] = ldg_hint<HINT>(r0 + k);
+        v1[i] = ldg_hint<HINT>(r1 + k);
+        v2[i] = ldg_hint<HINT>(r2 + k);
       }
     }
 #pragma unroll
@@ -414,6 +426,9 @@ void launch_apply(ApplyArgs a, int variant, cudaStream_t st) {
         case 4: apply_warp_v2<4><<<grid, 256, 0, st>>>(a); break;
         default: apply_warp_loop<<<grid, 256, 0, st>>>(a); break;
       }
+    } else if ((variant == 4 || variant == 5) && (L + 31) / 32 == 5) {
+      if (variant == 4) apply_warp_v1<5, 2><<<grid, 256, 0, st>>>(a);  // L2::256B prefetch
+      else apply_warp_v1<5, 1><<<grid, 256, 0, st>>>(a);                // L2::128B prefetch
     } else {
       switch ((L + 31) / 32) {
         case 1: apply_warp_v1<1><<<grid, 256, 0, st>>>(a); break;
