@@ -65,6 +65,8 @@ int32_t sg_field_d2h_rows(uint64_t field, int64_t row0, int64_t nrows, void* hos
  * for timing on the launching stream. */
 int32_t sg_host_alloc(size_t bytes, uint64_t* out_ptr);
 int32_t sg_host_free(uint64_t ptr);
+int32_t sg_host_register(uint64_t ptr, size_t bytes);
+int32_t sg_host_unregister(uint64_t ptr);
 int32_t sg_event_create(int32_t device, uint64_t* out_event);
 int32_t sg_event_record(uint64_t event, uint64_t stream);
 int32_t sg_event_elapsed_ms(uint64_t start, uint64_t end, float* out_ms);

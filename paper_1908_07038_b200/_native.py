@@ -39,6 +39,8 @@ _SIGS = {
     "sg_field_info": [u64, vp, vp, vp, vp, vp],
     "sg_host_alloc": [sz, vp],
     "sg_host_free": [u64],
+    "sg_host_register": [u64, sz],
+    "sg_host_unregister": [u64],
     "sg_event_create": [i32, vp],
     "sg_event_record": [u64, u64],
     "sg_event_elapsed_ms": [u64, u64, vp],

@@ -157,6 +157,21 @@ int32_t sg_host_free(uint64_t ptr) {
   SG_API_END
 }
 
+// Page-lock an existing host range (e.g. a numpy array) so h2d/d2h from it run at full PCIe
+// rate and asynchronously; sg_host_unregister undoes it.
+int32_t sg_host_register(uint64_t ptr, size_t bytes) {
+  SG_API_BEGIN
+  SG_REQUIRE(ptr && bytes, "empty range");
+  SG_CUDA(cudaHostRegister(reinterpret_cast<void*>(ptr), bytes, cudaHostRegisterPortable));
+  SG_API_END
+}
+
+int32_t sg_host_unregister(uint64_t ptr) {
+  SG_API_BEGIN
+  SG_CUDA(cudaHostUnregister(reinterpret_cast<void*>(ptr)));
+  SG_API_END
+}
+
 int32_t sg_event_create(int32_t device, uint64_t* out_event) {
   SG_API_BEGIN
   SG_REQUIRE(out_event, "null out pointer");

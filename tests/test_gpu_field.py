@@ -68,3 +68,14 @@ def test_stale_reads_raise(gpu):
         pass
     with pytest.raises(sg.StaleHost):
         f.host_view()
+
+
+def test_pinned_registration_context(gpu):
+    sg = gpu
+    f = sg.create_field("f", (5000, 137))
+    f.host[:] = np.random.default_rng(3).normal(size=f.host.shape)
+    with sg.pinned(f.host):
+        f.allocate_device()
+    assert np.array_equal(f.device.to_numpy(), f.host)
+    with sg.pinned(f.host):  # registering again after unregistering works
+        pass
