@@ -142,9 +142,11 @@ def fill_smooth(out: np.ndarray, xyz: np.ndarray, field_index: int, rows=None) -
         out[r] = basis[:, cols] * fac
 
 
-def setup_remap(sg, source, target, nparts, rank, ctx, method="fe"):
+def setup_remap(sg, source, target, nparts, rank, ctx, method="fe", partitioner="blocks"):
+    from paper_1908_07038_b200.partition import PARTITIONERS
+
     S, T = sg.grid_from_name(source), sg.grid_from_name(target)
-    dist = sg.blocks_partition(S, nparts)
+    dist = PARTITIONERS[partitioner](S, nparts)
     mesh = sg.generate_mesh(S, dist, rank, halo=2, include_pole=True)  # cli.py:131
     fs = sg.NodeColumns(mesh, ctx)
     tdist = sg.matching_partition(T, S, dist)
@@ -384,7 +386,7 @@ def run_multi(args):
     ctx = sg.DistContext(device=local, transport=args.transport)
     source, target, L, F, method = config(args.config)
     t0 = time.time()
-    S, T, mesh, fs, tdist, w = setup_remap(sg, source, target, world, rank, ctx, method)
+    S, T, mesh, fs, tdist, w = setup_remap(sg, source, target, world, rank, ctx, method, args.partitioner)
     m, n = len(w), mesh.nb_nodes
     n_owned = mesh.nb_owned_nodes
     hsrc = PinnedArray((n, L))
@@ -484,7 +486,7 @@ def run_multi(args):
             "metric": metric_name(source, target, method, L), "value": value, "unit": "Gpts·lev/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
-            "config": {"workload": f"{source}->{target} FE remap, {L} levels, blocks_partition P={world}, halo 2; "
+            "config": {"workload": f"{source}->{target} FE remap, {L} levels, {args.partitioner} P={world}, halo 2; "
                                    + (f"step = fused exchange+apply over peer memory ({args.transport} fences)"
                                       if args.fused else
                                       f"step = halo exchange ({args.transport}) + apply (interior block overlapped "
@@ -513,6 +515,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-mode", default="auto", choices=["auto", "dma", "compact", "zerocopy"],
                     help="host-buffer execute path for e2e (auto = zero-copy for pinned arrays)")
+    ap.add_argument("--partitioner", default="blocks", choices=["blocks", "equal_regions"],
+                    help="N>1 source decomposition: the reference's blocks bands, or equal regions")
     ap.add_argument("--fused", action="store_true",
                     help="N>1: no ghost copy — boundary targets read ghost rows from the owners' HBM "
                          "(CUDA IPC / NVLink) inside the apply kernel, fenced by NCCL barriers")

@@ -20,17 +20,19 @@ from .grid import grid_from_name
 from .interp import apply_remap, build_bilinear, build_remap
 from .mesh import generate_mesh
 from .parallel import run_ranks
-from .partition import blocks_partition, matching_partition
+from .partition import PARTITIONERS, matching_partition
 
 
 def run_remap_pipeline(source_name: str, target_name: str, nparts: int, field_spec: str, halo: int = 2,
-                       method: str = "finite-element", devices: Optional[List[int]] = None):
+                       method: str = "finite-element", devices: Optional[List[int]] = None,
+                       partitioner: str = "blocks"):
     source, target = grid_from_name(source_name), grid_from_name(target_name)
+    decompose = PARTITIONERS[partitioner]
     spec = FieldSpec(field_spec)
 
     def rank_program(ctx):
         comm = ctx if ctx.nranks > 1 else None
-        dist = blocks_partition(source, ctx.nranks)
+        dist = decompose(source, ctx.nranks)
         mesh = generate_mesh(source, dist, ctx.rank, halo=halo, include_pole=True)
         fs = NodeColumns(mesh, comm)
         tdist = matching_partition(target, source, dist)

@@ -205,3 +205,31 @@ def test_device_view_numpy_semantics(gpu):
     with f.device_view(sg.Intent.READ) as d:
         assert np.array_equal(d, np.full((2, 3), 3.0))
     assert f.copy_counters == before
+
+
+@pytest.mark.parametrize("P", [4, 8])
+def test_equal_regions_pipeline_and_halo(gpu, P):
+    """Equal-regions partitions (many neighbours per rank): halo ghosts equal their global ids,
+    the distributed remap equals the serial one, stencils equal the scaled oracle's."""
+    g = sg.grid_from_name("O64")
+    d = sg.equal_regions_partition(g, P)
+
+    def prog(ctx):
+        mesh = sg.generate_mesh(g, d, ctx.rank, halo=2, include_pole=True)
+        fs = sg.NodeColumns(mesh, ctx)
+        f = fs.create_field("g", 2, sg.Kind.INT64)
+        own = fs.owned_row_index()
+        f.host[own] = mesh.node_global[own, None]
+        fs.halo_exchange(f, ctx)
+        t = sg.grid_from_name("O32")
+        w = sg.build_remap(fs, t, sg.matching_partition(t, g, d))
+        conn = mesh.element_connectivity
+        e, c = O.locate_kdtree(mesh.node_xyz, conn.offsets, conn.indices, t.xyz()[w.target_global])
+        return (np.array_equal(f.host, np.repeat(mesh.node_global[:, None], 2, axis=1)),
+                len(fs.exchange_plan.peers), bool((e >= 0).all() and np.array_equal(c, w.nodes)))
+
+    res = sg.run_ranks(P, prog)
+    assert all(r[0] and r[2] for r in res)
+    serial, _, _ = sg.run_remap_pipeline("O64", "O32", 1, "harmonic:Y3,1")
+    par, _, msgs = sg.run_remap_pipeline("O64", "O32", P, "harmonic:Y3,1", partitioner="equal_regions")
+    assert np.max(np.abs(serial - par)) < 1e-13 and sum(msgs) == 0

@@ -91,3 +91,21 @@ def test_dump_field_format():
 def test_distribution_to_dict():
     d = sg.blocks_partition(sg.grid_from_name("F1"), 2)
     assert d.to_dict() == {"nparts": 2, "counts": [4, 4], "part_of": [0, 0, 0, 0, 1, 1, 1, 1]}
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8, 16, 32])
+def test_equal_regions_balanced_and_compact(P):
+    """Equal-regions decomposition (extension; the reference has only blocks): part sizes equal
+    blocks_partition's, every part is a compact region (fewer ghosts than bands at P >= 4)."""
+    from paper_1908_07038_b200.partition import eq_regions_collars
+
+    g = sg.grid_from_name("O64")
+    d = sg.equal_regions_partition(g, P)
+    assert sum(eq_regions_collars(P)) == P
+    assert d.counts.tolist() == sg.blocks_partition(g, P).counts.tolist()
+    assert np.array_equal(d.part_of, sg.equal_regions_partition(g, P).part_of)  # deterministic
+    if P >= 4:
+        def ghosts(dist):
+            return sum(int(sg.generate_mesh(g, dist, r, halo=2, include_pole=True).node_ghost.sum())
+                       for r in range(P))
+        assert ghosts(d) < ghosts(sg.blocks_partition(g, P))

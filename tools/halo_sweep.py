@@ -22,11 +22,14 @@ L = 137
 REPS = 20
 
 
-def main(grid="O1280", parts=(2, 4, 8), halos=(1, 2, 3)):
+def main(grid="O1280", parts=(2, 4, 8), halos=(1, 2, 3), partitioners=("blocks", "equal_regions")):
+    from paper_1908_07038_b200.partition import PARTITIONERS
+
     sg.set_device(0)
     g = sg.grid_from_name(grid)
-    for P in parts:
-        dist = sg.blocks_partition(g, P)
+    for pname in partitioners:
+      for P in parts:
+        dist = PARTITIONERS[pname](g, P)
         for h in halos:
             t0 = time.time()
             meshes = [sg.generate_mesh(g, dist, r, halo=h, include_pole=True) for r in range(P)]
@@ -68,7 +71,7 @@ def main(grid="O1280", parts=(2, 4, 8), halos=(1, 2, 3)):
             B = sum(ghosts) * L * 8
             worst = int(np.argmax(ghosts))
             print(json.dumps({
-                "grid": grid, "levels": L, "parts": P, "halo": h, "ghosts_per_rank": ghosts,
+                "grid": grid, "partitioner": pname, "levels": L, "parts": P, "halo": h, "ghosts_per_rank": ghosts,
                 "worst_rank": worst, "worst_rank_MB": ghosts[worst] * L * 8 / 1e6,
                 "bytes_per_exchange": B, "pull_ms_max": max(pull_ms), "pull_ms": pull_ms,
                 "pull_GBps_worst_rank": ghosts[worst] * L * 8 / (pull_ms[worst] * 1e-3) / 1e9,
