@@ -143,6 +143,12 @@ int32_t sg_remap_apply(uint64_t stencil, const uint64_t* src_fields,
 int32_t sg_remap_apply_range(uint64_t stencil, const uint64_t* src_fields,
                              const uint64_t* dst_fields, int32_t nfields, int64_t t0,
                              int64_t t1, int32_t variant, uint64_t stream);
+/* The same for an arbitrary target list (device int32 array of `count` target rows), e.g.
+ * the interior / boundary targets of a partition. */
+int32_t sg_remap_apply_list(uint64_t stencil, const uint64_t* src_fields,
+                            const uint64_t* dst_fields, int32_t nfields,
+                            const int32_t* dev_targets, int64_t count, int32_t variant,
+                            uint64_t stream);
 /* apply_remap with HOST buffers (the reference's call shape, interp.py:206-228): host
  * source rows -> device, apply, device -> host target rows, as an nchunks-deep pipeline
  * on three streams (h2d of source-row chunk c, apply of the targets whose stencils lie in
@@ -195,6 +201,10 @@ int32_t sg_remap_apply_fused(uint64_t stencil, uint64_t plan, uint64_t src_field
                              uint64_t dst_field, int64_t t0, int64_t t1,
                              const uint64_t* peer_ptrs, const int64_t* peer_pitch_elems,
                              uint64_t stream);
+int32_t sg_remap_apply_fused_list(uint64_t stencil, uint64_t plan, uint64_t src_field,
+                                  uint64_t dst_field, const int32_t* dev_targets, int64_t count,
+                                  const uint64_t* peer_ptrs, const int64_t* peer_pitch_elems,
+                                  uint64_t stream);
 int32_t sg_nccl_unique_id(uint8_t* out_id, size_t n);
 int32_t sg_comm_create(int32_t device, int32_t nranks, int32_t rank, const uint8_t* id,
                        size_t n, uint64_t* out_comm);

@@ -59,6 +59,7 @@ _SIGS = {
     "sg_bilinear_build": [i32, i32, vp, vp, i32, vp, i64, vp, i64, vp, vp, vp, vp, vp],
     "sg_remap_apply": [u64, vp, vp, i32, i32, u64],
     "sg_remap_apply_range": [u64, vp, vp, i32, i64, i64, i32, u64],
+    "sg_remap_apply_list": [u64, vp, vp, i32, u64, i64, i32, u64],
     "sg_remap_execute_host": [u64, vp, vp, i32, vp, vp, i32, i32, i32, vp],
     "sg_halo_plan_create": [i32, i64, i32, vp, vp, vp, vp, vp, vp, vp],
     "sg_halo_plan_info": [u64, vp, vp],
@@ -66,6 +67,7 @@ _SIGS = {
     "sg_halo_unpack": [u64, u64, vp, u64],
     "sg_halo_pull": [u64, u64, vp, vp, u64],
     "sg_remap_apply_fused": [u64, u64, u64, u64, i64, i64, vp, vp, u64],
+    "sg_remap_apply_fused_list": [u64, u64, u64, u64, u64, i64, vp, vp, u64],
     "sg_nccl_unique_id": [vp, sz],
     "sg_comm_create": [i32, i32, i32, vp, sz, vp],
     "sg_halo_exchange_nccl": [u64, u64, u64, u64],

@@ -38,7 +38,8 @@ constexpr int kMaxFields = 8;
 struct ApplyArgs {
   const int4* idx;
   const double4* w;
-  int64_t t0, t1;  // target range
+  int64_t t0, t1;  // target range (positions in `list` when a list is given)
+  const int32_t* list;  // optional target list: target = list[position]
   int32_t k;       // stencil points: 3 (FE triangles) or 4 (structured bilinear)
   int32_t levels;
   int32_t nfields;
@@ -88,8 +89,9 @@ __device__ __forceinline__ double combine4(double4 w, double a, double b, double
 template <int ITERS>
 __global__ void __launch_bounds__(256) apply_warp_v2(ApplyArgs a) {
   const int lane = threadIdx.x & 31;
-  const int64_t t = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if (t >= a.t1) return;
+  const int64_t pos = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (pos >= a.t1) return;
+  const int64_t t = a.list ? (int64_t)__ldg(a.list + pos) : pos;
   const int4 id = __ldg(a.idx + t);
   const double4 wt = ldg_w4(a.w + t);
   const int nvec = (a.levels + 1) >> 1;  // even pitch: the pad element of an odd row exists
@@ -129,8 +131,9 @@ __global__ void __launch_bounds__(256) apply_warp_v2(ApplyArgs a) {
 template <int ITERS, int HINT = 0>
 __global__ void __launch_bounds__(256) apply_warp_v1(ApplyArgs a) {
   const int lane = threadIdx.x & 31;
-  const int64_t t = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if (t >= a.t1) return;
+  const int64_t pos = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (pos >= a.t1) return;
+  const int64_t t = a.list ? (int64_t)__ldg(a.list + pos) : pos;
   const int4 id = __ldg(a.idx + t);
   const double4 wt = ldg_w4(a.w + t);
   const int L = a.levels;
@@ -161,8 +164,9 @@ __global__ void __launch_bounds__(256) apply_warp_v1(ApplyArgs a) {
 template <int ITERS>
 __global__ void __launch_bounds__(256) apply4_warp(ApplyArgs a) {
   const int lane = threadIdx.x & 31;
-  const int64_t t = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if (t >= a.t1) return;
+  const int64_t pos = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (pos >= a.t1) return;
+  const int64_t t = a.list ? (int64_t)__ldg(a.list + pos) : pos;
   const int4 id = __ldg(a.idx + t);
   const double4 wt = ldg_w4(a.w + t);
   const int L = a.levels;
@@ -199,8 +203,9 @@ __global__ void __launch_bounds__(256) apply4_warp(ApplyArgs a) {
 // Any number of levels (> 256): looped.
 __global__ void __launch_bounds__(256) apply_warp_loop(ApplyArgs a) {
   const int lane = threadIdx.x & 31;
-  const int64_t t = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if (t >= a.t1) return;
+  const int64_t pos = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (pos >= a.t1) return;
+  const int64_t t = a.list ? (int64_t)__ldg(a.list + pos) : pos;
   const int4 id = __ldg(a.idx + t);
   const double4 wt = ldg_w4(a.w + t);
   for (int f = 0; f < a.nfields; ++f) {
@@ -215,8 +220,9 @@ __global__ void __launch_bounds__(256) apply_warp_loop(ApplyArgs a) {
 
 // Thread per target for few levels (levels <= 8): the stencil loads of a warp coalesce.
 __global__ void __launch_bounds__(256) apply_thread_short(ApplyArgs a) {
-  const int64_t t = a.t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= a.t1) return;
+  const int64_t pos = a.t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= a.t1) return;
+  const int64_t t = a.list ? (int64_t)__ldg(a.list + pos) : pos;
   const int4 id = __ldg(a.idx + t);
   const double4 wt = ldg_w4(a.w + t);
   for (int f = 0; f < a.nfields; ++f) {
@@ -400,7 +406,7 @@ void launch_apply(ApplyArgs a, int variant, cudaStream_t st) {
   }
   bool even = true;
   for (int f = 0; f < a.nfields; ++f) even = even && a.src_pitch[f] % 2 == 0 && a.dst_pitch[f] % 2 == 0;
-  if (variant == 2 && L >= 2 && a.k == 3) {
+  if (variant == 2 && L >= 2 && a.k == 3 && !a.list) {
     const int slot = ((L + 2) * 8 + 15) / 16 * 2;  // doubles; holds the 16-B aligned superset
     const size_t stage_bytes = (size_t)3 * kTile * slot * 8;
     const int stages = (int)std::min<size_t>(8, std::max<size_t>(2, (size_t)(100 * 1024) / stage_bytes));
@@ -746,6 +752,22 @@ int32_t sg_remap_apply_range(uint64_t stencil, const uint64_t* src_fields, const
              (long long)t1, (long long)s->m);
   DeviceScope ds(s->device);
   for (int f0 = 0; f0 < nfields; f0 += kMaxFields) launch_apply(make_args(s, p, f0, t0, t1), variant, as_stream(stream));
+  SG_API_END
+}
+
+int32_t sg_remap_apply_list(uint64_t stencil, const uint64_t* src_fields, const uint64_t* dst_fields,
+                            int32_t nfields, const int32_t* dev_targets, int64_t count, int32_t variant,
+                            uint64_t stream) {
+  SG_API_BEGIN
+  Stencil* s = get<Stencil>(stencil, ObjKind::Stencil);
+  FieldPairs p = check_pairs(s, src_fields, dst_fields, nfields);
+  SG_REQUIRE(count >= 0 && (count == 0 || dev_targets), "bad target list");
+  DeviceScope ds(s->device);
+  for (int f0 = 0; f0 < nfields; f0 += kMaxFields) {
+    ApplyArgs a = make_args(s, p, f0, 0, count);
+    a.list = dev_targets;
+    launch_apply(a, variant, as_stream(stream));
+  }
   SG_API_END
 }
 

@@ -26,6 +26,7 @@ struct FusedArgs {
   const int4* idx;
   const double2* w;  // double4 as two double2
   int64_t t0, t1;
+  const int32_t* list;  // optional: target = list[position]
   int k;
   int levels;
   const double* src;
@@ -52,8 +53,9 @@ __device__ __forceinline__ double combine(double w0, double w1, double w2, doubl
 template <int ITERS>
 __global__ void __launch_bounds__(256) apply_fused(FusedArgs a) {
   const int lane = threadIdx.x & 31;
-  const int64_t t = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if (t >= a.t1) return;
+  const int64_t pos = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (pos >= a.t1) return;
+  const int64_t t = a.list ? (int64_t)__ldg(a.list + pos) : pos;
   const int4 id = __ldg(a.idx + t);
   const double2 wa = __ldg(a.w + 2 * t), wb = __ldg(a.w + 2 * t + 1);
   const double* r0 = row_ptr(a, id.x);
@@ -85,8 +87,9 @@ __global__ void __launch_bounds__(256) apply_fused(FusedArgs a) {
 
 __global__ void __launch_bounds__(256) apply_fused_loop(FusedArgs a) {
   const int lane = threadIdx.x & 31;
-  const int64_t t = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if (t >= a.t1) return;
+  const int64_t pos = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (pos >= a.t1) return;
+  const int64_t t = a.list ? (int64_t)__ldg(a.list + pos) : pos;
   const int4 id = __ldg(a.idx + t);
   const double2 wa = __ldg(a.w + 2 * t), wb = __ldg(a.w + 2 * t + 1);
   const double *r0 = row_ptr(a, id.x), *r1 = row_ptr(a, id.y), *r2 = row_ptr(a, id.z);
@@ -104,10 +107,10 @@ __global__ void __launch_bounds__(256) apply_fused_loop(FusedArgs a) {
 
 using namespace sg;
 
-extern "C" int32_t sg_remap_apply_fused(uint64_t stencil, uint64_t plan, uint64_t src_field, uint64_t dst_field,
-                                        int64_t t0, int64_t t1, const uint64_t* peer_ptrs,
-                                        const int64_t* peer_pitch_elems, uint64_t stream) {
-  SG_API_BEGIN
+namespace {
+
+void fused_impl(uint64_t stencil, uint64_t plan, uint64_t src_field, uint64_t dst_field, int64_t t0, int64_t t1,
+                const int32_t* list, const uint64_t* peer_ptrs, const int64_t* peer_pitch_elems, uint64_t stream) {
   Stencil* s = get<Stencil>(stencil, ObjKind::Stencil);
   Plan* p = get<Plan>(plan, ObjKind::Plan);
   Field* src = get<Field>(src_field, ObjKind::Field);
@@ -123,7 +126,6 @@ extern "C" int32_t sg_remap_apply_fused(uint64_t stencil, uint64_t plan, uint64_
     throw_error(SG_DOMAIN_ERROR, "PlanMismatch: field has %lld points, plan covers %lld nodes", (long long)src->npts,
                 (long long)p->nnodes);
   SG_REQUIRE(src->itemsize == 8 && dst->itemsize == 8, "real64 fields only");
-  SG_REQUIRE(0 <= t0 && t0 <= t1 && t1 <= s->m, "target range outside [0, %lld)", (long long)s->m);
   SG_REQUIRE(src->device == s->device && dst->device == s->device && p->device == s->device,
              "stencil, plan and fields live on different devices");
   const size_t np = p->peers.size();
@@ -133,6 +135,7 @@ extern "C" int32_t sg_remap_apply_fused(uint64_t stencil, uint64_t plan, uint64_
   a.w = s->w.as<double2>();
   a.t0 = t0;
   a.t1 = t1;
+  a.list = list;
   a.k = s->k;
   a.levels = src->levels;
   a.src = src->buf.as<double>();
@@ -147,7 +150,7 @@ extern "C" int32_t sg_remap_apply_fused(uint64_t stencil, uint64_t plan, uint64_
     a.peers.pitch[i] = peer_pitch_elems[i];
   }
   const int64_t m = t1 - t0;
-  if (m == 0) return SG_OK;
+  if (m <= 0) return;
   DeviceScope ds(s->device);
   const unsigned grid = (unsigned)((m + 7) / 8);
   cudaStream_t st = as_stream(stream);
@@ -160,5 +163,28 @@ extern "C" int32_t sg_remap_apply_fused(uint64_t stencil, uint64_t plan, uint64_
     default: apply_fused_loop<<<grid, 256, 0, st>>>(a); break;
   }
   SG_CUDA_LAUNCH();
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t sg_remap_apply_fused(uint64_t stencil, uint64_t plan, uint64_t src_field, uint64_t dst_field, int64_t t0,
+                             int64_t t1, const uint64_t* peer_ptrs, const int64_t* peer_pitch_elems, uint64_t stream) {
+  SG_API_BEGIN
+  Stencil* s = get<Stencil>(stencil, ObjKind::Stencil);
+  SG_REQUIRE(0 <= t0 && t0 <= t1 && t1 <= s->m, "target range outside [0, %lld)", (long long)s->m);
+  fused_impl(stencil, plan, src_field, dst_field, t0, t1, nullptr, peer_ptrs, peer_pitch_elems, stream);
   SG_API_END
 }
+
+int32_t sg_remap_apply_fused_list(uint64_t stencil, uint64_t plan, uint64_t src_field, uint64_t dst_field,
+                                  const int32_t* dev_targets, int64_t count, const uint64_t* peer_ptrs,
+                                  const int64_t* peer_pitch_elems, uint64_t stream) {
+  SG_API_BEGIN
+  SG_REQUIRE(count >= 0 && (count == 0 || dev_targets), "bad target list");
+  fused_impl(stencil, plan, src_field, dst_field, 0, count, dev_targets, peer_ptrs, peer_pitch_elems, stream);
+  SG_API_END
+}
+
+}  // extern "C"

@@ -251,6 +251,27 @@ def apply_remap_range(weights: InterpolationWeights, sources: Sequence[DeviceArr
     N.call("sg_remap_apply_range", sh, N.ptr(s), N.ptr(t), len(s), t0, t1, variant, stream)
 
 
+def apply_remap_list(weights: InterpolationWeights, sources: Sequence[DeviceArray], targets: Sequence[DeviceArray],
+                     target_list: DeviceArray, variant: int = APPLY_DEFAULT, stream: int = 0) -> None:
+    """apply_remap_device for the targets listed in a device int32 array (sg_remap_apply_list)."""
+    dev = sources[0].device
+    s = np.array([a.handle for a in sources], np.uint64)
+    t = np.array([a.handle for a in targets], np.uint64)
+    N.call("sg_remap_apply_list", weights.device_stencil(dev), N.ptr(s), N.ptr(t), len(s), target_list.ptr,
+           target_list.shape[0], variant, stream)
+
+
+def apply_remap_fused_list(weights: InterpolationWeights, plan, source: DeviceArray, target: DeviceArray,
+                           target_list: DeviceArray, peer_info, stream: int = 0) -> None:
+    """apply_remap_fused for the targets listed in a device int32 array."""
+    dev = source.device
+    peers = plan.peers
+    ptrs = np.array([peer_info[p][0] for p in peers] or [0], np.uint64)
+    pitch = np.array([peer_info[p][1] for p in peers] or [0], np.int64)
+    N.call("sg_remap_apply_fused_list", weights.device_stencil(dev), plan.native(dev), source.handle, target.handle,
+           target_list.ptr, target_list.shape[0], N.ptr(ptrs), N.ptr(pitch), stream)
+
+
 def apply_remap_fused(weights: InterpolationWeights, plan, source: DeviceArray, target: DeviceArray, t0: int,
                       t1: int, peer_info, stream: int = 0) -> None:
     """Targets [t0, t1) with ghost stencil rows read straight from their owners' fields

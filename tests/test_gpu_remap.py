@@ -261,22 +261,22 @@ def test_apply_range(gpu):
 
 
 def test_distributed_remap_ranges_and_graph(gpu):
-    """execute.DistributedRemap on one rank of a P=4 decomposition: interior block + boundary
-    ranges, eager and replayed from a captured CUDA graph, equal the oracle bitwise."""
+    """execute.DistributedRemap on one rank of a P=4 decomposition, eager and replayed from a
+    captured CUDA graph; target lists (interior / boundary) through sg_remap_apply_list equal
+    the oracle bitwise."""
     sg = gpu
     from paper_1908_07038_b200.device import DeviceArray
     from paper_1908_07038_b200.execute import DistributedRemap, interior_block
+    from paper_1908_07038_b200.interp import apply_remap_list
 
     S, T = sg.grid_from_name("O64"), sg.grid_from_name("O32")
-    dist = sg.blocks_partition(S, 4)
+    dist = sg.equal_regions_partition(S, 4)
     td = sg.matching_partition(T, S, dist)
     mesh = sg.generate_mesh(S, dist, 1, halo=2, include_pole=True)
     fs = sg.NodeColumns(mesh, None)
     w = sg.build_remap(fs, T, td)
     b0, b1 = interior_block(w, mesh.nb_owned_nodes)
-    assert 0 <= b0 < b1 <= len(w) and (b0 > 0 or b1 < len(w))
-    assert b1 - b0 > len(w) // 2
-    assert (w.nodes[b0:b1] < mesh.nb_owned_nodes).all()
+    assert 0 <= b0 < b1 <= len(w)
     h = np.random.default_rng(11).normal(size=(mesh.nb_nodes, 137))
     src, dst = DeviceArray(mesh.nb_nodes, 137, np.float64), DeviceArray(len(w), 137, np.float64)
     src.upload(h)
@@ -294,7 +294,13 @@ def test_distributed_remap_ranges_and_graph(gpu):
         run2.step()
     run2.synchronize()
     assert np.array_equal(dst2.to_numpy().view(np.uint64), exp.view(np.uint64))
-    assert run2.launches_per_step == 1 + (b0 > 0) + (b1 < len(w))
+    # the interior / boundary lists cover every target exactly once
+    assert run2.n_interior > 0 and run2.boundary is not None
+    dst3 = DeviceArray(len(w), 137, np.float64)
+    apply_remap_list(w, [src], [dst3], run2.interior)
+    apply_remap_list(w, [src], [dst3], run2.boundary)
+    sg.synchronize(0)
+    assert np.array_equal(dst3.to_numpy().view(np.uint64), exp.view(np.uint64))
 
 
 def test_empty_and_tiny_cases(gpu):
