@@ -16,3 +16,7 @@ timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --mast
   --master-port 29518 bench.py --impl reference --gpus 2 --steps 2 --warmup 3 --config cfg1 \
   > gpurun_out/bench_multi_ref.json 2> gpurun_out/bench_multi_ref.err
 echo "rc=$?" >> gpurun_out/bench_multi_ref.err
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
+  --master-port 29520 bench.py --gpus 4 --steps 5 --warmup 3 --transport ipc --fused --partitioner equal_regions \
+  --config cfg2 > gpurun_out/bench_multi_fused_eq4.json 2> gpurun_out/bench_multi_fused_eq4.err
+echo "rc=$?" >> gpurun_out/bench_multi_fused_eq4.err
