@@ -406,7 +406,7 @@ def run_multi(args):
         args.transport = ctx.transport = "ipc"
         run = DistributedRemap(fs, w, ctx, f.device, tf.device, variant=args.variant, fused=args.fused)
     log(f"rank {rank}: setup {time.time() - t0:.1f}s, {n} nodes ({n_owned} owned), {m} targets, "
-        f"interior block {run.b1 - run.b0}, {sum(len(v) for v in fs.exchange_plan.recv.values())} ghosts")
+        f"interior targets {run.n_interior}, {sum(len(v) for v in fs.exchange_plan.recv.values())} ghosts")
     for _ in range(args.warmup):
         run.step()
     run.synchronize()

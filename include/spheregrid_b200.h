@@ -135,7 +135,9 @@ int32_t sg_stencil_info(uint64_t stencil, int64_t* out_m, int64_t* out_source_nn
  * nfields source/target field pairs sharing the stencil.  ShapeMismatch (status 1) with
  * the reference messages when npts / levels disagree (interp.py:208-217).
  * variant: 0 = default (warp per target, vector loads), 2 = TMA bulk-copy (cp.async.bulk)
- * staged gather with a producer warp, 3 = warp per target, 8-B loads.                                                            */
+ * staged gather, producer warp + 16 consumer warps, 1 CTA/SM; 6 = the same with 8-target
+ * tiles, 2 CTAs/SM; 3 = warp per target, 8-B loads; 4 / 5 = 8-B loads with L2::256B /
+ * L2::128B prefetch-size hints.                                                            */
 int32_t sg_remap_apply(uint64_t stencil, const uint64_t* src_fields,
                        const uint64_t* dst_fields, int32_t nfields, int32_t variant,
                        uint64_t stream);

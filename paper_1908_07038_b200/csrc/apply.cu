@@ -236,9 +236,6 @@ __global__ void __launch_bounds__(256) apply_thread_short(ApplyArgs a) {
 }
 
 // ---- TMA bulk-copy staged gather ---------------------------------------------------------------
-constexpr int kTile = 8;  // targets per tile == consumer warps
-constexpr int kConsumerWarps = kTile;
-constexpr int kBulkThreads = (kConsumerWarps + 1) * 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -269,39 +266,58 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32
                : "memory");
 }
 
-// smem: ring of `stages` stages x 3*kTile row slots of `slot` doubles; each slot holds the
+// smem: ring of `stages` stages x 3*TILE row slots of `slot` doubles; each slot holds the
 // 16-B aligned superset of one source row (the row starts at element off = addr%16/8).
-__global__ void __launch_bounds__(kBulkThreads) apply_bulk(ApplyArgs a, int slot, int stages) {
+// Producer warp (lanes = targets of the tile) prefetches the NEXT tile's stencil entries
+// while the current copies fly, so the index load is off the critical path; consumer warps
+// load their weights before waiting on the tile's full barrier.
+template <int TILE>
+__global__ void __launch_bounds__((TILE + 1) * 32) apply_bulk(ApplyArgs a, int slot, int stages) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + stages;
-  unsigned char* offs = reinterpret_cast<unsigned char*>(empty + stages);  // [stages][3*kTile]
-  double* ring = reinterpret_cast<double*>(smem_raw + ((16 * stages + 3 * kTile * stages + 127) / 128) * 128);
-  const int64_t ntiles = (a.t1 - a.t0 + kTile - 1) / kTile;
+  unsigned char* offs = reinterpret_cast<unsigned char*>(empty + stages);  // [stages][3*TILE]
+  double* ring = reinterpret_cast<double*>(smem_raw + ((16 * stages + 3 * TILE * stages + 127) / 128) * 128);
+  const int64_t ntiles = (a.t1 - a.t0 + TILE - 1) / TILE;
   const int64_t nwork = ntiles * a.nfields;  // work item = (tile, field)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&empty[s], TILE);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (warp == kConsumerWarps) {
-    // ===== producer warp: lane j loads target j's stencil and issues its 3 row copies =====
+  if (warp == TILE) {
+    // ===== producer warp =====
+    int4 next_id = make_int4(0, 0, 0, 0);
+    {
+      const int64_t item = blockIdx.x;
+      if (item < nwork) {
+        const int64_t tb = a.t0 + (item / a.nfields) * TILE;
+        if (lane < TILE && tb + lane < a.t1) next_id = __ldg(a.idx + tb + lane);
+      }
+    }
     int it = 0;
     for (int64_t item = blockIdx.x; item < nwork; item += gridDim.x, ++it) {
       const int stage = it % stages;
+      const int4 id = next_id;
+      {  // prefetch the next item's stencil entries
+        const int64_t nitem = item + gridDim.x;
+        if (nitem < nwork) {
+          const int64_t ntb = a.t0 + (nitem / a.nfields) * TILE;
+          if (lane < TILE && ntb + lane < a.t1) next_id = __ldg(a.idx + ntb + lane);
+        }
+      }
       if (it >= stages) mbar_wait(&empty[stage], ((it / stages) - 1) & 1);
       const int64_t tile = item / a.nfields;
       const int f = (int)(item % a.nfields);
-      const int64_t tb = a.t0 + tile * kTile;
-      const int nt = (int)min((int64_t)kTile, a.t1 - tb);
+      const int64_t tb = a.t0 + tile * TILE;
+      const int nt = (int)min((int64_t)TILE, a.t1 - tb);
       uint32_t bytes[3] = {0, 0, 0};
       const double* rows[3] = {nullptr, nullptr, nullptr};
       if (lane < nt) {
-        const int4 id = __ldg(a.idx + tb + lane);
         const int ids[3] = {id.x, id.y, id.z};
         for (int c = 0; c < 3; ++c) {
           const double* r = a.src[f] + (int64_t)ids[c] * a.src_pitch[f];
@@ -309,7 +325,7 @@ __global__ void __launch_bounds__(kBulkThreads) apply_bulk(ApplyArgs a, int slot
           const uintptr_t s0 = p & ~uintptr_t(15), s1 = (p + (uintptr_t)a.levels * 8 + 15) & ~uintptr_t(15);
           rows[c] = reinterpret_cast<const double*>(s0);
           bytes[c] = (uint32_t)(s1 - s0);
-          offs[stage * 3 * kTile + 3 * lane + c] = (unsigned char)((p - s0) >> 3);
+          offs[stage * 3 * TILE + 3 * lane + c] = (unsigned char)((p - s0) >> 3);
         }
       }
       uint32_t total = bytes[0] + bytes[1] + bytes[2];
@@ -317,7 +333,7 @@ __global__ void __launch_bounds__(kBulkThreads) apply_bulk(ApplyArgs a, int slot
       if (lane == 0) mbar_expect_tx(&full[stage], total);
       __syncwarp();
       if (lane < nt) {
-        double* base = ring + (size_t)stage * 3 * kTile * slot;
+        double* base = ring + (size_t)stage * 3 * TILE * slot;
         for (int c = 0; c < 3; ++c) bulk_g2s(base + (3 * lane + c) * slot, rows[c], bytes[c], &full[stage]);
       }
     }
@@ -327,16 +343,17 @@ __global__ void __launch_bounds__(kBulkThreads) apply_bulk(ApplyArgs a, int slot
   int it = 0;
   for (int64_t item = blockIdx.x; item < nwork; item += gridDim.x, ++it) {
     const int stage = it % stages;
-    mbar_wait(&full[stage], (it / stages) & 1);
     const int64_t tile = item / a.nfields;
     const int f = (int)(item % a.nfields);
-    const int64_t tb = a.t0 + tile * kTile;
-    const int nt = (int)min((int64_t)kTile, a.t1 - tb);
+    const int64_t tb = a.t0 + tile * TILE;
+    const int nt = (int)min((int64_t)TILE, a.t1 - tb);
+    double4 wt = make_double4(0, 0, 0, 0);
+    if (warp < nt) wt = ldg_w4(a.w + tb + warp);
+    mbar_wait(&full[stage], (it / stages) & 1);
     if (warp < nt) {
       const int64_t t = tb + warp;
-      const double4 wt = ldg_w4(a.w + t);
-      const double* base = ring + (size_t)stage * 3 * kTile * slot;
-      const unsigned char* o = offs + stage * 3 * kTile + 3 * warp;
+      const double* base = ring + (size_t)stage * 3 * TILE * slot;
+      const unsigned char* o = offs + stage * 3 * TILE + 3 * warp;
       const double* r0 = base + (3 * warp + 0) * slot + o[0];
       const double* r1 = base + (3 * warp + 1) * slot + o[1];
       const double* r2 = base + (3 * warp + 2) * slot + o[2];
@@ -347,6 +364,9 @@ __global__ void __launch_bounds__(kBulkThreads) apply_bulk(ApplyArgs a, int slot
     if (lane == 0) mbar_arrive(&empty[stage]);
   }
 }
+
+template <int TILE>
+void launch_bulk(ApplyArgs a, int L, int64_t m, size_t budget, cudaStream_t st);
 
 __global__ void mark_sources(const int4* idx, int64_t m, int k, unsigned char* mark) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -385,6 +405,22 @@ int num_sms() {
   return n;
 }
 
+template <int TILE>
+void launch_bulk(ApplyArgs a, int L, int64_t m, size_t budget, cudaStream_t st) {
+  const int slot = ((L + 2) * 8 + 15) / 16 * 2;  // doubles; holds the 16-B aligned superset
+  const size_t stage_bytes = (size_t)3 * TILE * slot * 8;
+  const int stages = (int)std::min<size_t>(8, std::max<size_t>(2, budget / stage_bytes));
+  const size_t hdr = ((16 * stages + 3 * TILE * stages + 127) / 128) * 128;
+  const size_t smem = hdr + stages * stage_bytes;
+  SG_REQUIRE(smem <= 220 * 1024, "levels too large for the bulk-copy variant");
+  SG_CUDA(cudaFuncSetAttribute(apply_bulk<TILE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_bulk<TILE>, (TILE + 1) * 32, smem));
+  const int64_t nwork = (m + TILE - 1) / TILE * a.nfields;
+  const int64_t grid = std::min<int64_t>((int64_t)num_sms() * std::max(per_sm, 1), nwork);
+  apply_bulk<TILE><<<(unsigned)grid, (TILE + 1) * 32, smem, st>>>(a, slot, stages);
+}
+
 // Launches the apply of targets [t0, t1) for up to kMaxFields field pairs.
 void launch_apply(ApplyArgs a, int variant, cudaStream_t st) {
   const int64_t m = a.t1 - a.t0;
@@ -406,19 +442,9 @@ void launch_apply(ApplyArgs a, int variant, cudaStream_t st) {
   }
   bool even = true;
   for (int f = 0; f < a.nfields; ++f) even = even && a.src_pitch[f] % 2 == 0 && a.dst_pitch[f] % 2 == 0;
-  if (variant == 2 && L >= 2 && a.k == 3 && !a.list) {
-    const int slot = ((L + 2) * 8 + 15) / 16 * 2;  // doubles; holds the 16-B aligned superset
-    const size_t stage_bytes = (size_t)3 * kTile * slot * 8;
-    const int stages = (int)std::min<size_t>(8, std::max<size_t>(2, (size_t)(100 * 1024) / stage_bytes));
-    const size_t hdr = ((16 * stages + 3 * kTile * stages + 127) / 128) * 128;
-    const size_t smem = hdr + stages * stage_bytes;
-    SG_REQUIRE(smem <= 220 * 1024, "levels too large for the bulk-copy variant");
-    SG_CUDA(cudaFuncSetAttribute(apply_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_bulk, kBulkThreads, smem));
-    const int64_t nwork = (m + kTile - 1) / kTile * a.nfields;
-    const int64_t grid = std::min<int64_t>((int64_t)num_sms() * std::max(per_sm, 1), nwork);
-    apply_bulk<<<(unsigned)grid, kBulkThreads, smem, st>>>(a, slot, stages);
+  if ((variant == 2 || variant == 6) && L >= 2 && a.k == 3 && !a.list) {
+    if (variant == 2) launch_bulk<16>(a, L, m, 200 * 1024, st);  // 1 CTA per SM, 17 warps
+    else launch_bulk<8>(a, L, m, 100 * 1024, st);                // 2 CTAs per SM, 9 warps
   } else if (L <= 8) {
     apply_thread_short<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(a);
   } else {
