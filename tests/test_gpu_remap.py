@@ -127,7 +127,7 @@ def test_apply_variants_multifield_bitwise(gpu):
         srcs = [DeviceArray(mesh.nb_nodes, L, np.float64) for _ in hosts]
         for d, h in zip(srcs, hosts):
             d.upload(h)
-        for variant in (0, 2, 3):
+        for variant in (0, 2, 3, 4, 5, 6, 7):
             dsts = [DeviceArray(len(w), L, np.float64) for _ in hosts]
             sg.apply_remap_device(w, srcs, dsts, variant=variant)
             for d, h in zip(dsts, hosts):

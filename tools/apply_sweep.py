@@ -23,7 +23,7 @@ samp = np.random.default_rng(1).choice(len(w), 3000, replace=False)
 exp = O.apply_remap(w.nodes[samp], w.weights[samp], host)
 res = {}
 for rnd in range(2):
-    for v in (0, 2, 6):
+    for v in (0, 2, 6, 7):
         for _ in range(3):
             sg.apply_remap_device(w, [src], [dst], variant=v)
         e0, e1 = Event(), Event()
