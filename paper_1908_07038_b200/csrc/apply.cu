@@ -443,9 +443,9 @@ void launch_apply(ApplyArgs a, int variant, cudaStream_t st) {
   bool even = true;
   for (int f = 0; f < a.nfields; ++f) even = even && a.src_pitch[f] % 2 == 0 && a.dst_pitch[f] % 2 == 0;
   if ((variant == 2 || variant == 6 || variant == 7) && L >= 2 && a.k == 3 && !a.list) {
-    if (variant == 2) launch_bulk<8>(a, L, m, 56 * 1024, st);       // 2 stages, 4 CTAs/SM, 36 warps
-    else if (variant == 6) launch_bulk<4>(a, L, m, 28 * 1024, st);  // 2 stages, ~8 CTAs/SM, 40 warps
-    else launch_bulk<4>(a, L, m, 42 * 1024, st);                    // 3 stages, ~5 CTAs/SM
+    if (variant == 2) launch_bulk<4>(a, L, m, 42 * 1024, st);       // 3 stages, ~5 CTAs/SM
+    else if (variant == 6) launch_bulk<4>(a, L, m, 56 * 1024, st);  // 4 stages, ~4 CTAs/SM
+    else launch_bulk<2>(a, L, m, 21 * 1024, st);                    // 3 stages, ~10 CTAs/SM
   } else if (L <= 8) {
     apply_thread_short<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(a);
   } else {
