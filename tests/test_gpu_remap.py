@@ -378,3 +378,25 @@ def test_o1280_partitioned_stencils_vs_scaled_oracle(gpu, golden, P, ranks):
         elem, corners = O.locate_kdtree(mesh.node_xyz, conn.offsets, conn.indices, txyz[w.target_global])
         assert (elem >= 0).all()
         assert np.array_equal(w.nodes, corners), r
+
+
+@pytest.mark.parametrize("src,tgt,halo,P", [("O48", "O96", 2, 1), ("F16", "O32", 2, 1), ("O64", "F24", 2, 1),
+                                           ("F12", "F12", 0, 1), ("O80", "O160", 2, 4), ("O96", "F48", 3, 3)])
+def test_grid_pairs_vs_scaled_oracle(gpu, src, tgt, halo, P):
+    """Upsampling (targets next to source nodes: exact score ties), full <-> octahedral, the
+    identity remap and partitioned meshes: every stencil equals the reference algorithm's
+    (oracle.locate_kdtree), every weight within 1e-13."""
+    sg = gpu
+    S, T = sg.grid_from_name(src), sg.grid_from_name(tgt)
+    dist = sg.blocks_partition(S, P)
+    td = sg.matching_partition(T, S, dist)
+    txyz = T.xyz()
+    for r in range(P):
+        mesh = sg.generate_mesh(S, dist, r, halo=halo, include_pole=True)
+        w = sg.build_remap(sg.NodeColumns(mesh, None), T, td)
+        conn = mesh.element_connectivity
+        e, c = O.locate_kdtree(mesh.node_xyz, conn.offsets, conn.indices, txyz[w.target_global])
+        assert (e >= 0).all()
+        assert np.array_equal(w.nodes, c), (src, tgt, r)
+        ow = O.barycentric_weights_batched(mesh.node_xyz, c, txyz[w.target_global])
+        assert np.abs(w.weights - ow).max() <= W_TOL
