@@ -64,6 +64,7 @@ int32_t sg_field_d2h_rows(uint64_t field, int64_t row0, int64_t nrows, void* hos
 /* pinned host buffers (cudaHostAlloc) for asynchronous, full-rate h2d/d2h, and CUDA events
  * for timing on the launching stream. */
 int32_t sg_host_alloc(size_t bytes, uint64_t* out_ptr);
+int32_t sg_host_alloc_flags(size_t bytes, int32_t flags, uint64_t* out_ptr);
 int32_t sg_host_free(uint64_t ptr);
 int32_t sg_host_register(uint64_t ptr, size_t bytes);
 int32_t sg_host_unregister(uint64_t ptr);

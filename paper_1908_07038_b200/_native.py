@@ -38,6 +38,7 @@ _SIGS = {
     "sg_field_d2h_rows": [u64, i64, i64, vp, u64],
     "sg_field_info": [u64, vp, vp, vp, vp, vp],
     "sg_host_alloc": [sz, vp],
+    "sg_host_alloc_flags": [sz, i32, vp],
     "sg_host_free": [u64],
     "sg_host_register": [u64, sz],
     "sg_host_unregister": [u64],

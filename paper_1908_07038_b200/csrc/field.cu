@@ -142,11 +142,15 @@ cudaEvent_t sg_event_raw(uint64_t h) { return get<Event>(h, ObjKind::Event)->ev;
 
 extern "C" {
 
-int32_t sg_host_alloc(size_t bytes, uint64_t* out_ptr) {
+int32_t sg_host_alloc(size_t bytes, uint64_t* out_ptr) { return sg_host_alloc_flags(bytes, 0, out_ptr); }
+
+// flags bit 0: write-combined (fast CPU writes and PCIe reads, very slow CPU reads)
+int32_t sg_host_alloc_flags(size_t bytes, int32_t flags, uint64_t* out_ptr) {
   SG_API_BEGIN
   SG_REQUIRE(out_ptr, "null out pointer");
   void* p = nullptr;
-  SG_CUDA(cudaHostAlloc(&p, std::max<size_t>(bytes, 1), cudaHostAllocPortable));
+  unsigned int f = cudaHostAllocPortable | ((flags & 1) ? cudaHostAllocWriteCombined : 0);
+  SG_CUDA(cudaHostAlloc(&p, std::max<size_t>(bytes, 1), f));
   *out_ptr = reinterpret_cast<uint64_t>(p);
   SG_API_END
 }
