@@ -34,7 +34,7 @@ from .errors import DegenerateTriangle, NotLocated, ShapeMismatch
 from .field import Field, MemoryState
 from .functionspace import NodeColumns
 from .grid import Grid
-from .mesh import Mesh, element_triangles
+from .mesh import Mesh
 from .partition import Distribution
 
 CONTAIN_EPS = 1e-12

@@ -1,11 +1,11 @@
 """H2D / D2H DMA rates on the box: 4 GB contiguous, pinned (portable) vs write-combined,
 one and two streams."""
-import json, os, sys, time
+import json, os, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_1908_07038_b200 as sg
-from paper_1908_07038_b200.device import DeviceArray, PinnedArray, Event, Stream
+from paper_1908_07038_b200.device import DeviceArray, PinnedArray, Event
 sg.set_device(0)
 n = 4 << 30
 rows = n // (137 * 8)
