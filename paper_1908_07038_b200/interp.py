@@ -44,6 +44,7 @@ _KNN_WIDE = 32
 APPLY_DEFAULT, APPLY_WARP, APPLY_BULK = 0, 1, 2
 # host-buffer execute path used by apply_remap on host-resident fields (see execute_host)
 HOST_EXECUTE_MODE = "auto"
+HOST_EXECUTE_CHUNKS = 0  # 0: min(32, targets / 32768)
 
 
 @dataclass(frozen=True)
@@ -350,7 +351,7 @@ def apply_remap(weights: InterpolationWeights, source_field: Field, target_field
     th = target_field.host
     direct = th.dtype == np.float64 and th.flags["C_CONTIGUOUS"] and th.flags["WRITEABLE"]
     out = th if direct else np.empty(target_field.shape, np.float64)
-    execute_host(weights, [host_src], [out], [src], [dst], mode=HOST_EXECUTE_MODE)
+    execute_host(weights, [host_src], [out], [src], [dst], nchunks=HOST_EXECUTE_CHUNKS, mode=HOST_EXECUTE_MODE)
     if not direct:
         th[:] = out
     if target_field.state is MemoryState.SYNCED:
