@@ -389,8 +389,10 @@ __global__ void nearest_node_kernel(const double* xyz, int64_t n, const double* 
   double bd = INFINITY;
   int64_t bi = INT64_MAX;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    double dx = xyz[3 * i] - px, dy = xyz[3 * i + 1] - py, dz = xyz[3 * i + 2] - pz;
-    double d = dx * dx + dy * dy + dz * dz;
+    const double dx = __dsub_rn(xyz[3 * i], px), dy = __dsub_rn(xyz[3 * i + 1], py),
+                 dz = __dsub_rn(xyz[3 * i + 2], pz);
+    // unfused, like cKDTree's squared Euclidean distance (interp.py:186)
+    const double d = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
     if (d < bd || (d == bd && i < bi)) { bd = d; bi = i; }
   }
   __shared__ double sd[256];

@@ -111,6 +111,8 @@ def test_not_located_and_fallback(gpu, golden):
         assert np.array_equal(w.nodes[ok], z[f"r{r}_nodes"][ok])
         assert np.all(w.weights[w.fallback] == [1.0, 0.0, 0.0])
         assert np.all(w.nodes[w.fallback][:, 0] == w.nodes[w.fallback][:, 1])
+        # the fallback node is the reference's cKDTree nearest node (no ties in this case)
+        assert np.array_equal(w.nodes[w.fallback], z[f"r{r}_nodes"][w.fallback])
 
 
 def test_apply_variants_multifield_bitwise(gpu):
