@@ -27,6 +27,8 @@
 #include <cstring>
 #include <memory>
 
+#include <emmintrin.h>
+
 #include "host_pool.h"
 #include "stencil.cuh"
 
@@ -556,6 +558,15 @@ struct HostPlan {
   }
 };
 
+// Row copy into the pinned staging ring with non-temporal 8-B stores (movnti): the staging
+// lines are not read for ownership, cutting host memory traffic of the packing by a third.
+inline void copy_rows_nt(char* dst, const char* src, size_t bytes) {
+  long long* d = reinterpret_cast<long long*>(dst);
+  const long long* s = reinterpret_cast<const long long*>(src);
+  const size_t n = bytes / 8;
+  for (size_t i = 0; i < n; ++i) _mm_stream_si64(d + i, s[i]);
+}
+
 HostPool& host_pool() {
   static HostPool pool(std::max(1u, std::min(32u, std::thread::hardware_concurrency())) - 1);
   return pool;
@@ -877,7 +888,8 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
         const char* host = reinterpret_cast<const char*>(host_src[f]);
         host_pool().parallel_for((nr + grain - 1) / grain, [&](int b) {
           for (int k = b * grain; k < std::min(nr, (b + 1) * grain); ++k)
-            std::memcpy(stage + (runs[k].dst - base) * row, host + runs[k].src * row, (size_t)runs[k].len * row);
+            copy_rows_nt(stage + (runs[k].dst - base) * row, host + runs[k].src * row, (size_t)runs[k].len * row);
+          _mm_sfence();
         });
         if (nrows)
           SG_CUDA(cudaMemcpyAsync(hp->csrc[f]->as<char>() + base * row, stage, (size_t)nrows * row,

@@ -44,7 +44,7 @@ _KNN_WIDE = 32
 APPLY_DEFAULT, APPLY_WARP, APPLY_BULK = 0, 1, 2
 # host-buffer execute path used by apply_remap on host-resident fields (see execute_host)
 HOST_EXECUTE_MODE = "auto"
-HOST_EXECUTE_CHUNKS = 0  # 0: min(32, targets / 32768)
+HOST_EXECUTE_CHUNKS = 0  # 0: min(64, targets / 16384)
 
 
 @dataclass(frozen=True)
@@ -310,7 +310,7 @@ def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], 
     sh = weights.device_stencil(dev)
     m = len(weights)
     if nchunks <= 0:
-        nchunks = int(max(1, min(32, m // 32768)))
+        nchunks = int(max(1, min(64, m // 16384)))
     for a, d in zip(list(host_src) + list(host_dst), list(dev_src) + list(dev_dst)):
         if a.shape != d.shape or a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
             raise ValueError("host arrays must be C-contiguous float64 of the device arrays' shape")
