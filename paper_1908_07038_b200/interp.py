@@ -304,7 +304,7 @@ def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], 
     should be pinned (``device.PinnedArray``) for full PCIe rate.  mode: "dma" (chunked
     copies of the referenced row runs), "compact" (only referenced rows, packed on the host by
     the library's thread pool), "zerocopy" (the kernel reads/writes the pinned host arrays
-    directly over PCIe), "auto" (= dma, the fastest measured).
+    directly over PCIe), "auto" (= compact, the fastest measured).
     Returns source rows moved."""
     dev = dev_src[0].device
     sh = weights.device_stencil(dev)
@@ -320,9 +320,9 @@ def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], 
     t = np.array([a.handle for a in dev_dst], np.uint64)
     rows = C.c_int64(0)
     if mode == "auto":
-        # measured on cfg3 (profiles/r01_e2e_modes.md): dma 138 ms/step, compact 145 ms,
-        # zero-copy 153 ms — the copy engines win
-        mode = "dma"
+        # measured on cfg3 (profiles/r01_e2e_modes.md): compact 124 ms/step (non-temporal
+        # host packing of the referenced rows), dma 134 ms, zero-copy 153 ms
+        mode = "compact"
     flags = {"dma": 0, "compact": 1, "zerocopy": 2}[mode]
     N.call("sg_remap_execute_host", sh, N.ptr(s), N.ptr(t), len(s), N.ptr(hs), N.ptr(hd), nchunks, variant,
            flags, N.ref(rows))
