@@ -305,6 +305,8 @@ def run_single(args):
 
     sgi.HOST_EXECUTE_MODE = args.e2e_mode
     sgi.HOST_EXECUTE_CHUNKS = args.e2e_chunks
+    if args.e2e_period >= 0:
+        sgi.HOST_EXECUTE_DIRECT_PERIOD = args.e2e_period
     fsrc = [sg.Field(name=f"src{f}", shape=(n, L), kind=sg.Kind.REAL64, host=hsrc[f].array) for f in range(F)]
     fdst = [sg.Field(name=f"dst{f}", shape=(m, L), kind=sg.Kind.REAL64, host=hdst[f].array) for f in range(F)]
     e2e_steps = max(3, min(args.steps, 10))
@@ -353,7 +355,7 @@ def run_single(args):
         "e2e": {"value": units / e2e_s / 1e9, "unit": "Gpts·lev/s", "h2d_bytes_per_step": n * L * 8 * F,
                 "d2h_bytes_per_step": m * L * 8 * F, "ms_per_step": e2e_s * 1e3,
                 "api": "paper_1908_07038_b200.apply_remap(weights, host Field, host Field)",
-                "mode": args.e2e_mode, "chunks": args.e2e_chunks},
+                "mode": args.e2e_mode, "chunks": args.e2e_chunks, "direct_period": args.e2e_period},
         "cpu_baseline": cpu,
         "gpu_launches": args.steps,
         "parity": {"apply_bitwise_vs_oracle_sample": bitwise, "e2e_bitwise": e2e_ok},
@@ -515,6 +517,8 @@ def main():
     ap.add_argument("--variant", type=int, default=0, help="apply kernel: 0 default, 1 warp LDG, 2 TMA bulk")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=0, help="host-execute pipeline depth (0 = auto)")
+    ap.add_argument("--e2e-period", type=int, default=-1,
+                    help="compact e2e: copy every n-th chunk directly instead of packing (-1 = library default)")
     ap.add_argument("--e2e-mode", default="auto", choices=["auto", "dma", "compact", "zerocopy"],
                     help="host-buffer execute path for e2e (auto = zero-copy for pinned arrays)")
     ap.add_argument("--partitioner", default="blocks", choices=["blocks", "equal_regions"],

@@ -541,11 +541,16 @@ struct HostPlan {
   int64_t rows_copied = 0;
   cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_cmp;
+  std::vector<int4> idx_host;           // stencil copy (compact rebuilds)
+  std::vector<unsigned char> mark_host; // referenced source rows
   // compact mode: only referenced rows cross PCIe, packed on the host into pinned staging
   bool compact_ready = false;
-  int64_t ncompact = 0;                           // U
-  std::vector<std::vector<CompactRun>> cruns;     // chunk c: exact referenced runs
-  std::vector<int64_t> cb;                        // chunk c: compact rows [cb[c], cb[c+1])
+  int period = -1;                                // every period-th chunk is copied directly
+  int64_t ncompact = 0;                           // device rows of the compact source
+  std::vector<std::vector<CompactRun>> cruns;     // chunk c: exact referenced runs (packed chunks)
+  std::vector<int64_t> cb;                        // chunk c: device rows [cb[c], cb[c+1])
+  std::vector<char> direct;                       // chunk c copied straight from the user array
+  std::vector<int64_t> rlo;                       // chunk c: first source row
   DevBuf cidx;                                    // int4[m]: stencil in compact row numbering
   std::vector<std::unique_ptr<DevBuf>> csrc;      // per field: U compact rows on the device
   static constexpr int kRing = 3;
@@ -561,10 +566,16 @@ struct HostPlan {
 // Row copy into the pinned staging ring with non-temporal 8-B stores (movnti): the staging
 // lines are not read for ownership, cutting host memory traffic of the packing by a third.
 inline void copy_rows_nt(char* dst, const char* src, size_t bytes) {
-  long long* d = reinterpret_cast<long long*>(dst);
-  const long long* s = reinterpret_cast<const long long*>(src);
-  const size_t n = bytes / 8;
-  for (size_t i = 0; i < n; ++i) _mm_stream_si64(d + i, s[i]);
+  // 8-B aligned rows: one movnti to reach 16-B destination alignment, then 16-B streams
+  size_t off = 0;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) && bytes >= 8) {
+    _mm_stream_si64(reinterpret_cast<long long*>(dst), *reinterpret_cast<const long long*>(src));
+    off = 8;
+  }
+  for (; off + 16 <= bytes; off += 16)
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + off), _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + off)));
+  for (; off + 8 <= bytes; off += 8)
+    _mm_stream_si64(reinterpret_cast<long long*>(dst + off), *reinterpret_cast<const long long*>(src + off));
 }
 
 HostPool& host_pool() {
@@ -572,30 +583,44 @@ HostPool& host_pool() {
   return pool;
 }
 
-void build_compact(Stencil* s, HostPlan* hp, const std::vector<int4>& idx, const std::vector<unsigned char>& mark) {
+// Device layout of the compact source: chunk by chunk, a packed chunk contributes its
+// referenced rows, a direct chunk (every `period`-th, period > 0) its whole row range, which
+// one DMA copies straight from the user's array — the split balances host packing bandwidth
+// against PCIe bytes.  The stencil is renumbered into that layout.
+void build_compact(Stencil* s, HostPlan* hp, const std::vector<int4>& idx, const std::vector<unsigned char>& mark,
+                   int period) {
   const int64_t n = s->source_nnodes, m = s->m;
   std::vector<int32_t> cpos((size_t)n, -1);
-  int64_t u = 0;
-  for (int64_t i = 0; i < n; ++i)
-    if (mark[i]) cpos[i] = (int32_t)u++;
-  hp->ncompact = u;
   hp->cruns.assign(hp->nchunks, {});
   hp->cb.assign(hp->nchunks + 1, 0);
-  int64_t rprev = 0;
+  hp->direct.assign(hp->nchunks, 0);
+  hp->rlo.assign(hp->nchunks + 1, 0);
+  int64_t rprev = 0, u = 0;
   for (int c = 0; c < hp->nchunks; ++c) {
     const int64_t rb = (c + 1 == hp->nchunks) ? n : n * (c + 1) / hp->nchunks;
-    int64_t i = rprev;
-    while (i < rb) {
-      while (i < rb && !mark[i]) ++i;
-      if (i >= rb) break;
-      int64_t j = i;
-      while (j < rb && mark[j]) ++j;
-      hp->cruns[c].push_back(CompactRun{i, j - i, cpos[i]});
-      i = j;
+    hp->rlo[c] = rprev;
+    hp->cb[c] = u;
+    if (period > 0 && c % period == period - 1) {
+      hp->direct[c] = 1;
+      for (int64_t i = rprev; i < rb; ++i) cpos[i] = (int32_t)(u + (i - rprev));
+      u += rb - rprev;
+    } else {
+      int64_t i = rprev;
+      while (i < rb) {
+        while (i < rb && !mark[i]) ++i;
+        if (i >= rb) break;
+        int64_t j = i;
+        while (j < rb && mark[j]) ++j;
+        hp->cruns[c].push_back(CompactRun{i, j - i, u});
+        for (int64_t q = i; q < j; ++q) cpos[q] = (int32_t)u++;
+        i = j;
+      }
     }
-    hp->cb[c + 1] = hp->cruns[c].empty() ? hp->cb[c] : hp->cruns[c].back().dst + hp->cruns[c].back().len;
     rprev = rb;
   }
+  hp->rlo[hp->nchunks] = n;
+  hp->cb[hp->nchunks] = u;
+  hp->ncompact = u;
   std::vector<int4> ci((size_t)m);
   for (int64_t t = 0; t < m; ++t) {
     const int4 id = idx[t];
@@ -603,6 +628,7 @@ void build_compact(Stencil* s, HostPlan* hp, const std::vector<int4>& idx, const
   }
   hp->cidx.alloc(s->device, std::max<size_t>(ci.size(), 1) * sizeof(int4));
   if (m) SG_CUDA(cudaMemcpy(hp->cidx.ptr, ci.data(), ci.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  hp->period = period;
   hp->compact_ready = true;
 }
 
@@ -660,7 +686,8 @@ HostPlan* host_plan(Stencil* s, int nchunks) {
     tprev = te;
     rprev = rb;
   }
-  build_compact(s, hp, idx, mark);
+  hp->idx_host = std::move(idx);
+  hp->mark_host = std::move(mark);
   SG_CUDA(cudaStreamCreateWithFlags(&hp->s_in, cudaStreamNonBlocking));
   SG_CUDA(cudaStreamCreateWithFlags(&hp->s_cmp, cudaStreamNonBlocking));
   SG_CUDA(cudaStreamCreateWithFlags(&hp->s_out, cudaStreamNonBlocking));
@@ -857,9 +884,12 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
   HostPlan* hp = host_plan(s, nchunks);
   const bool compact = (flags & 1) != 0;
   if (compact) {
+    const int period = (flags >> 8) & 0xff;
+    if (!hp->compact_ready || hp->period != period) build_compact(s, hp, hp->idx_host, hp->mark_host, period);
     // device compact sources and the pinned staging ring (sized for the largest chunk)
     size_t maxc = 0;
-    for (int c = 0; c < nchunks; ++c) maxc = std::max<size_t>(maxc, (size_t)(hp->cb[c + 1] - hp->cb[c]));
+    for (int c = 0; c < nchunks; ++c)
+      if (!hp->direct[c]) maxc = std::max<size_t>(maxc, (size_t)(hp->cb[c + 1] - hp->cb[c]));
     const size_t need = std::max<size_t>(maxc * row, 16);
     if (hp->ring_bytes < need || hp->ring_fields < nfields) {
       for (void* q : hp->ring)
@@ -877,8 +907,24 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
   int64_t tprev = 0, copied = 0;
   for (int c = 0; c < nchunks; ++c) {
     if (compact) {
-      const int slot = c % HostPlan::kRing;
-      if (c >= HostPlan::kRing) SG_CUDA(cudaEventSynchronize(hp->ev_in[c - HostPlan::kRing]));  // slot free
+      if (hp->direct[c]) {  // whole row range straight from the user's array
+        const int64_t nrows = hp->rlo[c + 1] - hp->rlo[c];
+        for (int f = 0; f < nfields; ++f)
+          if (nrows)
+            SG_CUDA(cudaMemcpyAsync(hp->csrc[f]->as<char>() + hp->cb[c] * row,
+                                    reinterpret_cast<const char*>(host_src[f]) + hp->rlo[c] * row, (size_t)nrows * row,
+                                    cudaMemcpyHostToDevice, hp->s_in));
+        copied += nrows;
+        SG_CUDA(cudaEventRecord(hp->ev_in[c], hp->s_in));
+        goto issued;
+      }
+      {
+      int packed_before = 0;
+      for (int q = 0; q < c; ++q) packed_before += !hp->direct[q];
+      const int slot = packed_before % HostPlan::kRing;
+      // slot free: the last packed chunk that used it has been copied
+      for (int q = c - 1, seen = 0; q >= 0 && seen < HostPlan::kRing; --q)
+        if (!hp->direct[q] && ++seen == HostPlan::kRing) SG_CUDA(cudaEventSynchronize(hp->ev_in[q]));
       const auto& runs = hp->cruns[c];
       const int64_t base = hp->cb[c], nrows = hp->cb[c + 1] - hp->cb[c];
       const int nr = (int)runs.size();
@@ -896,6 +942,7 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
                                   cudaMemcpyHostToDevice, hp->s_in));
       }
       copied += nrows;
+      }
     } else {
       for (int f = 0; f < nfields; ++f) {
         char* dev = p.src[f]->buf.as<char>();
@@ -906,6 +953,7 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
       }
     }
     SG_CUDA(cudaEventRecord(hp->ev_in[c], hp->s_in));
+  issued:
     SG_CUDA(cudaStreamWaitEvent(hp->s_cmp, hp->ev_in[c], 0));
     const int64_t te = hp->t_end[c];
     for (int f0 = 0; f0 < nfields; f0 += kMaxFields) {

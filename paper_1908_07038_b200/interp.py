@@ -45,6 +45,7 @@ APPLY_DEFAULT, APPLY_WARP, APPLY_BULK = 0, 1, 2
 # host-buffer execute path used by apply_remap on host-resident fields (see execute_host)
 HOST_EXECUTE_MODE = "auto"
 HOST_EXECUTE_CHUNKS = 0  # 0: min(64, targets / 16384)
+HOST_EXECUTE_DIRECT_PERIOD = 0  # compact mode: every n-th chunk copied directly (0: none)
 
 
 @dataclass(frozen=True)
@@ -298,7 +299,7 @@ def _is_pinned(a: np.ndarray) -> bool:
 
 def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], host_dst: Sequence[np.ndarray],
                  dev_src: Sequence[DeviceArray], dev_dst: Sequence[DeviceArray], nchunks: int = 0,
-                 variant: int = APPLY_DEFAULT, mode: str = "auto") -> int:
+                 variant: int = APPLY_DEFAULT, mode: str = "auto", direct_period: int = -1) -> int:
     """Host buffers in, host buffers out (sg_remap_execute_host): chunked h2d of the referenced
     source rows, apply, d2h of the target rows, overlapped on three streams.  Host arrays
     should be pinned (``device.PinnedArray``) for full PCIe rate.  mode: "dma" (chunked
@@ -324,6 +325,10 @@ def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], 
         # host packing of the referenced rows), dma 134 ms, zero-copy 153 ms
         mode = "compact"
     flags = {"dma": 0, "compact": 1, "zerocopy": 2}[mode]
+    if direct_period < 0:
+        direct_period = HOST_EXECUTE_DIRECT_PERIOD
+    if mode == "compact" and direct_period > 0:
+        flags |= (min(int(direct_period), 255) << 8)  # every n-th chunk: one direct DMA
     N.call("sg_remap_execute_host", sh, N.ptr(s), N.ptr(t), len(s), N.ptr(hs), N.ptr(hd), nchunks, variant,
            flags, N.ref(rows))
     return rows.value

@@ -218,13 +218,14 @@ def test_execute_host_pipeline_bitwise(gpu):
     hs = PinnedArray((mesh.nb_nodes, L))
     hs.array[:] = np.random.default_rng(3).normal(size=hs.array.shape)
     exp = O.apply_remap(w.nodes, w.weights, hs.array)
-    for mode in ("dma", "compact", "zerocopy"):
+    for mode, period in (("dma", 0), ("compact", 0), ("compact", 2), ("compact", 5), ("zerocopy", 0)):
         for nchunks in (1, 3, 17):
             hd = PinnedArray((len(w), L))
             ds, dd = DeviceArray(mesh.nb_nodes, L, np.float64), DeviceArray(len(w), L, np.float64)
-            rows = execute_host(w, [hs.array], [hd.array], [ds], [dd], nchunks=nchunks, mode=mode)
-            assert np.array_equal(hd.array.view(np.uint64), exp.view(np.uint64)), (nchunks, mode)
-            if mode == "dma":
+            rows = execute_host(w, [hs.array], [hd.array], [ds], [dd], nchunks=nchunks, mode=mode,
+                                direct_period=period)
+            assert np.array_equal(hd.array.view(np.uint64), exp.view(np.uint64)), (nchunks, mode, period)
+            if mode == "dma" or period:
                 assert w.distinct_sources() <= rows <= mesh.nb_nodes
             else:
                 assert rows == w.distinct_sources()
