@@ -109,3 +109,16 @@ def test_equal_regions_balanced_and_compact(P):
             return sum(int(sg.generate_mesh(g, dist, r, halo=2, include_pole=True).node_ghost.sum())
                        for r in range(P))
         assert ghosts(d) < ghosts(sg.blocks_partition(g, P))
+
+
+def test_grid_point_and_geometry_helpers():
+    """grid_point (grid.py:128-135), PointLonLat / lonlat_to_xyz round trip (geometry.py)."""
+    g = sg.grid_from_name("O4")
+    p = sg.grid_point(g, 5)
+    assert p.lat == g.latitudes[0] and p.lon == 360.0 * 5 / 20
+    v = sg.lonlat_to_xyz(sg.PointLonLat(-30.0, 45.0))
+    q = sg.xyz_to_lonlat(v)
+    assert abs(q.lon - 330.0) < 1e-12 and abs(q.lat - 45.0) < 1e-12
+    with pytest.raises(sg.NotOnUnitSphere):
+        sg.PointXYZ(1.0, 1.0, 0.0)
+    assert g.describe()["npts"] == g.npts
