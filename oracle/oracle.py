@@ -244,3 +244,23 @@ def barycentric_weights_batched(xyz, corners, points):
     M = np.stack([xyz[corners[:, 0]], xyz[corners[:, 1]], xyz[corners[:, 2]]], axis=2)
     w = np.linalg.solve(M, points[:, :, None])[:, :, 0]
     return w / w.sum(axis=1, keepdims=True)
+
+
+_MIX = (np.uint64(0x9E3779B97F4A7C15), np.uint64(0xC2B2AE3D27D4EB4F), np.uint64(0xBF58476D1CE4E5B9),
+        np.uint64(0x94D049BB133111EB))
+
+
+def checksum_partial(gids: np.ndarray, values: np.ndarray) -> int:
+    """functionspace.py:233-248 restated: wrapping u64 sum over (point, level) of
+    splitmix64_finalizer(gid*G + (level+1)*Lv ^ value_bits)."""
+    gamma, lev, m1, m2 = _MIX
+    bits = values.view(np.uint64) if values.dtype.itemsize == 8 else values.view(np.uint32).astype(np.uint64)
+    levels = np.arange(values.shape[1], dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        x = (gids.astype(np.uint64)[:, None] * gamma + (levels[None, :] + np.uint64(1)) * lev) ^ bits
+        x ^= x >> np.uint64(30)
+        x *= m1
+        x ^= x >> np.uint64(27)
+        x *= m2
+        x ^= x >> np.uint64(31)
+        return int(np.sum(x, dtype=np.uint64))

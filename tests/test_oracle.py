@@ -140,3 +140,10 @@ def test_bench_reference_arm_runs_on_cpu():
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
+
+
+def test_oracle_checksum_equals_reference(golden):
+    z = golden("checksum")
+    for name in ("O32", "F8", "O16"):
+        vals = z[f"{name}_values"]
+        assert O.checksum_partial(np.arange(len(vals)), vals) == int(z[f"{name}_p1"][0])
