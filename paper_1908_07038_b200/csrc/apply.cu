@@ -24,32 +24,14 @@
 #include <mutex>
 #include <vector>
 
-#include <cstring>
-#include <memory>
-
-#include <emmintrin.h>
-
-#include "host_pool.h"
-#include "stencil.cuh"
+#include "apply_internal.cuh"
 
 namespace sg {
 namespace {
+using detail::ApplyArgs;
+using detail::kMaxFields;
 
-constexpr int kMaxFields = 8;
 
-struct ApplyArgs {
-  const int4* idx;
-  const double4* w;
-  int64_t t0, t1;  // target range (positions in `list` when a list is given)
-  const int32_t* list;  // optional target list: target = list[position]
-  int32_t k;       // stencil points: 3 (FE triangles) or 4 (structured bilinear)
-  int32_t levels;
-  int32_t nfields;
-  const double* src[kMaxFields];
-  double* dst[kMaxFields];
-  int64_t src_pitch[kMaxFields];
-  int64_t dst_pitch[kMaxFields];
-};
 
 __device__ __forceinline__ double2 ldg_stream2(const double2* p) {
   double2 v;
@@ -424,6 +406,9 @@ void launch_bulk(ApplyArgs a, int L, int64_t m, size_t budget, cudaStream_t st) 
 }
 
 // Launches the apply of targets [t0, t1) for up to kMaxFields field pairs.
+}  // namespace
+
+namespace detail {
 void launch_apply(ApplyArgs a, int variant, cudaStream_t st) {
   const int64_t m = a.t1 - a.t0;
   if (m <= 0) return;
@@ -481,10 +466,7 @@ void launch_apply(ApplyArgs a, int variant, cudaStream_t st) {
   SG_CUDA_LAUNCH();
 }
 
-struct FieldPairs {
-  std::vector<Field*> src, dst;
-  int32_t levels = -1;
-};
+
 
 FieldPairs check_pairs(const Stencil* s, const uint64_t* src_fields, const uint64_t* dst_fields, int nfields) {
   SG_REQUIRE(nfields >= 1, "nfields must be >= 1");
@@ -530,194 +512,7 @@ ApplyArgs make_args(const Stencil* s, const FieldPairs& p, int f0, int64_t t0, i
 }
 
 // ---- host pipeline plan (per stencil, built on first use) -----------------------------------
-struct CompactRun {
-  int64_t src, len, dst;  // source row, rows, compact row
-};
-
-struct HostPlan {
-  int nchunks = 0;
-  std::vector<int64_t> t_end;                                  // chunk c: targets [t_end[c-1], t_end[c])
-  std::vector<std::vector<std::pair<int64_t, int64_t>>> runs;  // chunk c: referenced source rows
-  int64_t rows_copied = 0;
-  cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
-  std::vector<cudaEvent_t> ev_in, ev_cmp;
-  std::vector<int4> idx_host;           // stencil copy (compact rebuilds)
-  std::vector<unsigned char> mark_host; // referenced source rows
-  // compact mode: only referenced rows cross PCIe, packed on the host into pinned staging
-  bool compact_ready = false;
-  int period = -1;                                // every period-th chunk is copied directly
-  int64_t ncompact = 0;                           // device rows of the compact source
-  std::vector<std::vector<CompactRun>> cruns;     // chunk c: exact referenced runs (packed chunks)
-  std::vector<int64_t> cb;                        // chunk c: device rows [cb[c], cb[c+1])
-  std::vector<char> direct;                       // chunk c copied straight from the user array
-  std::vector<int64_t> rlo;                       // chunk c: first source row
-  DevBuf cidx;                                    // int4[m]: stencil in compact row numbering
-  std::vector<std::unique_ptr<DevBuf>> csrc;      // per field: U compact rows on the device
-  static constexpr int kRing = 3;
-  std::vector<void*> ring;                        // per (field, slot): pinned staging
-  size_t ring_bytes = 0;
-  int ring_fields = 0;
-  ~HostPlan() {
-    for (void* p : ring)
-      if (p) cudaFreeHost(p);
-  }
-};
-
-// Row copy into the pinned staging ring with non-temporal 8-B stores (movnti): the staging
-// lines are not read for ownership, cutting host memory traffic of the packing by a third.
-inline void copy_rows_nt(char* dst, const char* src, size_t bytes) {
-  // 8-B aligned rows: one movnti to reach 16-B destination alignment, then 16-B streams
-  size_t off = 0;
-  if ((reinterpret_cast<uintptr_t>(dst) & 15) && bytes >= 8) {
-    _mm_stream_si64(reinterpret_cast<long long*>(dst), *reinterpret_cast<const long long*>(src));
-    off = 8;
-  }
-  for (; off + 16 <= bytes; off += 16)
-    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + off), _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + off)));
-  for (; off + 8 <= bytes; off += 8)
-    _mm_stream_si64(reinterpret_cast<long long*>(dst + off), *reinterpret_cast<const long long*>(src + off));
-}
-
-HostPool& host_pool() {
-  static HostPool pool(std::max(1u, std::min(32u, std::thread::hardware_concurrency())) - 1);
-  return pool;
-}
-
-// Device layout of the compact source: chunk by chunk, a packed chunk contributes its
-// referenced rows, a direct chunk (every `period`-th, period > 0) its whole row range, which
-// one DMA copies straight from the user's array — the split balances host packing bandwidth
-// against PCIe bytes.  The stencil is renumbered into that layout.
-void build_compact(Stencil* s, HostPlan* hp, const std::vector<int4>& idx, const std::vector<unsigned char>& mark,
-                   int period) {
-  const int64_t n = s->source_nnodes, m = s->m;
-  std::vector<int32_t> cpos((size_t)n, -1);
-  hp->cruns.assign(hp->nchunks, {});
-  hp->cb.assign(hp->nchunks + 1, 0);
-  hp->direct.assign(hp->nchunks, 0);
-  hp->rlo.assign(hp->nchunks + 1, 0);
-  int64_t rprev = 0, u = 0;
-  for (int c = 0; c < hp->nchunks; ++c) {
-    const int64_t rb = (c + 1 == hp->nchunks) ? n : n * (c + 1) / hp->nchunks;
-    hp->rlo[c] = rprev;
-    hp->cb[c] = u;
-    if (period > 0 && c % period == period - 1) {
-      hp->direct[c] = 1;
-      for (int64_t i = rprev; i < rb; ++i) cpos[i] = (int32_t)(u + (i - rprev));
-      u += rb - rprev;
-    } else {
-      int64_t i = rprev;
-      while (i < rb) {
-        while (i < rb && !mark[i]) ++i;
-        if (i >= rb) break;
-        int64_t j = i;
-        while (j < rb && mark[j]) ++j;
-        hp->cruns[c].push_back(CompactRun{i, j - i, u});
-        for (int64_t q = i; q < j; ++q) cpos[q] = (int32_t)u++;
-        i = j;
-      }
-    }
-    rprev = rb;
-  }
-  hp->rlo[hp->nchunks] = n;
-  hp->cb[hp->nchunks] = u;
-  hp->ncompact = u;
-  std::vector<int4> ci((size_t)m);
-  for (int64_t t = 0; t < m; ++t) {
-    const int4 id = idx[t];
-    ci[t] = make_int4(cpos[id.x], cpos[id.y], cpos[id.z], s->k == 4 ? cpos[id.w] : 0);
-  }
-  hp->cidx.alloc(s->device, std::max<size_t>(ci.size(), 1) * sizeof(int4));
-  if (m) SG_CUDA(cudaMemcpy(hp->cidx.ptr, ci.data(), ci.size() * sizeof(int4), cudaMemcpyHostToDevice));
-  hp->period = period;
-  hp->compact_ready = true;
-}
-
-std::mutex g_plan_mu;
-
-HostPlan* host_plan(Stencil* s, int nchunks) {
-  std::lock_guard<std::mutex> lk(g_plan_mu);
-  auto* hp = static_cast<HostPlan*>(s->host_plan);
-  if (hp && hp->nchunks == nchunks) return hp;
-  s->destroy_host_plan();
-  auto owned = std::make_unique<HostPlan>();
-  hp = owned.get();
-  hp->nchunks = nchunks;
-  const int64_t m = s->m, n = s->source_nnodes;
-  std::vector<int4> idx((size_t)m);
-  if (m) SG_CUDA(cudaMemcpy(idx.data(), s->idx.ptr, (size_t)m * sizeof(int4), cudaMemcpyDeviceToHost));
-  std::vector<unsigned char> mark((size_t)n, 0);
-  std::vector<int64_t> pmax((size_t)m);
-  int64_t run_max = -1;
-  for (int64_t t = 0; t < m; ++t) {
-    const int4 id = idx[t];
-    mark[id.x] = mark[id.y] = mark[id.z] = 1;
-    run_max = std::max<int64_t>(run_max, std::max(id.x, std::max(id.y, id.z)));
-    if (s->k == 4) {
-      mark[id.w] = 1;
-      run_max = std::max<int64_t>(run_max, id.w);
-    }
-    pmax[t] = run_max;  // monotone: targets [0, t] need source rows <= pmax[t]
-  }
-  int64_t tprev = 0, rprev = 0;
-  hp->t_end.resize(nchunks);
-  hp->runs.resize(nchunks);
-  for (int c = 0; c < nchunks; ++c) {
-    const int64_t rb = (c + 1 == nchunks) ? n : n * (c + 1) / nchunks;  // source rows [rprev, rb)
-    int64_t te = (c + 1 == nchunks) ? m : (int64_t)(std::lower_bound(pmax.begin(), pmax.end(), rb) - pmax.begin());
-    te = std::max(te, tprev);
-    hp->t_end[c] = te;
-    // referenced runs of [rprev, rb); unreferenced gaps shorter than 64 rows are copied through
-    int64_t i = rprev;
-    while (i < rb) {
-      while (i < rb && !mark[i]) ++i;
-      if (i >= rb) break;
-      int64_t j = i;
-      for (;;) {
-        while (j < rb && mark[j]) ++j;
-        int64_t g = j;
-        while (g < rb && !mark[g] && g - j < 64) ++g;
-        if (g < rb && mark[g]) j = g;  // short gap: merge
-        else break;
-      }
-      hp->runs[c].emplace_back(i, j);
-      hp->rows_copied += j - i;
-      i = j;
-    }
-    tprev = te;
-    rprev = rb;
-  }
-  hp->idx_host = std::move(idx);
-  hp->mark_host = std::move(mark);
-  SG_CUDA(cudaStreamCreateWithFlags(&hp->s_in, cudaStreamNonBlocking));
-  SG_CUDA(cudaStreamCreateWithFlags(&hp->s_cmp, cudaStreamNonBlocking));
-  SG_CUDA(cudaStreamCreateWithFlags(&hp->s_out, cudaStreamNonBlocking));
-  hp->ev_in.resize(nchunks);
-  hp->ev_cmp.resize(nchunks);
-  for (int c = 0; c < nchunks; ++c) {
-    SG_CUDA(cudaEventCreateWithFlags(&hp->ev_in[c], cudaEventDisableTiming));
-    SG_CUDA(cudaEventCreateWithFlags(&hp->ev_cmp[c], cudaEventDisableTiming));
-  }
-  s->host_plan = owned.release();
-  return hp;
-}
-
-}  // namespace
-
-void Stencil::destroy_host_plan() {
-  auto* hp = static_cast<HostPlan*>(host_plan);
-  if (!hp) return;
-  int cur = -1;
-  cudaGetDevice(&cur);
-  if (cur != device) cudaSetDevice(device);
-  for (auto e : hp->ev_in) cudaEventDestroy(e);
-  for (auto e : hp->ev_cmp) cudaEventDestroy(e);
-  if (hp->s_in) cudaStreamDestroy(hp->s_in);
-  if (hp->s_cmp) cudaStreamDestroy(hp->s_cmp);
-  if (hp->s_out) cudaStreamDestroy(hp->s_out);
-  if (cur != device && cur >= 0) cudaSetDevice(cur);
-  delete hp;
-  host_plan = nullptr;
-}
+}  // namespace detail
 
 void stencil_finalize(Stencil* s, const int32_t* d_idx3, const double* d_w3, cudaStream_t st) {
   s->idx.alloc(s->device, (size_t)std::max<int64_t>(s->m, 1) * sizeof(int4));
@@ -748,6 +543,7 @@ void stencil_finalize(Stencil* s, const int32_t* d_idx3, const double* d_w3, cud
 }  // namespace sg
 
 using namespace sg;
+using namespace sg::detail;
 
 extern "C" {
 
@@ -833,153 +629,6 @@ int32_t sg_remap_apply_list(uint64_t stencil, const uint64_t* src_fields, const 
     a.list = dev_targets;
     launch_apply(a, variant, as_stream(stream));
   }
-  SG_API_END
-}
-
-int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, const uint64_t* dst_fields,
-                              int32_t nfields, const uint64_t* host_src, const uint64_t* host_dst, int32_t nchunks,
-                              int32_t variant, int32_t flags, int64_t* out_rows_copied) {
-  SG_API_BEGIN
-  Stencil* s = get<Stencil>(stencil, ObjKind::Stencil);
-  FieldPairs p = check_pairs(s, src_fields, dst_fields, nfields);
-  SG_REQUIRE(host_src && host_dst, "null host arrays");
-  for (int f = 0; f < nfields; ++f) {
-    SG_REQUIRE(host_src[f] && host_dst[f], "null host array for field %d", f);
-    SG_REQUIRE(p.src[f]->pitch == p.levels && p.dst[f]->pitch == p.levels, "execute_host needs dense fields");
-  }
-  SG_REQUIRE(nchunks >= 1 && nchunks <= 1024, "nchunks must be in [1, 1024]");
-  DeviceScope ds(s->device);
-  const size_t row = (size_t)p.levels * 8;
-  if (flags & 2) {
-    // zero-copy: the apply kernel reads the referenced source rows straight out of pinned
-    // host memory over PCIe and streams the target rows back into pinned host memory — no
-    // staging, no DMA engine, only referenced rows cross the link (U/n = 77 % at cfg3)
-    std::vector<const double*> hs(nfields);
-    std::vector<double*> hd(nfields);
-    for (int f = 0; f < nfields; ++f) {
-      for (int io = 0; io < 2; ++io) {
-        const void* hp_ = reinterpret_cast<const void*>(io ? host_dst[f] : host_src[f]);
-        cudaPointerAttributes at{};
-        SG_CUDA(cudaPointerGetAttributes(&at, hp_));
-        SG_REQUIRE(at.type == cudaMemoryTypeHost && at.devicePointer,
-                   "zero-copy execute needs pinned, mapped host arrays (sg_host_alloc)");
-        if (io) hd[f] = static_cast<double*>(at.devicePointer);
-        else hs[f] = static_cast<const double*>(at.devicePointer);
-      }
-    }
-    cudaStream_t st = 0;
-    for (int f0 = 0; f0 < nfields; f0 += kMaxFields) {
-      ApplyArgs a = make_args(s, p, f0, 0, s->m);
-      for (int f = 0; f < a.nfields; ++f) {
-        a.src[f] = hs[f0 + f];
-        a.dst[f] = hd[f0 + f];
-        a.src_pitch[f] = a.dst_pitch[f] = p.levels;
-      }
-      launch_apply(a, variant == 2 ? 0 : variant, st);
-    }
-    SG_CUDA(cudaStreamSynchronize(st));
-    if (out_rows_copied) *out_rows_copied = s->distinct_sources;
-    return SG_OK;
-  }
-  HostPlan* hp = host_plan(s, nchunks);
-  const bool compact = (flags & 1) != 0;
-  if (compact) {
-    const int period = (flags >> 8) & 0xff;
-    if (!hp->compact_ready || hp->period != period) build_compact(s, hp, hp->idx_host, hp->mark_host, period);
-    // device compact sources and the pinned staging ring (sized for the largest chunk)
-    size_t maxc = 0;
-    for (int c = 0; c < nchunks; ++c)
-      if (!hp->direct[c]) maxc = std::max<size_t>(maxc, (size_t)(hp->cb[c + 1] - hp->cb[c]));
-    const size_t need = std::max<size_t>(maxc * row, 16);
-    if (hp->ring_bytes < need || hp->ring_fields < nfields) {
-      for (void* q : hp->ring)
-        if (q) cudaFreeHost(q);
-      hp->ring.assign((size_t)nfields * HostPlan::kRing, nullptr);
-      for (auto& q : hp->ring) SG_CUDA(cudaHostAlloc(&q, need, cudaHostAllocPortable));
-      hp->ring_bytes = need;
-      hp->ring_fields = nfields;
-    }
-    while ((int)hp->csrc.size() < nfields) hp->csrc.emplace_back(new DevBuf());
-    for (int f = 0; f < nfields; ++f)
-      if (hp->csrc[f]->bytes < std::max<size_t>(hp->ncompact * row, 16))
-        hp->csrc[f]->alloc(s->device, std::max<size_t>(hp->ncompact * row, 16));
-  }
-  int64_t tprev = 0, copied = 0;
-  for (int c = 0; c < nchunks; ++c) {
-    if (compact) {
-      if (hp->direct[c]) {  // whole row range straight from the user's array
-        const int64_t nrows = hp->rlo[c + 1] - hp->rlo[c];
-        for (int f = 0; f < nfields; ++f)
-          if (nrows)
-            SG_CUDA(cudaMemcpyAsync(hp->csrc[f]->as<char>() + hp->cb[c] * row,
-                                    reinterpret_cast<const char*>(host_src[f]) + hp->rlo[c] * row, (size_t)nrows * row,
-                                    cudaMemcpyHostToDevice, hp->s_in));
-        copied += nrows;
-        SG_CUDA(cudaEventRecord(hp->ev_in[c], hp->s_in));
-        goto issued;
-      }
-      {
-      int packed_before = 0;
-      for (int q = 0; q < c; ++q) packed_before += !hp->direct[q];
-      const int slot = packed_before % HostPlan::kRing;
-      // slot free: the last packed chunk that used it has been copied
-      for (int q = c - 1, seen = 0; q >= 0 && seen < HostPlan::kRing; --q)
-        if (!hp->direct[q] && ++seen == HostPlan::kRing) SG_CUDA(cudaEventSynchronize(hp->ev_in[q]));
-      const auto& runs = hp->cruns[c];
-      const int64_t base = hp->cb[c], nrows = hp->cb[c + 1] - hp->cb[c];
-      const int nr = (int)runs.size();
-      const int grain = std::max(1, nr / (host_pool().size() * 4));
-      for (int f = 0; f < nfields; ++f) {
-        char* stage = static_cast<char*>(hp->ring[(size_t)f * HostPlan::kRing + slot]);
-        const char* host = reinterpret_cast<const char*>(host_src[f]);
-        host_pool().parallel_for((nr + grain - 1) / grain, [&](int b) {
-          for (int k = b * grain; k < std::min(nr, (b + 1) * grain); ++k)
-            copy_rows_nt(stage + (runs[k].dst - base) * row, host + runs[k].src * row, (size_t)runs[k].len * row);
-          _mm_sfence();
-        });
-        if (nrows)
-          SG_CUDA(cudaMemcpyAsync(hp->csrc[f]->as<char>() + base * row, stage, (size_t)nrows * row,
-                                  cudaMemcpyHostToDevice, hp->s_in));
-      }
-      copied += nrows;
-      }
-    } else {
-      for (int f = 0; f < nfields; ++f) {
-        char* dev = p.src[f]->buf.as<char>();
-        const char* host = reinterpret_cast<const char*>(host_src[f]);
-        for (auto& r : hp->runs[c])
-          SG_CUDA(cudaMemcpyAsync(dev + r.first * row, host + r.first * row, (size_t)(r.second - r.first) * row,
-                                  cudaMemcpyHostToDevice, hp->s_in));
-      }
-    }
-    SG_CUDA(cudaEventRecord(hp->ev_in[c], hp->s_in));
-  issued:
-    SG_CUDA(cudaStreamWaitEvent(hp->s_cmp, hp->ev_in[c], 0));
-    const int64_t te = hp->t_end[c];
-    for (int f0 = 0; f0 < nfields; f0 += kMaxFields) {
-      ApplyArgs a = make_args(s, p, f0, tprev, te);
-      if (compact) {
-        a.idx = hp->cidx.as<int4>();
-        for (int f = 0; f < a.nfields; ++f) {
-          a.src[f] = hp->csrc[f0 + f]->as<double>();
-          a.src_pitch[f] = p.levels;
-        }
-      }
-      launch_apply(a, variant, hp->s_cmp);
-    }
-    SG_CUDA(cudaEventRecord(hp->ev_cmp[c], hp->s_cmp));
-    SG_CUDA(cudaStreamWaitEvent(hp->s_out, hp->ev_cmp[c], 0));
-    if (te > tprev)
-      for (int f = 0; f < nfields; ++f)
-        SG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(host_dst[f]) + tprev * row,
-                                p.dst[f]->buf.as<char>() + tprev * row, (size_t)(te - tprev) * row,
-                                cudaMemcpyDeviceToHost, hp->s_out));
-    tprev = te;
-  }
-  SG_CUDA(cudaStreamSynchronize(hp->s_out));
-  SG_CUDA(cudaStreamSynchronize(hp->s_cmp));
-  SG_CUDA(cudaStreamSynchronize(hp->s_in));
-  if (out_rows_copied) *out_rows_copied = compact ? copied : hp->rows_copied;
   SG_API_END
 }
 
