@@ -17,9 +17,7 @@
 //    works) into a STAGES-deep ring guarded by full/empty mbarriers; 8 consumer warps (one
 //    target each) compute from shared memory and stream the rows out.
 //  * thread per target for levels <= 8.
-// sg_remap_execute_host pipelines host->device copies of source-row chunks, the apply of the
-// targets whose stencils are complete, and device->host copies of their rows on three
-// streams, and copies only source rows the stencil references.
+// The host-buffer pipeline (sg_remap_execute_host) lives in execute_host.cu.
 #include <algorithm>
 #include <mutex>
 #include <vector>
