@@ -314,11 +314,13 @@ def run_single(args):
     for f in range(F):
         sg.apply_remap(w, fsrc[f], fdst[f])  # warm (staging buffers)
     clocks.active = True
-    t = time.perf_counter()
+    e2e_times = []
     for _ in range(e2e_steps):
+        t = time.perf_counter()
         for f in range(F):
             sg.apply_remap(w, fsrc[f], fdst[f])
-    e2e_s = (time.perf_counter() - t) / e2e_steps
+        e2e_times.append(time.perf_counter() - t)
+    e2e_s = statistics.median(e2e_times)
     clocks.active = False
     clocks.stop()
     e2e_ok = bool(np.array_equal(hdst[0].array[samp].view(np.uint64), exp.view(np.uint64)))
@@ -354,7 +356,8 @@ def run_single(args):
                      "traffic": ncu_traffic(args.config), "algorithmic_bytes_per_launch": B,
                      "kernel_ms": kern_ms, "peak_source": peak_src},
         "e2e": {"value": units / e2e_s / 1e9, "unit": "Gpts·lev/s", "h2d_bytes_per_step": n * L * 8 * F,
-                "d2h_bytes_per_step": m * L * 8 * F, "ms_per_step": e2e_s * 1e3,
+                "d2h_bytes_per_step": m * L * 8 * F, "ms_per_step": e2e_s * 1e3, "statistic": "median",
+                "ms_per_step_mean": 1e3 * sum(e2e_times) / len(e2e_times),
                 "api": "paper_1908_07038_b200.apply_remap(weights, host Field, host Field)",
                 "mode": args.e2e_mode, "chunks": args.e2e_chunks, "direct_period": args.e2e_period},
         "cpu_baseline": cpu,
