@@ -338,7 +338,8 @@ def apply_remap(weights: InterpolationWeights, source_field: Field, target_field
     """target[t] = sum_i w_i * source[node_i], every level (interp.py:206-228)."""
     _check_shapes(weights, source_field, target_field)
     dev = current_device()
-    on_device = (source_field.state in (MemoryState.SYNCED, MemoryState.DEVICE_DIRTY)
+    on_device = (source_field.kind.dtype == np.float64 and target_field.kind.dtype == np.float64
+                 and source_field.state in (MemoryState.SYNCED, MemoryState.DEVICE_DIRTY)
                  and target_field.state in (MemoryState.SYNCED, MemoryState.DEVICE_DIRTY)
                  and source_field.device is not None and target_field.device is not None
                  and source_field.device.device == target_field.device.device)

@@ -403,3 +403,23 @@ def test_grid_pairs_vs_scaled_oracle(gpu, src, tgt, halo, P):
         assert np.array_equal(w.nodes, c), (src, tgt, r)
         ow = O.barycentric_weights_batched(mesh.node_xyz, c, txyz[w.target_global])
         assert np.abs(w.weights - ow).max() <= W_TOL
+
+
+def test_apply_real32_fields_like_numpy(gpu):
+    """Non-real64 fields follow numpy's promotion (interp.py:219-224): f64 arithmetic on the
+    upcast source, the result cast into the target's kind."""
+    sg = gpu
+    S, T = sg.grid_from_name("O16"), sg.grid_from_name("F8")
+    dist = sg.blocks_partition(S, 1)
+    mesh = sg.generate_mesh(S, dist, 0, halo=0, include_pole=True)
+    fs = sg.NodeColumns(mesh, None)
+    td = sg.matching_partition(T, S, dist)
+    w = sg.build_remap(fs, T, td)
+    f = fs.create_field("s", 3, sg.Kind.REAL32)
+    f.host[:] = np.random.default_rng(2).normal(size=f.host.shape).astype(np.float32)
+    tf = sg.StructuredColumns(T, td, 0).create_field("t", 3, sg.Kind.REAL32)
+    f.allocate_device()
+    tf.allocate_device()
+    sg.apply_remap(w, f, tf)
+    exp = O.apply_remap(w.nodes, w.weights, f.host).astype(np.float32)
+    assert np.array_equal(tf.host, exp)
