@@ -353,7 +353,9 @@ def run_single(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(args.config), "algorithmic_bytes_per_launch": B,
                      "kernel_ms": kern_ms, "peak_source": peak_src},
-        "e2e": {"value": units / e2e_s / 1e9, "unit": "Gpts·lev/s", "h2d_bytes_per_step": n * L * 8 * F,
+        "e2e": {"value": units / e2e_s / 1e9, "unit": "Gpts·lev/s",
+                "h2d_bytes_per_step": int(w.__dict__.get("last_host_rows_moved", n)) * L * 8 * F,
+                "input_bytes_per_step": n * L * 8 * F,
                 "d2h_bytes_per_step": m * L * 8 * F, "ms_per_step": e2e_s * 1e3, "statistic": "median",
                 "ms_per_step_mean": 1e3 * sum(e2e_times) / len(e2e_times),
                 "api": "paper_1908_07038_b200.apply_remap(weights, host Field, host Field)",

@@ -357,7 +357,9 @@ def apply_remap(weights: InterpolationWeights, source_field: Field, target_field
     th = target_field.host
     direct = th.dtype == np.float64 and th.flags["C_CONTIGUOUS"] and th.flags["WRITEABLE"]
     out = th if direct else np.empty(target_field.shape, np.float64)
-    execute_host(weights, [host_src], [out], [src], [dst], nchunks=HOST_EXECUTE_CHUNKS, mode=HOST_EXECUTE_MODE)
+    moved = execute_host(weights, [host_src], [out], [src], [dst], nchunks=HOST_EXECUTE_CHUNKS,
+                         mode=HOST_EXECUTE_MODE)
+    weights.__dict__["last_host_rows_moved"] = moved  # source rows that crossed PCIe (bench accounting)
     if not direct:
         th[:] = out
     if target_field.state is MemoryState.SYNCED:
