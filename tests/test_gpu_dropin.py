@@ -249,3 +249,23 @@ def test_custom_grid_remap_vs_oracle(gpu):
     e, c = O.locate_kdtree(mesh.node_xyz, conn.offsets, conn.indices, T.xyz())
     assert np.array_equal(e < 0, w.fallback)
     assert np.array_equal(w.nodes[~w.fallback], c[~w.fallback])
+
+
+def test_cli_remap_report(gpu, tmp_path):
+    """test_cli.py:132-152: the remap subcommand's report and dump format."""
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    out = tmp_path / "f.txt"
+    r = subprocess.run([sys.executable, "-m", "paper_1908_07038_b200", "remap", "--source", "O8", "--target", "F4",
+                        "--parts", "2", "--field", "constant:1", "--out", str(out), "--report"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    report = dict(line.split(": ") for line in r.stdout.strip().splitlines() if ": " in line)
+    assert float(report["max_error"]) < 1e-13
+    assert int(report["messages_during_interpolation"]) == 0
+    text = out.read_text()
+    assert text.startswith("# field:")
+    assert len([ln for ln in text.splitlines() if not ln.startswith("#")]) == 128
