@@ -75,6 +75,7 @@ int32_t sg_event_elapsed_ms(uint64_t start, uint64_t end, float* out_ms);
  * graphs of a captured steady-state step (the multi-GPU exchange + apply). */
 int32_t sg_stream_create(int32_t device, uint64_t* out_handle, uint64_t* out_stream);
 int32_t sg_stream_wait_event(uint64_t stream, uint64_t event);
+int32_t sg_enable_peer_access(int32_t device, int32_t peer);
 int32_t sg_graph_begin(int32_t device, uint64_t stream);
 int32_t sg_graph_end(int32_t device, uint64_t stream, uint64_t* out_graph);
 int32_t sg_graph_launch(uint64_t graph, uint64_t stream);

@@ -47,6 +47,7 @@ _SIGS = {
     "sg_event_elapsed_ms": [u64, u64, vp],
     "sg_stream_create": [i32, vp, vp],
     "sg_stream_wait_event": [u64, u64],
+    "sg_enable_peer_access": [i32, i32],
     "sg_graph_begin": [i32, u64],
     "sg_graph_end": [i32, u64, vp],
     "sg_graph_launch": [u64, u64],

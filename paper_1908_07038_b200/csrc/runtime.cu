@@ -55,6 +55,24 @@ int32_t sg_stream_wait_event(uint64_t stream, uint64_t event_handle) {
   SG_API_END
 }
 
+// Let kernels on `device` dereference memory of `peer` (NVLink P2P within one process:
+// run_ranks with one thread per GPU).  Idempotent.
+int32_t sg_enable_peer_access(int32_t device, int32_t peer) {
+  SG_API_BEGIN
+  if (device == peer) return SG_OK;
+  DeviceScope ds(device);
+  int can = 0;
+  SG_CUDA(cudaDeviceCanAccessPeer(&can, device, peer));
+  if (!can) throw_error(SG_DOMAIN_ERROR, "CudaError: device %d cannot access device %d", device, peer);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    e = cudaSuccess;
+  }
+  SG_CUDA(e);
+  SG_API_END
+}
+
 int32_t sg_graph_begin(int32_t device, uint64_t stream) {
   SG_API_BEGIN
   DeviceScope ds(device);

@@ -172,6 +172,11 @@ class RankContext:
         got = cache.get(dev_array.handle)
         if got is None:
             got = cache[dev_array.handle] = self.share((dev_array.ptr, dev_array.pitch, dev_array.device))
+            from . import _native as N
+
+            for _, _, dev in got:  # NVLink P2P between this rank's GPU and every peer's
+                if dev != dev_array.device:
+                    N.call("sg_enable_peer_access", dev_array.device, dev)
         return got
 
     def device_exchange(self, plan, dev_array, stream: int = 0) -> None:
