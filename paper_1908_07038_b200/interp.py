@@ -165,13 +165,14 @@ class InterpolationWeights:
             self.stencil, self.stencil_device = N.Handle(h.value), device
         return self.stencil.handle
 
-    def _staging(self, device: int, src_shape, dst_shape):
-        key = (device, tuple(src_shape), tuple(dst_shape))
+    def _staging(self, device: int, src_shape, dst_shape, nfields: int = 1):
+        """Device staging pairs for host-resident fields, cached per (device, shapes, F)."""
+        key = (device, tuple(src_shape), tuple(dst_shape), nfields)
         cache = self.__dict__.setdefault("_staging_cache", {})
         if key not in cache:
             cache.clear()
-            cache[key] = (DeviceArray(src_shape[0], src_shape[1], np.float64, device),
-                          DeviceArray(dst_shape[0], dst_shape[1], np.float64, device))
+            cache[key] = ([DeviceArray(src_shape[0], src_shape[1], np.float64, device) for _ in range(nfields)],
+                          [DeviceArray(dst_shape[0], dst_shape[1], np.float64, device) for _ in range(nfields)])
         return cache[key]
 
     def distinct_sources(self) -> int:
@@ -336,34 +337,61 @@ def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], 
 
 def apply_remap(weights: InterpolationWeights, source_field: Field, target_field: Field) -> None:
     """target[t] = sum_i w_i * source[node_i], every level (interp.py:206-228)."""
-    _check_shapes(weights, source_field, target_field)
+    apply_remap_fields(weights, [source_field], [target_field])
+
+
+def apply_remap_fields(weights: InterpolationWeights, source_fields: Sequence[Field],
+                       target_fields: Sequence[Field]) -> None:
+    """apply_remap for F field pairs sharing one stencil in one pass: device-resident pairs
+    in one kernel launch, host-resident pairs in one pipelined host-buffer execute."""
+    if len(source_fields) != len(target_fields) or not source_fields:
+        raise ValueError("need matching, non-empty source/target field lists")
+    for s, t in zip(source_fields, target_fields):
+        _check_shapes(weights, s, t)
     dev = current_device()
-    on_device = (source_field.kind.dtype == np.float64 and target_field.kind.dtype == np.float64
-                 and source_field.state in (MemoryState.SYNCED, MemoryState.DEVICE_DIRTY)
-                 and target_field.state in (MemoryState.SYNCED, MemoryState.DEVICE_DIRTY)
-                 and source_field.device is not None and target_field.device is not None
-                 and source_field.device.device == target_field.device.device)
-    if on_device:
-        apply_remap_device(weights, [source_field.device], [target_field.device])
-        N.call("sg_stream_synchronize", source_field.device.device, 0)
-        target_field.mark_device_written()
+
+    def resident(s, t):
+        return (s.kind.dtype == np.float64 and t.kind.dtype == np.float64
+                and s.state in (MemoryState.SYNCED, MemoryState.DEVICE_DIRTY)
+                and t.state in (MemoryState.SYNCED, MemoryState.DEVICE_DIRTY)
+                and s.device is not None and t.device is not None and s.device.device == t.device.device)
+
+    pairs = list(zip(source_fields, target_fields))
+    on_dev = [p for p in pairs if resident(*p)]
+    on_host = [p for p in pairs if not resident(*p)]
+    if on_dev:
+        apply_remap_device(weights, [s.device for s, _ in on_dev], [t.device for _, t in on_dev])
+        N.call("sg_stream_synchronize", on_dev[0][0].device.device, 0)
+        for _, t in on_dev:
+            t.mark_device_written()
+    if not on_host:
         return
     # host-resident fields: reference semantics (reads source.host, writes target.host);
     # the arithmetic runs on the device through staging buffers cached on the weights
-    src, dst = weights._staging(dev, source_field.shape, target_field.shape)
-    host_src = source_field.host
-    if host_src.dtype != np.float64 or not host_src.flags["C_CONTIGUOUS"]:
-        host_src = np.ascontiguousarray(host_src, dtype=np.float64)
-    th = target_field.host
-    direct = th.dtype == np.float64 and th.flags["C_CONTIGUOUS"] and th.flags["WRITEABLE"]
-    out = th if direct else np.empty(target_field.shape, np.float64)
-    moved = execute_host(weights, [host_src], [out], [src], [dst], nchunks=HOST_EXECUTE_CHUNKS,
-                         mode=HOST_EXECUTE_MODE)
-    weights.__dict__["last_host_rows_moved"] = moved  # source rows that crossed PCIe (bench accounting)
-    if not direct:
-        th[:] = out
-    if target_field.state is MemoryState.SYNCED:
-        target_field.state = MemoryState.HOST_DIRTY
+    shapes = {(s.shape, t.shape) for s, t in on_host}
+    groups = [on_host] if len(shapes) == 1 else [[p] for p in on_host]
+    for group in groups:
+        srcs, dsts = weights._staging(dev, group[0][0].shape, group[0][1].shape, len(group))
+        host_src, outs, copy_back = [], [], []
+        for s, t in group:
+            h = s.host
+            if h.dtype != np.float64 or not h.flags["C_CONTIGUOUS"]:
+                h = np.ascontiguousarray(h, dtype=np.float64)
+            host_src.append(h)
+            th = t.host
+            direct = th.dtype == np.float64 and th.flags["C_CONTIGUOUS"] and th.flags["WRITEABLE"]
+            out = th if direct else np.empty(t.shape, np.float64)
+            outs.append(out)
+            copy_back.append(None if direct else (th, out))
+        moved = execute_host(weights, host_src, outs, srcs, dsts, nchunks=HOST_EXECUTE_CHUNKS,
+                             mode=HOST_EXECUTE_MODE)
+        weights.__dict__["last_host_rows_moved"] = moved  # source rows per field that crossed PCIe
+        for cb in copy_back:
+            if cb is not None:
+                cb[0][:] = cb[1]
+        for _, t in group:
+            if t.state is MemoryState.SYNCED:
+                t.state = MemoryState.HOST_DIRTY
 
 
 def export_weights(weights: InterpolationWeights, stream) -> None:

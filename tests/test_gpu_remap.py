@@ -449,3 +449,32 @@ def test_halo1_not_located_pattern_vs_scaled_oracle(gpu):
                 sg.build_remap(fs, T, td)
             assert ei.value.target_global_index == int(w.target_global[np.argmax(w.fallback)])
     assert any_fail or True
+
+
+def test_apply_remap_fields_host_and_device(gpu):
+    """apply_remap_fields: F host-resident pairs in one pipelined execute, device-resident
+    pairs in one launch — each bitwise equal to the per-field apply."""
+    sg = gpu
+    S, T = sg.grid_from_name("O48"), sg.grid_from_name("O24")
+    dist = sg.blocks_partition(S, 1)
+    mesh = sg.generate_mesh(S, dist, 0, halo=0, include_pole=True)
+    fs = sg.NodeColumns(mesh, None)
+    td = sg.matching_partition(T, S, dist)
+    w = sg.build_remap(fs, T, td)
+    tfs = sg.StructuredColumns(T, td, 0)
+    rng = np.random.default_rng(12)
+    srcs = [fs.create_field(f"s{k}", 9) for k in range(3)]
+    for s in srcs:
+        s.host[:] = rng.normal(size=s.host.shape)
+    dsts = [tfs.create_field(f"t{k}", 9) for k in range(3)]
+    sg.apply_remap_fields(w, srcs, dsts)
+    for s, t in zip(srcs, dsts):
+        assert np.array_equal(t.host.view(np.uint64), O.apply_remap(w.nodes, w.weights, s.host).view(np.uint64))
+    dsts2 = [tfs.create_field(f"u{k}", 9).allocate_device() for k in range(3)]
+    for s in srcs:
+        s.allocate_device()
+    sg.apply_remap_fields(w, srcs, dsts2)
+    for t, ref in zip(dsts2, dsts):
+        assert t.state is sg.MemoryState.DEVICE_DIRTY
+        t.update_host()
+        assert np.array_equal(t.host, ref.host)
