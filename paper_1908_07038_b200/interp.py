@@ -323,8 +323,10 @@ def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], 
     rows = C.c_int64(0)
     if mode == "auto":
         # measured on cfg3 (profiles/r01_e2e_modes.md): compact 124 ms/step (non-temporal
-        # host packing of the referenced rows), dma 134 ms, zero-copy 153 ms
-        mode = "compact"
+        # host packing of the referenced rows), dma 134 ms, zero-copy 153 ms.  Packing only
+        # pays when a good share of the rows is skipped (cfg5 bilinear reads every row).
+        u = weights.distinct_sources() if weights.stencil is not None else weights.source_nnodes
+        mode = "compact" if u < 0.85 * max(weights.source_nnodes, 1) else "dma"
     flags = {"dma": 0, "compact": 1, "zerocopy": 2}[mode]
     if direct_period < 0:
         direct_period = HOST_EXECUTE_DIRECT_PERIOD
