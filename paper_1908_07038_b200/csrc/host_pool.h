@@ -26,8 +26,10 @@ class HostPool {
   }
   int size() const { return (int)threads_.size() + 1; }
   // Runs fn(i) for i in [0, n) on the pool and the calling thread; returns when all are done.
+  // Callers from several threads (in-process ranks) are serialised: one job at a time.
   void parallel_for(int n, const std::function<void(int)>& fn) {
     if (n <= 0) return;
+    std::lock_guard<std::mutex> job_lock(call_mu_);
     {
       std::lock_guard<std::mutex> lk(mu_);
       fn_ = &fn;
@@ -69,6 +71,7 @@ class HostPool {
     }
   }
   std::vector<std::thread> threads_;
+  std::mutex call_mu_;  // one parallel_for at a time
   std::mutex mu_;
   std::condition_variable cv_, done_cv_;
   const std::function<void(int)>* fn_ = nullptr;

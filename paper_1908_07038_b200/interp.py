@@ -23,6 +23,7 @@ and applies the reference's tie rule explicitly (see csrc/locate.cu).
 from __future__ import annotations
 
 import ctypes as C
+import time
 from dataclasses import dataclass, field as dc_field
 from typing import List, Optional, Sequence, Tuple
 
@@ -288,6 +289,21 @@ def apply_remap_fused(weights: InterpolationWeights, plan, source: DeviceArray, 
            t0, t1, N.ptr(ptrs), N.ptr(pitch), stream)
 
 
+def _auto_mode(weights: InterpolationWeights) -> str:
+    """Host-execute path chooser.  Packing (compact) only pays when the stencil skips a good
+    share of the source rows (cfg5 bilinear reads every row -> dma); whether it beats plain
+    DMA depends on the host's memory bandwidth (profiles/r01_e2e_modes.md: 124 vs 134 ms on
+    one box, 142 vs 135 on another), so the first calls time both and the faster one is kept."""
+    n = max(weights.source_nnodes, 1)
+    if weights.distinct_sources() >= 0.85 * n:
+        return "dma"
+    seen = weights.__dict__.setdefault("_auto_s", {})
+    for m in ("compact", "dma"):
+        if len(seen.get(m, [])) < 2:  # the first call of a mode also builds its plan
+            return m
+    return min(("compact", "dma"), key=lambda m: min(seen[m]))
+
+
 def _is_pinned(a: np.ndarray) -> bool:
     """True when ``a`` lives in a library pinned allocation (device.PinnedArray)."""
     from .device import PinnedArray
@@ -306,7 +322,8 @@ def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], 
     should be pinned (``device.PinnedArray``) for full PCIe rate.  mode: "dma" (chunked
     copies of the referenced row runs), "compact" (only referenced rows, packed on the host by
     the library's thread pool), "zerocopy" (the kernel reads/writes the pinned host arrays
-    directly over PCIe), "auto" (= compact, the fastest measured).
+    directly over PCIe), "auto" (times compact and dma on the first calls, keeps the
+    faster; dma when the stencil reads >= 85 % of the source rows).
     Returns source rows moved."""
     dev = dev_src[0].device
     sh = weights.device_stencil(dev)
@@ -321,19 +338,19 @@ def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], 
     s = np.array([a.handle for a in dev_src], np.uint64)
     t = np.array([a.handle for a in dev_dst], np.uint64)
     rows = C.c_int64(0)
-    if mode == "auto":
-        # measured on cfg3 (profiles/r01_e2e_modes.md): compact 124 ms/step (non-temporal
-        # host packing of the referenced rows), dma 134 ms, zero-copy 153 ms.  Packing only
-        # pays when a good share of the rows is skipped (cfg5 bilinear reads every row).
-        u = weights.distinct_sources() if weights.stencil is not None else weights.source_nnodes
-        mode = "compact" if u < 0.85 * max(weights.source_nnodes, 1) else "dma"
+    tuned = mode == "auto"
+    if tuned:
+        mode = _auto_mode(weights)
     flags = {"dma": 0, "compact": 1, "zerocopy": 2}[mode]
     if direct_period < 0:
         direct_period = HOST_EXECUTE_DIRECT_PERIOD
     if mode == "compact" and direct_period > 0:
         flags |= (min(int(direct_period), 255) << 8)  # every n-th chunk: one direct DMA
+    t0 = time.perf_counter()
     N.call("sg_remap_execute_host", sh, N.ptr(s), N.ptr(t), len(s), N.ptr(hs), N.ptr(hd), nchunks, variant,
            flags, N.ref(rows))
+    if tuned:
+        weights.__dict__.setdefault("_auto_s", {}).setdefault(mode, []).append(time.perf_counter() - t0)
     return rows.value
 
 
