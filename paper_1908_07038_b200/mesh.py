@@ -13,7 +13,8 @@ from __future__ import annotations
 import ctypes as C
 import enum
 from dataclasses import dataclass
-from typing import List, Tuple
+import math
+from typing import List, Optional, Tuple
 
 import numpy as np
 
@@ -21,7 +22,7 @@ from . import _native as N
 from .errors import InvalidDistribution
 from .geometry import lonlat_to_xyz_array
 from .grid import Grid
-from .partition import Distribution
+from .partition import Distribution, blocks_partition
 
 TRIANGLE = 3
 QUAD = 4
@@ -163,3 +164,69 @@ def split_quad(row: np.ndarray) -> List[np.ndarray]:
 def element_triangles(mesh: Mesh, e: int) -> List[np.ndarray]:
     row = mesh.element_connectivity.row(e)
     return [np.asarray(row, dtype=np.int64)] if len(row) == 3 else split_quad(row)
+
+
+# -- serial topology and mesh diagnostics (mesh.py:134-140, 174-226, 344-420 of the reference) --
+
+@dataclass
+class SerialTopology:
+    nnodes: int                    # grid.npts (+2 with poles)
+    elem_nodes: List[np.ndarray]   # global node ids per element, serial order
+    node_lonlat: np.ndarray
+    north_pole: Optional[int]
+    south_pole: Optional[int]
+
+
+def serial_topology(grid: Grid, include_pole: bool) -> SerialTopology:
+    """The global element sweep (mesh.py:174-226): the one-partition, halo-0 mesh of the
+    native generator, whose local numbering is the global one."""
+    m = generate_mesh(grid, blocks_partition(grid, 1), 0, halo=0, include_pole=include_pole)
+    conn = m.element_connectivity
+    gidx = m.node_global[conn.indices]
+    elem_nodes = [gidx[conn.offsets[e]:conn.offsets[e + 1]] for e in range(len(conn))]
+    order = np.argsort(m.elem_serial_id, kind="stable")
+    npts = grid.npts
+    return SerialTopology(
+        nnodes=npts + (2 if include_pole else 0), elem_nodes=[elem_nodes[e] for e in order],
+        node_lonlat=_lonlat_with_poles(grid, include_pole),
+        north_pole=npts if include_pole else None, south_pole=npts + 1 if include_pole else None)
+
+
+def _edges(mesh: Mesh) -> np.ndarray:
+    """Unique undirected element sides as sorted (i, j) pairs."""
+    off, idx = mesh.element_connectivity.offsets, mesh.element_connectivity.indices
+    k = np.diff(off)
+    pos = np.arange(len(idx), dtype=np.int64)
+    first = np.repeat(off[:-1], k)
+    nxt = np.where(pos + 1 < np.repeat(off[1:], k), pos + 1, first)
+    a, b = idx, idx[nxt]
+    pairs = np.stack([np.minimum(a, b), np.maximum(a, b)], axis=1)
+    return np.unique(pairs, axis=0) if len(pairs) else pairs
+
+
+def mesh_stats(mesh: Mesh) -> dict:
+    """V, E (unique sides), F, Euler characteristic and owned counts (mesh.py:355-375); an
+    element is owned by the partition owning its lowest-partition node."""
+    off, idx = mesh.element_connectivity.offsets, mesh.element_connectivity.indices
+    v, f = mesh.nb_nodes, mesh.nb_elements
+    e = len(_edges(mesh))
+    owned = int((np.minimum.reduceat(mesh.node_part[idx], off[:-1]) == mesh.partition_id).sum()) if f else 0
+    return {"V": v, "E": e, "F": f, "chi": v - e + f, "owned_nodes": mesh.nb_owned_nodes, "owned_elements": owned}
+
+
+def total_area(mesh: Mesh) -> float:
+    """Sum of spherical triangle areas over the split elements, L'Huilier's theorem
+    (mesh.py:378-420), vectorised over all triangles."""
+    tris = [t for e in range(mesh.nb_elements) for t in element_triangles(mesh, e)]
+    if not tris:
+        return 0.0
+    t = np.asarray(tris, dtype=np.int64)
+    a, b, c = (mesh.node_xyz[t[:, i]] for i in range(3))
+
+    def angle(u, w):
+        return np.arctan2(np.linalg.norm(np.cross(u, w), axis=1), np.einsum("ij,ij->i", u, w))
+
+    sa, sb, sc = angle(b, c), angle(c, a), angle(a, b)
+    s = 0.5 * (sa + sb + sc)
+    x = np.tan(0.5 * s) * np.tan(0.5 * (s - sa)) * np.tan(0.5 * (s - sb)) * np.tan(0.5 * (s - sc))
+    return float(np.sum(4.0 * np.arctan(np.sqrt(np.maximum(x, 0.0)))))
