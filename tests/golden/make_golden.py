@@ -218,7 +218,49 @@ def checksums():
     save("checksum", **out)
 
 
+def rotated():
+    """Rotated lon-lat grids (grid.py:121-140, geometry.py:97-151): lon/lat and xyz of two
+    rotated grids, and the serial O32 -> rotated O16 remap (stencils + apply); mesh_stats /
+    total_area of a few serial meshes (mesh.py:355-420)."""
+    from spheregrid.geometry import RotationSpec
+    from spheregrid.grid import GridKind, GridSpec, build_grid
+    from spheregrid.mesh import mesh_stats, total_area
+    out = {}
+    for tag, kind, n, rot in [("F8", GridKind.FULL_GAUSSIAN, 8, (10.0, 45.0)),
+                              ("O16", GridKind.OCTAHEDRAL_GAUSSIAN, 16, (-40.0, 30.0))]:
+        g = build_grid(GridSpec(kind, n, projection=RotationSpec(*rot)))
+        out[f"{tag}_rot"] = np.array(rot)
+        out[f"{tag}_lonlats"] = g.lonlats()
+        out[f"{tag}_xyz"] = g.xyz()
+    S = R.grid_from_name("O32")
+    T = build_grid(GridSpec(GridKind.OCTAHEDRAL_GAUSSIAN, 16, projection=RotationSpec(-40.0, 30.0)))
+    dist = R.blocks_partition(S, 1)
+    mesh = R.generate_mesh(S, dist, 0, halo=2, include_pole=True)
+    fs = R.NodeColumns(mesh, None)
+    tdist = R.matching_partition(T, S, dist)
+    w = R.build_remap(fs, T, tdist)
+    f = fs.create_field("src", levels=3)
+    f.host[:] = np.random.default_rng(2026).normal(size=f.host.shape)
+    tf = R.StructuredColumns(T, tdist, 0).create_field("dst", levels=3)
+    R.apply_remap(w, f, tf)
+    for k, v in stencil_arrays(w).items():
+        out["remap_" + k] = v
+    out["remap_out"] = tf.host
+    out["remap_part_of"] = tdist.part_of
+    stats = []
+    for name, pole, P, part, halo in [("F1", False, 1, 0, 0), ("F1", True, 1, 0, 0), ("O8", True, 1, 0, 0),
+                                      ("F8", False, 4, 1, 1), ("O16", True, 3, 2, 2)]:
+        g = R.grid_from_name(name)
+        m = R.generate_mesh(g, R.blocks_partition(g, P), part, halo=halo, include_pole=pole)
+        st = mesh_stats(m)
+        stats.append([st[k] for k in ("V", "E", "F", "chi", "owned_nodes", "owned_elements")])
+        out[f"area_{name}_{int(pole)}_{P}_{part}_{halo}"] = np.array(total_area(m))
+    out["mesh_stats"] = np.array(stats, dtype=np.int64)
+    save("rotated", **out)
+
+
 JOBS = {
+    "rotated": rotated,
     "checksum": checksums,
     "latitudes": latitudes,
     "cfg1": lambda: serial_remap("O32", "O16", 10, "cfg1_O32_O16"),

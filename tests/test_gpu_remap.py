@@ -478,3 +478,29 @@ def test_apply_remap_fields_host_and_device(gpu):
         assert t.state is sg.MemoryState.DEVICE_DIRTY
         t.update_host()
         assert np.array_equal(t.host, ref.host)
+
+
+def test_rotated_target_grid_bitexact(gpu, golden):
+    """O32 -> O16 in a rotated frame (RotationSpec(-40, 30), grid.py:121-140): device stencils
+    bit-exact to the reference's, weights within W_TOL, apply bitwise vs the numpy expression."""
+    sg = gpu
+    from paper_1908_07038_b200.grid import GridKind, GridSpec, build_grid
+    z = golden("rotated")
+    S = sg.grid_from_name("O32")
+    T = build_grid(GridSpec(GridKind.OCTAHEDRAL_GAUSSIAN, 16, projection=sg.RotationSpec(*z["O16_rot"])))
+    dist = sg.blocks_partition(S, 1)
+    mesh = sg.generate_mesh(S, dist, 0, halo=2, include_pole=True)
+    fs = sg.NodeColumns(mesh, None)
+    td = sg.matching_partition(T, S, dist)
+    assert np.array_equal(td.part_of, z["remap_part_of"])
+    w = sg.build_remap(fs, T, td)
+    assert np.array_equal(w.target_global, z["remap_target_global"])
+    assert np.array_equal(w.nodes, z["remap_nodes"].astype(np.int64))
+    assert np.abs(w.weights - z["remap_weights"]).max() <= W_TOL
+    f = fs.create_field("s", levels=3)
+    f.host[:] = np.random.default_rng(2026).normal(size=f.host.shape)
+    tf = sg.StructuredColumns(T, td, 0).create_field("d", levels=3)
+    sg.apply_remap(w, f, tf)
+    exp = O.apply_remap(w.nodes, w.weights, f.host)
+    assert np.array_equal(exp.view(np.uint64), tf.host.view(np.uint64))
+    assert np.abs(tf.host - z["remap_out"]).max() / np.abs(z["remap_out"]).max() <= REL_TOL

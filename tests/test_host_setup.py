@@ -122,3 +122,63 @@ def test_grid_point_and_geometry_helpers():
     with pytest.raises(sg.NotOnUnitSphere):
         sg.PointXYZ(1.0, 1.0, 0.0)
     assert g.describe()["npts"] == g.npts
+
+
+def _rotated_grid(tag, z):
+    from paper_1908_07038_b200.grid import GridKind, GridSpec, build_grid
+    kind = GridKind.FULL_GAUSSIAN if tag.startswith("F") else GridKind.OCTAHEDRAL_GAUSSIAN
+    return build_grid(GridSpec(kind, int(tag[1:]), projection=sg.RotationSpec(*z[f"{tag}_rot"])))
+
+
+@pytest.mark.parametrize("tag", ["F8", "O16"])
+def test_rotated_grid_coordinates_equal_reference(golden, tag):
+    """grid.py:121-140: rotated lon/lat and xyz bit-identical to the reference's."""
+    z = golden("rotated")
+    g = _rotated_grid(tag, z)
+    assert np.array_equal(g.lonlats().view(np.uint64), z[f"{tag}_lonlats"].view(np.uint64))
+    assert np.array_equal(g.xyz().view(np.uint64), z[f"{tag}_xyz"].view(np.uint64))
+    # scalar path (Grid.point -> unrotate) agrees with the vectorised one to rounding
+    for gi in (0, 5, g.npts // 2, g.npts - 1):
+        p = g.point(gi)
+        lon, lat = z[f"{tag}_lonlats"][gi]
+        assert abs(p.lat - lat) < 1e-9 and min(abs(p.lon - lon), 360 - abs(p.lon - lon)) < 1e-9
+
+
+def test_rotation_round_trip_and_distance():
+    r = sg.RotationSpec(10.0, 45.0)
+    p = sg.PointLonLat(33.0, -12.5)
+    q = sg.unrotate(sg.rotate(p, r), r)
+    assert abs(q.lon - p.lon) < 1e-12 and abs(q.lat - p.lat) < 1e-12
+    pole = sg.rotate(sg.PointLonLat(10.0, 45.0), r)
+    assert abs(pole.lat - 90.0) < 1e-9
+    assert sg.rotate(p, sg.RotationSpec()) is p
+    a, b = sg.PointLonLat(0.0, 0.0), sg.PointLonLat(90.0, 0.0)
+    assert abs(sg.great_circle_distance(a, b) - np.pi / 2) < 1e-15
+    # distances are invariant under the rotation
+    g0, g1 = sg.PointLonLat(12.0, 40.0), sg.PointLonLat(-70.0, -3.0)
+    d0 = sg.great_circle_distance(g0, g1)
+    assert abs(sg.great_circle_distance(sg.rotate(g0, r), sg.rotate(g1, r)) - d0) < 1e-12
+
+
+def test_mesh_stats_and_area_equal_reference(golden):
+    """mesh.py:355-420: V/E/F/chi/owned counts exact; L'Huilier area within 1e-12 relative."""
+    z = golden("rotated")
+    cases = [("F1", False, 1, 0, 0), ("F1", True, 1, 0, 0), ("O8", True, 1, 0, 0), ("F8", False, 4, 1, 1),
+             ("O16", True, 3, 2, 2)]
+    for row, (name, pole, P, part, halo) in zip(z["mesh_stats"], cases):
+        g = sg.grid_from_name(name)
+        m = sg.generate_mesh(g, sg.blocks_partition(g, P), part, halo=halo, include_pole=pole)
+        st = sg.mesh_stats(m)
+        assert [st[k] for k in ("V", "E", "F", "chi", "owned_nodes", "owned_elements")] == row.tolist()
+        ref = float(z[f"area_{name}_{int(pole)}_{P}_{part}_{halo}"])
+        assert abs(sg.total_area(m) - ref) <= 1e-12 * ref
+
+
+def test_serial_topology_is_global_sweep():
+    g = sg.grid_from_name("O2")
+    topo = sg.serial_topology(g, include_pole=True)
+    m = sg.generate_mesh(g, sg.blocks_partition(g, 1), 0, halo=0, include_pole=True)
+    assert topo.nnodes == g.npts + 2 and topo.north_pole == g.npts and topo.south_pole == g.npts + 1
+    assert len(topo.elem_nodes) == m.nb_elements
+    assert sum(len(e) for e in topo.elem_nodes) == len(m.element_connectivity.indices)
+    assert topo.node_lonlat.shape == (g.npts + 2, 2)

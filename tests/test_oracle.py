@@ -147,3 +147,20 @@ def test_oracle_checksum_equals_reference(golden):
     for name in ("O32", "F8", "O16"):
         vals = z[f"{name}_values"]
         assert O.checksum_partial(np.arange(len(vals)), vals) == int(z[f"{name}_p1"][0])
+
+
+def test_oracle_rotated_target_equals_reference(golden):
+    """O32 -> rotated O16 (RotationSpec(-40, 30)): the oracle's stencils/weights/apply equal
+    the reference's on targets whose coordinates come from the rotated grid."""
+    from paper_1908_07038_b200.grid import GridKind, GridSpec, build_grid
+    z = golden("rotated")
+    S = sg.grid_from_name("O32")
+    T = build_grid(GridSpec(GridKind.OCTAHEDRAL_GAUSSIAN, 16, projection=sg.RotationSpec(*z["O16_rot"])))
+    mesh = sg.generate_mesh(S, sg.blocks_partition(S, 1), 0, halo=2, include_pole=True)
+    conn = mesh.element_connectivity
+    r = O.build_remap(mesh.node_xyz, conn.offsets, conn.indices, T.xyz()[z["remap_target_global"]])
+    assert np.array_equal(r["nodes"], z["remap_nodes"])
+    assert np.array_equal(r["weights"].view(np.uint64), z["remap_weights"].view(np.uint64))
+    src = np.random.default_rng(2026).normal(size=(mesh.nb_nodes, 3))
+    out = O.apply_remap(z["remap_nodes"].astype(np.int64), z["remap_weights"], src)
+    assert np.array_equal(out.view(np.uint64), z["remap_out"].view(np.uint64))
