@@ -305,7 +305,7 @@ def run_single(args):
     fsrc = [sg.Field(name=f"src{f}", shape=(n, L), kind=sg.Kind.REAL64, host=hsrc[f].array) for f in range(F)]
     fdst = [sg.Field(name=f"dst{f}", shape=(m, L), kind=sg.Kind.REAL64, host=hdst[f].array) for f in range(F)]
     e2e_steps = max(3, min(args.steps, 10))
-    for _ in range(4):  # warm: staging buffers, pipeline plans, the auto mode's two trials per path
+    for _ in range(6):  # warm: staging buffers, pipeline plans, the auto mode's two trials per path
         sg.apply_remap_fields(w, fsrc, fdst)
     clocks.active = True
     e2e_times = []
@@ -523,7 +523,7 @@ def main():
     ap.add_argument("--e2e-chunks", type=int, default=0, help="host-execute pipeline depth (0 = auto)")
     ap.add_argument("--e2e-period", type=int, default=-1,
                     help="compact e2e: copy every n-th chunk directly instead of packing (-1 = library default)")
-    ap.add_argument("--e2e-mode", default="auto", choices=["auto", "dma", "compact", "zerocopy"],
+    ap.add_argument("--e2e-mode", default="auto", choices=["auto", "dma", "compact", "gather", "zerocopy"],
                     help="host-buffer execute path for e2e (auto = zero-copy for pinned arrays)")
     ap.add_argument("--partitioner", default="blocks", choices=["blocks", "equal_regions"],
                     help="N>1 source decomposition: the reference's blocks bands, or equal regions")

@@ -1,9 +1,11 @@
 // The host-buffer execute (sg_remap_execute_host): apply_remap with HOST source and target
 // arrays (interp.py:206-228), pipelined over source-row chunks on three streams — h2d of a
-// chunk, apply of the targets whose stencils are complete, d2h of their rows — in three modes:
+// chunk, apply of the targets whose stencils are complete, d2h of their rows — in four modes:
 // dma (copy the referenced row runs), compact (pack only referenced rows on the host with
 // non-temporal stores into a pinned ring; apply from a compact device copy with a renumbered
-// stencil) and zero-copy (the kernel reads/writes pinned host memory directly).
+// stencil), gather (the same compact device copy, filled by a GPU kernel that reads only the
+// referenced rows straight out of the pinned, mapped user array: no host CPU work, no DMA of
+// unreferenced rows) and zero-copy (the apply kernel reads/writes pinned host memory directly).
 #include <emmintrin.h>
 
 #include <algorithm>
@@ -41,6 +43,7 @@ struct HostPlan {
   std::vector<char> direct;                       // chunk c copied straight from the user array
   std::vector<int64_t> rlo;                       // chunk c: first source row
   DevBuf cidx;                                    // int4[m]: stencil in compact row numbering
+  DevBuf gsrc;                                    // int32[ncompact]: source row of each compact row
   std::vector<std::unique_ptr<DevBuf>> csrc;      // per field: U compact rows on the device
   static constexpr int kRing = 3;
   std::vector<void*> ring;                        // per (field, slot): pinned staging
@@ -65,6 +68,48 @@ inline void copy_rows_nt(char* dst, const char* src, size_t bytes) {
     _mm_stream_si128(reinterpret_cast<__m128i*>(dst + off), _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + off)));
   for (; off + 8 <= bytes; off += 8)
     _mm_stream_si64(reinterpret_cast<long long*>(dst + off), *reinterpret_cast<const long long*>(src + off));
+}
+
+// gather mode: compact rows [u0, u1) <- host rows gsrc[u], one warp per row, every load of
+// the row in flight before the stores (PCIe read latency; tools/probes/pcie_gather_probe.cu:
+// 48.6 GB/s against 55.6 for a plain DMA, on 77 % of the bytes)
+template <int IT>
+__global__ void __launch_bounds__(256) gather_rows(const double* __restrict__ host, const int32_t* __restrict__ gsrc,
+                                                   double* __restrict__ out, int64_t u0, int64_t u1, int levels) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = u0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); u < u1; u += stride) {
+    const double* src = host + (int64_t)__ldg(gsrc + u) * levels;
+    double* dst = out + u * levels;
+    if (IT == 0) {
+      for (int l = lane; l < levels; l += 32) dst[l] = src[l];
+      continue;
+    }
+    double v[IT > 0 ? IT : 1];
+#pragma unroll
+    for (int i = 0; i < IT; ++i)
+      if (lane + 32 * i < levels) v[i] = src[lane + 32 * i];
+#pragma unroll
+    for (int i = 0; i < IT; ++i)
+      if (lane + 32 * i < levels) dst[lane + 32 * i] = v[i];
+  }
+}
+
+void launch_gather(const double* host, const int32_t* gsrc, double* out, int64_t u0, int64_t u1, int levels,
+                   cudaStream_t st) {
+  if (u1 <= u0) return;
+  // 4 of the 8 resident 256-thread blocks per SM: leaves room for the apply of the previous
+  // chunk, which runs concurrently on its own stream
+  const unsigned grid = (unsigned)std::min<int64_t>((u1 - u0 + 7) / 8, 148 * 4);
+  switch ((levels + 31) / 32) {
+    case 1: gather_rows<1><<<grid, 256, 0, st>>>(host, gsrc, out, u0, u1, levels); break;
+    case 2: gather_rows<2><<<grid, 256, 0, st>>>(host, gsrc, out, u0, u1, levels); break;
+    case 3: gather_rows<3><<<grid, 256, 0, st>>>(host, gsrc, out, u0, u1, levels); break;
+    case 4: gather_rows<4><<<grid, 256, 0, st>>>(host, gsrc, out, u0, u1, levels); break;
+    case 5: gather_rows<5><<<grid, 256, 0, st>>>(host, gsrc, out, u0, u1, levels); break;
+    default: gather_rows<0><<<grid, 256, 0, st>>>(host, gsrc, out, u0, u1, levels); break;
+  }
+  SG_CUDA_LAUNCH();
 }
 
 HostPool& host_pool() {
@@ -117,6 +162,15 @@ void build_compact(Stencil* s, HostPlan* hp, const std::vector<int4>& idx, const
   }
   hp->cidx.alloc(s->device, std::max<size_t>(ci.size(), 1) * sizeof(int4));
   if (m) SG_CUDA(cudaMemcpy(hp->cidx.ptr, ci.data(), ci.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  std::vector<int32_t> gs((size_t)u);
+  for (int c = 0; c < hp->nchunks; ++c) {
+    if (hp->direct[c])
+      for (int64_t i = hp->rlo[c]; i < hp->rlo[c + 1]; ++i) gs[(size_t)(hp->cb[c] + i - hp->rlo[c])] = (int32_t)i;
+    for (const auto& r : hp->cruns[c])
+      for (int64_t q = 0; q < r.len; ++q) gs[(size_t)(r.dst + q)] = (int32_t)(r.src + q);
+  }
+  hp->gsrc.alloc(s->device, std::max<size_t>(gs.size(), 1) * sizeof(int32_t));
+  if (u) SG_CUDA(cudaMemcpy(hp->gsrc.ptr, gs.data(), gs.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   hp->period = period;
   hp->compact_ready = true;
 }
@@ -230,6 +284,14 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
   SG_REQUIRE(nchunks >= 1 && nchunks <= 1024, "nchunks must be in [1, 1024]");
   DeviceScope ds(s->device);
   const size_t row = (size_t)p.levels * 8;
+  // device addresses of pinned, mapped host arrays (zero-copy and gather modes)
+  auto mapped = [](uint64_t host, const char* mode) -> void* {
+    cudaPointerAttributes at{};
+    SG_CUDA(cudaPointerGetAttributes(&at, reinterpret_cast<const void*>(host)));
+    SG_REQUIRE(at.type == cudaMemoryTypeHost && at.devicePointer,
+               "%s execute needs pinned, mapped host arrays (sg_host_alloc / sg_host_register)", mode);
+    return at.devicePointer;
+  };
   if (flags & 2) {
     // zero-copy: the apply kernel reads the referenced source rows straight out of pinned
     // host memory over PCIe and streams the target rows back into pinned host memory — no
@@ -237,15 +299,8 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
     std::vector<const double*> hs(nfields);
     std::vector<double*> hd(nfields);
     for (int f = 0; f < nfields; ++f) {
-      for (int io = 0; io < 2; ++io) {
-        const void* hp_ = reinterpret_cast<const void*>(io ? host_dst[f] : host_src[f]);
-        cudaPointerAttributes at{};
-        SG_CUDA(cudaPointerGetAttributes(&at, hp_));
-        SG_REQUIRE(at.type == cudaMemoryTypeHost && at.devicePointer,
-                   "zero-copy execute needs pinned, mapped host arrays (sg_host_alloc)");
-        if (io) hd[f] = static_cast<double*>(at.devicePointer);
-        else hs[f] = static_cast<const double*>(at.devicePointer);
-      }
+      hs[f] = static_cast<const double*>(mapped(host_src[f], "zero-copy"));
+      hd[f] = static_cast<double*>(mapped(host_dst[f], "zero-copy"));
     }
     cudaStream_t st = 0;
     for (int f0 = 0; f0 < nfields; f0 += kMaxFields) {
@@ -262,16 +317,20 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
     return SG_OK;
   }
   HostPlan* hp = host_plan(s, nchunks);
-  const bool compact = (flags & 1) != 0;
+  const bool gather = (flags & 4) != 0;
+  const bool compact = (flags & 1) != 0 || gather;
+  std::vector<const double*> gsrc_host(gather ? nfields : 0);
+  for (int f = 0; f < (int)gsrc_host.size(); ++f)
+    gsrc_host[f] = static_cast<const double*>(mapped(host_src[f], "gather"));
   if (compact) {
-    const int period = (flags >> 8) & 0xff;
+    const int period = gather ? 0 : (flags >> 8) & 0xff;
     if (!hp->compact_ready || hp->period != period) build_compact(s, hp, hp->idx_host, hp->mark_host, period);
     // device compact sources and the pinned staging ring (sized for the largest chunk)
     size_t maxc = 0;
     for (int c = 0; c < nchunks; ++c)
       if (!hp->direct[c]) maxc = std::max<size_t>(maxc, (size_t)(hp->cb[c + 1] - hp->cb[c]));
     const size_t need = std::max<size_t>(maxc * row, 16);
-    if (hp->ring_bytes < need || hp->ring_fields < nfields) {
+    if (!gather && (hp->ring_bytes < need || hp->ring_fields < nfields)) {
       for (void* q : hp->ring)
         if (q) cudaFreeHost(q);
       hp->ring.assign((size_t)nfields * HostPlan::kRing, nullptr);
@@ -295,6 +354,14 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
                                     reinterpret_cast<const char*>(host_src[f]) + hp->rlo[c] * row, (size_t)nrows * row,
                                     cudaMemcpyHostToDevice, hp->s_in));
         copied += nrows;
+        SG_CUDA(cudaEventRecord(hp->ev_in[c], hp->s_in));
+        goto issued;
+      }
+      if (gather) {  // GPU gather of the chunk's referenced rows from the mapped user array
+        for (int f = 0; f < nfields; ++f)
+          launch_gather(gsrc_host[f], hp->gsrc.as<int32_t>(), hp->csrc[f]->as<double>(), hp->cb[c], hp->cb[c + 1],
+                        p.levels, hp->s_in);
+        copied += hp->cb[c + 1] - hp->cb[c];
         SG_CUDA(cudaEventRecord(hp->ev_in[c], hp->s_in));
         goto issued;
       }

@@ -289,19 +289,21 @@ def apply_remap_fused(weights: InterpolationWeights, plan, source: DeviceArray, 
            t0, t1, N.ptr(ptrs), N.ptr(pitch), stream)
 
 
-def _auto_mode(weights: InterpolationWeights) -> str:
-    """Host-execute path chooser.  Packing (compact) only pays when the stencil skips a good
-    share of the source rows (cfg5 bilinear reads every row -> dma); whether it beats plain
-    DMA depends on the host's memory bandwidth (profiles/r01_e2e_modes.md: 124 vs 134 ms on
-    one box, 142 vs 135 on another), so the first calls time both and the faster one is kept."""
+def _auto_mode(weights: InterpolationWeights, mapped: bool) -> str:
+    """Host-execute path chooser.  Moving only the referenced rows (gather / compact) pays
+    when the stencil skips a good share of the source rows (cfg5 bilinear reads every row ->
+    dma); which way wins depends on the host (profiles/r01_e2e_modes.md: compact 124 vs dma
+    134 ms on one box, 142 vs 135 on another), so the first calls time each candidate and the
+    fastest is kept.  gather needs pinned, mapped source arrays (device.PinnedArray)."""
     n = max(weights.source_nnodes, 1)
     if weights.distinct_sources() >= 0.85 * n:
         return "dma"
+    modes = ("gather", "compact", "dma") if mapped else ("compact", "dma")
     seen = weights.__dict__.setdefault("_auto_s", {})
-    for m in ("compact", "dma"):
+    for m in modes:
         if len(seen.get(m, [])) < 2:  # the first call of a mode also builds its plan
             return m
-    return min(("compact", "dma"), key=lambda m: min(seen[m]))
+    return min(modes, key=lambda m: min(seen[m]))
 
 
 def _is_pinned(a: np.ndarray) -> bool:
@@ -321,9 +323,11 @@ def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], 
     source rows, apply, d2h of the target rows, overlapped on three streams.  Host arrays
     should be pinned (``device.PinnedArray``) for full PCIe rate.  mode: "dma" (chunked
     copies of the referenced row runs), "compact" (only referenced rows, packed on the host by
-    the library's thread pool), "zerocopy" (the kernel reads/writes the pinned host arrays
-    directly over PCIe), "auto" (times compact and dma on the first calls, keeps the
-    faster; dma when the stencil reads >= 85 % of the source rows).
+    the library's thread pool), "gather" (only referenced rows, read by a GPU kernel straight
+    from the pinned, mapped source arrays into a compact device copy), "zerocopy" (the apply
+    kernel reads/writes the pinned host arrays directly over PCIe), "auto" (times the
+    candidates on the first calls and keeps the fastest; dma when the stencil reads >= 85 %
+    of the source rows).
     Returns source rows moved."""
     dev = dev_src[0].device
     sh = weights.device_stencil(dev)
@@ -340,8 +344,8 @@ def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], 
     rows = C.c_int64(0)
     tuned = mode == "auto"
     if tuned:
-        mode = _auto_mode(weights)
-    flags = {"dma": 0, "compact": 1, "zerocopy": 2}[mode]
+        mode = _auto_mode(weights, all(_is_pinned(a) for a in host_src))
+    flags = {"dma": 0, "compact": 1, "zerocopy": 2, "gather": 4}[mode]
     if direct_period < 0:
         direct_period = HOST_EXECUTE_DIRECT_PERIOD
     if mode == "compact" and direct_period > 0:

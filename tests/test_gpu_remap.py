@@ -218,7 +218,7 @@ def test_execute_host_pipeline_bitwise(gpu):
     hs = PinnedArray((mesh.nb_nodes, L))
     hs.array[:] = np.random.default_rng(3).normal(size=hs.array.shape)
     exp = O.apply_remap(w.nodes, w.weights, hs.array)
-    for mode, period in (("dma", 0), ("compact", 0), ("compact", 2), ("compact", 5), ("zerocopy", 0)):
+    for mode, period in (("dma", 0), ("compact", 0), ("compact", 2), ("compact", 5), ("gather", 0), ("zerocopy", 0)):
         for nchunks in (1, 3, 17):
             hd = PinnedArray((len(w), L))
             ds, dd = DeviceArray(mesh.nb_nodes, L, np.float64), DeviceArray(len(w), L, np.float64)
@@ -234,8 +234,36 @@ def test_execute_host_pipeline_bitwise(gpu):
     out = np.empty((len(w), L))
     execute_host(w, [hp], [out], [ds], [dd])
     assert np.array_equal(out.view(np.uint64), exp.view(np.uint64))
-    with pytest.raises(Exception):
-        execute_host(w, [hp], [out], [ds], [dd], mode="zerocopy")
+    for mode in ("zerocopy", "gather"):
+        with pytest.raises(Exception, match="pinned, mapped"):
+            execute_host(w, [hp], [out], [ds], [dd], mode=mode)
+
+
+@pytest.mark.parametrize("levels", [1, 10, 33, 200])
+def test_execute_host_gather_levels_and_fields(gpu, levels):
+    """gather mode (GPU reads only the referenced rows from mapped pinned memory) for every
+    kernel shape (1..5 warps of levels, and the generic loop) and 3 fields per call."""
+    sg = gpu
+    from paper_1908_07038_b200.device import DeviceArray, PinnedArray
+    from paper_1908_07038_b200.interp import execute_host
+
+    S, T = sg.grid_from_name("O64"), sg.grid_from_name("O32")
+    dist = sg.blocks_partition(S, 1)
+    mesh = sg.generate_mesh(S, dist, 0, halo=2, include_pole=True)
+    w = sg.build_remap(sg.NodeColumns(mesh, None), T, sg.matching_partition(T, S, dist))
+    rng = np.random.default_rng(levels)
+    hs = [PinnedArray((mesh.nb_nodes, levels)) for _ in range(3)]
+    hd = [PinnedArray((len(w), levels)) for _ in range(3)]
+    for h in hs:
+        h.array[:] = rng.normal(size=h.array.shape)
+    ds = [DeviceArray(mesh.nb_nodes, levels, np.float64) for _ in range(3)]
+    dd = [DeviceArray(len(w), levels, np.float64) for _ in range(3)]
+    for nchunks in (1, 5):
+        rows = execute_host(w, [h.array for h in hs], [h.array for h in hd], ds, dd, nchunks=nchunks, mode="gather")
+        assert rows == w.distinct_sources()
+        for a, b in zip(hs, hd):
+            exp = O.apply_remap(w.nodes, w.weights, a.array)
+            assert np.array_equal(b.array.view(np.uint64), exp.view(np.uint64)), (levels, nchunks)
 
 
 def test_apply_range(gpu):
