@@ -230,7 +230,7 @@ def test_execute_host_pipeline_bitwise(gpu):
             else:
                 assert rows == w.distinct_sources()
     # pageable host arrays cannot be read zero-copy: "auto" falls back to dma
-    hp = np.ascontiguousarray(hs.array)
+    hp = hs.array.copy()  # pageable (ascontiguousarray would return the pinned array itself)
     out = np.empty((len(w), L))
     execute_host(w, [hp], [out], [ds], [dd])
     assert np.array_equal(out.view(np.uint64), exp.view(np.uint64))
