@@ -523,7 +523,7 @@ def main():
     ap.add_argument("--e2e-chunks", type=int, default=0, help="host-execute pipeline depth (0 = auto)")
     ap.add_argument("--e2e-period", type=int, default=-1,
                     help="compact e2e: copy every n-th chunk directly instead of packing (-1 = library default)")
-    ap.add_argument("--e2e-mode", default="auto", choices=["auto", "dma", "compact", "gather", "zerocopy"],
+    ap.add_argument("--e2e-mode", default="auto", choices=["auto", "dma", "compact", "gather", "gather_warp", "zerocopy"],
                     help="host-buffer execute path for e2e (auto = zero-copy for pinned arrays)")
     ap.add_argument("--partitioner", default="blocks", choices=["blocks", "equal_regions"],
                     help="N>1 source decomposition: the reference's blocks bands, or equal regions")

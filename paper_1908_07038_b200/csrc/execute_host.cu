@@ -16,6 +16,7 @@
 
 #include "apply_internal.cuh"
 #include "host_pool.h"
+#include "tma.cuh"
 
 namespace sg {
 namespace {
@@ -44,6 +45,11 @@ struct HostPlan {
   std::vector<int64_t> rlo;                       // chunk c: first source row
   DevBuf cidx;                                    // int4[m]: stencil in compact row numbering
   DevBuf gsrc;                                    // int32[ncompact]: source row of each compact row
+  // gather mode, TMA path: referenced runs cut into pieces of <= piece_rows rows
+  int piece_levels = -1, piece_rows = 0;
+  std::vector<int64_t> pb;                        // chunk c: pieces [pb[c], pb[c+1])
+  DevBuf pieces;                                  // int2 (first source row, rows) per piece
+  DevBuf pdst;                                    // int64 first compact row per piece
   std::vector<std::unique_ptr<DevBuf>> csrc;      // per field: U compact rows on the device
   static constexpr int kRing = 3;
   std::vector<void*> ring;                        // per (field, slot): pinned staging
@@ -70,9 +76,73 @@ inline void copy_rows_nt(char* dst, const char* src, size_t bytes) {
     _mm_stream_si64(reinterpret_cast<long long*>(dst + off), *reinterpret_cast<const long long*>(src + off));
 }
 
-// gather mode: compact rows [u0, u1) <- host rows gsrc[u], one warp per row, every load of
-// the row in flight before the stores (PCIe read latency; tools/probes/pcie_gather_probe.cu:
-// 48.6 GB/s against 55.6 for a plain DMA, on 77 % of the bytes)
+// gather mode, TMA path (the default): one producer thread per CTA bulk-copies the 16-B
+// aligned superset of a piece (a run of consecutive referenced source rows, <= piece_rows
+// rows) out of the mapped host array into a shared-memory ring stage; 4 consumer warps copy
+// the stage into the piece's compact rows.  The copy engine of the TMA unit issues larger PCIe
+// reads than warp loads: tools/probes/pcie_gather_probe.cu measured 50.5 GB/s vs 48.6 for the
+// warp-per-row gather below (DMA of every row: 55.6 GB/s, but on 1/0.77 more bytes).
+constexpr int kGatherStages = 4;
+constexpr int kGatherPieceDoubles = 12 * 137;  // ~13 KB per stage
+
+__global__ void __launch_bounds__(160) gather_tma(const double* __restrict__ host, int64_t host_rows,
+                                                  const int2* __restrict__ pieces, const int64_t* __restrict__ pdst,
+                                                  double* __restrict__ out, int64_t p0, int64_t p1, int levels,
+                                                  int slot) {
+  using namespace tma;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + kGatherStages;
+  double* ring = reinterpret_cast<double*>(smem_raw + 128);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(host);
+  const uintptr_t hi = reinterpret_cast<uintptr_t>(host + host_rows * levels);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kGatherStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 4) {  // producer
+    if (lane != 0) return;
+    int it = 0;
+    for (int64_t p = p0 + blockIdx.x; p < p1; p += gridDim.x, ++it) {
+      const int st = it % kGatherStages;
+      if (it >= kGatherStages) mbar_wait(&empty[st], ((it / kGatherStages) - 1) & 1);
+      const int2 pc = __ldg(pieces + p);
+      const uintptr_t a = reinterpret_cast<uintptr_t>(host + (int64_t)pc.x * levels);
+      const uintptr_t s0 = a & ~uintptr_t(15), s1 = (a + (uintptr_t)pc.y * levels * 8 + 15) & ~uintptr_t(15);
+      if (s0 < lo || s1 > hi) {  // superset leaves the array: consumers load this piece directly
+        mbar_arrive(&full[st]);
+      } else {
+        mbar_expect_tx(&full[st], (uint32_t)(s1 - s0));
+        bulk_g2s(ring + (size_t)st * slot, reinterpret_cast<const void*>(s0), (uint32_t)(s1 - s0), &full[st]);
+      }
+    }
+    return;
+  }
+  int it = 0;
+  for (int64_t p = p0 + blockIdx.x; p < p1; p += gridDim.x, ++it) {
+    const int st = it % kGatherStages;
+    const int2 pc = __ldg(pieces + p);
+    double* d = out + __ldg(pdst + p) * levels;
+    const double* src = host + (int64_t)pc.x * levels;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    const uintptr_t s0 = a & ~uintptr_t(15), s1 = (a + (uintptr_t)pc.y * levels * 8 + 15) & ~uintptr_t(15);
+    const bool direct = s0 < lo || s1 > hi;
+    const double* b = direct ? src : ring + (size_t)st * slot + ((a - s0) >> 3);
+    const int n = pc.y * levels;
+    mbar_wait(&full[st], (it / kGatherStages) & 1);
+    for (int i = threadIdx.x; i < n; i += 128) d[i] = b[i];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+}
+
+// warp-per-row gather (levels too large for a ring stage): compact rows [u0, u1) <- host
+// rows gsrc[u], every load of the row in flight before the stores (PCIe read latency)
 template <int IT>
 __global__ void __launch_bounds__(256) gather_rows(const double* __restrict__ host, const int32_t* __restrict__ gsrc,
                                                    double* __restrict__ out, int64_t u0, int64_t u1, int levels) {
@@ -95,11 +165,11 @@ __global__ void __launch_bounds__(256) gather_rows(const double* __restrict__ ho
   }
 }
 
-void launch_gather(const double* host, const int32_t* gsrc, double* out, int64_t u0, int64_t u1, int levels,
-                   cudaStream_t st) {
+// 4 of the 8 resident 256-thread blocks per SM: leaves room for the apply of the previous
+// chunk, which runs concurrently on its own stream
+void launch_gather_rows(const double* host, const int32_t* gsrc, double* out, int64_t u0, int64_t u1, int levels,
+                        cudaStream_t st) {
   if (u1 <= u0) return;
-  // 4 of the 8 resident 256-thread blocks per SM: leaves room for the apply of the previous
-  // chunk, which runs concurrently on its own stream
   const unsigned grid = (unsigned)std::min<int64_t>((u1 - u0 + 7) / 8, 148 * 4);
   switch ((levels + 31) / 32) {
     case 1: gather_rows<1><<<grid, 256, 0, st>>>(host, gsrc, out, u0, u1, levels); break;
@@ -110,6 +180,46 @@ void launch_gather(const double* host, const int32_t* gsrc, double* out, int64_t
     default: gather_rows<0><<<grid, 256, 0, st>>>(host, gsrc, out, u0, u1, levels); break;
   }
   SG_CUDA_LAUNCH();
+}
+
+int gather_slot(int levels, int piece_rows) { return (piece_rows * levels + 2 + 1) & ~1; }  // doubles, 16-B multiple
+
+void launch_gather_tma(const double* host, int64_t host_rows, const int2* pieces, const int64_t* pdst, double* out,
+                       int64_t p0, int64_t p1, int levels, int piece_rows, cudaStream_t st) {
+  if (p1 <= p0) return;
+  const int slot = gather_slot(levels, piece_rows);
+  const size_t smem = 128 + (size_t)kGatherStages * slot * 8;
+  SG_CUDA(cudaFuncSetAttribute(gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // two CTAs per SM (4 stages x ~13 KB each): the apply of the previous chunk co-resides
+  const unsigned grid = (unsigned)std::min<int64_t>(p1 - p0, 148 * 2);
+  gather_tma<<<grid, 160, smem, st>>>(host, host_rows, pieces, pdst, out, p0, p1, levels, slot);
+  SG_CUDA_LAUNCH();
+}
+
+// Pieces of the referenced runs for `levels` (rebuilt when the level count changes).
+void build_pieces(int device, HostPlan* hp, int levels) {
+  const int prows = std::max(1, kGatherPieceDoubles / levels);
+  if (hp->piece_levels == levels && hp->piece_rows == prows) return;
+  std::vector<int2> pcs;
+  std::vector<int64_t> dst;
+  hp->pb.assign(hp->nchunks + 1, 0);
+  for (int c = 0; c < hp->nchunks; ++c) {
+    hp->pb[c] = (int64_t)pcs.size();
+    for (const auto& r : hp->cruns[c])
+      for (int64_t q = 0; q < r.len; q += prows) {
+        pcs.push_back(make_int2((int)(r.src + q), (int)std::min<int64_t>(prows, r.len - q)));
+        dst.push_back(r.dst + q);
+      }
+  }
+  hp->pb[hp->nchunks] = (int64_t)pcs.size();
+  hp->pieces.alloc(device, std::max<size_t>(pcs.size(), 1) * sizeof(int2));
+  hp->pdst.alloc(device, std::max<size_t>(dst.size(), 1) * sizeof(int64_t));
+  if (!pcs.empty()) {
+    SG_CUDA(cudaMemcpy(hp->pieces.ptr, pcs.data(), pcs.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    SG_CUDA(cudaMemcpy(hp->pdst.ptr, dst.data(), dst.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  }
+  hp->piece_levels = levels;
+  hp->piece_rows = prows;
 }
 
 HostPool& host_pool() {
@@ -319,6 +429,9 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
   HostPlan* hp = host_plan(s, nchunks);
   const bool gather = (flags & 4) != 0;
   const bool compact = (flags & 1) != 0 || gather;
+  // TMA ring stage must hold at least one 16-B aligned row superset; flags bit 3 forces the
+  // warp-per-row gather (kept for comparison)
+  const bool tma_gather = gather && !(flags & 8) && (size_t)p.levels * 8 + 16 <= (size_t)kGatherPieceDoubles * 8;
   std::vector<const double*> gsrc_host(gather ? nfields : 0);
   for (int f = 0; f < (int)gsrc_host.size(); ++f)
     gsrc_host[f] = static_cast<const double*>(mapped(host_src[f], "gather"));
@@ -339,6 +452,7 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
       hp->ring_fields = nfields;
     }
     while ((int)hp->csrc.size() < nfields) hp->csrc.emplace_back(new DevBuf());
+    if (tma_gather) build_pieces(s->device, hp, p.levels);
     for (int f = 0; f < nfields; ++f)
       if (hp->csrc[f]->bytes < std::max<size_t>(hp->ncompact * row, 16))
         hp->csrc[f]->alloc(s->device, std::max<size_t>(hp->ncompact * row, 16));
@@ -358,9 +472,14 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
         goto issued;
       }
       if (gather) {  // GPU gather of the chunk's referenced rows from the mapped user array
-        for (int f = 0; f < nfields; ++f)
-          launch_gather(gsrc_host[f], hp->gsrc.as<int32_t>(), hp->csrc[f]->as<double>(), hp->cb[c], hp->cb[c + 1],
-                        p.levels, hp->s_in);
+        for (int f = 0; f < nfields; ++f) {
+          if (tma_gather)
+            launch_gather_tma(gsrc_host[f], s->source_nnodes, hp->pieces.as<int2>(), hp->pdst.as<int64_t>(),
+                              hp->csrc[f]->as<double>(), hp->pb[c], hp->pb[c + 1], p.levels, hp->piece_rows, hp->s_in);
+          else
+            launch_gather_rows(gsrc_host[f], hp->gsrc.as<int32_t>(), hp->csrc[f]->as<double>(), hp->cb[c],
+                               hp->cb[c + 1], p.levels, hp->s_in);
+        }
         copied += hp->cb[c + 1] - hp->cb[c];
         SG_CUDA(cudaEventRecord(hp->ev_in[c], hp->s_in));
         goto issued;

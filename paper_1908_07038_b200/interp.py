@@ -345,7 +345,7 @@ def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], 
     tuned = mode == "auto"
     if tuned:
         mode = _auto_mode(weights, all(_is_pinned(a) for a in host_src))
-    flags = {"dma": 0, "compact": 1, "zerocopy": 2, "gather": 4}[mode]
+    flags = {"dma": 0, "compact": 1, "zerocopy": 2, "gather": 4, "gather_warp": 4 | 8}[mode]
     if direct_period < 0:
         direct_period = HOST_EXECUTE_DIRECT_PERIOD
     if mode == "compact" and direct_period > 0:

@@ -239,7 +239,7 @@ def test_execute_host_pipeline_bitwise(gpu):
             execute_host(w, [hp], [out], [ds], [dd], mode=mode)
 
 
-@pytest.mark.parametrize("levels", [1, 10, 33, 200])
+@pytest.mark.parametrize("levels", [1, 10, 33, 137, 200, 2000])
 def test_execute_host_gather_levels_and_fields(gpu, levels):
     """gather mode (GPU reads only the referenced rows from mapped pinned memory) for every
     kernel shape (1..5 warps of levels, and the generic loop) and 3 fields per call."""
@@ -258,12 +258,14 @@ def test_execute_host_gather_levels_and_fields(gpu, levels):
         h.array[:] = rng.normal(size=h.array.shape)
     ds = [DeviceArray(mesh.nb_nodes, levels, np.float64) for _ in range(3)]
     dd = [DeviceArray(len(w), levels, np.float64) for _ in range(3)]
-    for nchunks in (1, 5):
-        rows = execute_host(w, [h.array for h in hs], [h.array for h in hd], ds, dd, nchunks=nchunks, mode="gather")
+    for nchunks, mode in ((1, "gather"), (5, "gather"), (5, "gather_warp")):
+        for h in hd:
+            h.array[:] = np.nan
+        rows = execute_host(w, [h.array for h in hs], [h.array for h in hd], ds, dd, nchunks=nchunks, mode=mode)
         assert rows == w.distinct_sources()
         for a, b in zip(hs, hd):
             exp = O.apply_remap(w.nodes, w.weights, a.array)
-            assert np.array_equal(b.array.view(np.uint64), exp.view(np.uint64)), (levels, nchunks)
+            assert np.array_equal(b.array.view(np.uint64), exp.view(np.uint64)), (levels, nchunks, mode)
 
 
 def test_apply_range(gpu):
