@@ -1,0 +1,56 @@
+#!/usr/bin/env python
+"""e2e sweep on cfg3 in one process: host-execute modes x gather CTAs/SM x pipeline chunks,
+through the public apply_remap_fields on pinned host fields (bench.py's e2e leg).  One JSON
+line per setting; every result checked bitwise against the first (dma) run."""
+import json
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+
+
+def main():
+    import paper_1908_07038_b200 as sg
+    import paper_1908_07038_b200.interp as sgi
+    from paper_1908_07038_b200.device import PinnedArray
+
+    sg.set_device(0)
+    S, T, mesh, fs, tdist, w = bench.setup_remap(sg, "O1280", "O640", 1, 0, None)
+    m, n, L = len(w), mesh.nb_nodes, 137
+    hsrc, hdst = PinnedArray((n, L)), PinnedArray((m, L))
+    bench.fill_smooth(hsrc.array, mesh.node_xyz, 0)
+    fsrc = sg.Field(name="src", shape=(n, L), kind=sg.Kind.REAL64, host=hsrc.array)
+    fdst = sg.Field(name="dst", shape=(m, L), kind=sg.Kind.REAL64, host=hdst.array)
+    ref = None
+    settings = [("dma", 2, 64)]
+    for mode in sys.argv[1].split(",") if len(sys.argv) > 1 else ["gather"]:
+        for ctas in (2, 4, 8):
+            for ch in (32, 64, 128):
+                settings.append((mode, ctas, ch))
+    for mode, ctas, ch in settings:
+        os.environ["SG_GATHER_CTAS"] = str(ctas)  # honoured by the build that ran the sweep
+        sgi.HOST_EXECUTE_MODE, sgi.HOST_EXECUTE_CHUNKS = mode, ch
+        hdst.array[:] = 0
+        for _ in range(3):
+            sg.apply_remap_fields(w, [fsrc], [fdst])
+        ts = []
+        for _ in range(8):
+            t = time.perf_counter()
+            sg.apply_remap_fields(w, [fsrc], [fdst])
+            ts.append(time.perf_counter() - t)
+        if ref is None:
+            ref = hdst.array.copy()
+        ok = bool(np.array_equal(ref.view(np.uint64), hdst.array.view(np.uint64)))
+        ms = statistics.median(ts) * 1e3
+        print(json.dumps({"mode": mode, "ctas_per_sm": ctas, "chunks": ch, "ms": round(ms, 2),
+                          "gpts_lev_s": round(m * L / (ms * 1e-3) / 1e9, 4), "bitwise": ok}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
