@@ -1,6 +1,8 @@
 """Apply-kernel variant sweep on cfg3 (O1280 -> O640, 137 levels): per variant the mean
 kernel time over 20 launches, two interleaved rounds.  Variants: 0 default (8-B loads),
-2 TMA bulk 16-target tiles (1 CTA/SM), 6 TMA bulk 8-target tiles (2 CTAs/SM)."""
+2/6/7 TMA bulk tiles, 4/5 L2 prefetch hints (apply.cu launch_apply).  Experimental
+variants measured once and removed are listed in profiles/r01_apply_variant_sweep2.jsonl.
+Usage: apply_sweep.py [comma-separated variants]"""
 import json, os, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -23,7 +25,7 @@ samp = np.random.default_rng(1).choice(len(w), 3000, replace=False)
 exp = O.apply_remap(w.nodes[samp], w.weights[samp], host)
 res = {}
 for rnd in range(2):
-    for v in (0, 2, 6, 7):
+    for v in [int(x) for x in (sys.argv[1].split(',') if len(sys.argv) > 1 else ['0', '2', '6', '7'])]:
         for _ in range(3):
             sg.apply_remap_device(w, [src], [dst], variant=v)
         e0, e1 = Event(), Event()
