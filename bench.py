@@ -524,9 +524,11 @@ def main():
     ap.add_argument("--e2e-period", type=int, default=-1,
                     help="compact e2e: copy every n-th chunk directly instead of packing (-1 = library default)")
     ap.add_argument("--e2e-mode", default="auto", choices=["auto", "dma", "compact", "gather", "gather_warp", "zerocopy"],
-                    help="host-buffer execute path for e2e (auto = zero-copy for pinned arrays)")
-    ap.add_argument("--partitioner", default="blocks", choices=["blocks", "equal_regions"],
-                    help="N>1 source decomposition: the reference's blocks bands, or equal regions")
+                    help="host-buffer execute path for e2e (auto = time gather/compact/dma on the first "
+                         "calls and keep the fastest)")
+    ap.add_argument("--partitioner", default="equal_regions", choices=["blocks", "equal_regions"],
+                    help="N>1 source decomposition: equal regions (BASELINE configs[2]; EQ zonal "
+                         "equal-area parts sized like blocks) or the reference pipeline's blocks bands")
     ap.add_argument("--fused", action="store_true",
                     help="N>1: no ghost copy — boundary targets read ghost rows from the owners' HBM "
                          "(CUDA IPC / NVLink) inside the apply kernel, fenced by NCCL barriers")
