@@ -29,12 +29,15 @@ def main():
     fdst = sg.Field(name="dst", shape=(m, L), kind=sg.Kind.REAL64, host=hdst.array)
     ref = None
     settings = [("dma", 2, 64)]
+    env = os.environ.get("SWEEP_ENV", "SG_GATHER_CTAS")  # knob swept in the third column
+    vals = [int(x) for x in os.environ.get("SWEEP_VALS", "2,4,8").split(",")]
+    chunks = [int(x) for x in os.environ.get("SWEEP_CHUNKS", "32,64,128").split(",")]
     for mode in sys.argv[1].split(",") if len(sys.argv) > 1 else ["gather"]:
-        for ctas in (2, 4, 8):
-            for ch in (32, 64, 128):
-                settings.append((mode, ctas, ch))
+        for v in vals:
+            for ch in chunks:
+                settings.append((mode, v, ch))
     for mode, ctas, ch in settings:
-        os.environ["SG_GATHER_CTAS"] = str(ctas)  # honoured by the build that ran the sweep
+        os.environ[env] = str(ctas)
         sgi.HOST_EXECUTE_MODE, sgi.HOST_EXECUTE_CHUNKS = mode, ch
         hdst.array[:] = 0
         for _ in range(3):
@@ -48,7 +51,7 @@ def main():
             ref = hdst.array.copy()
         ok = bool(np.array_equal(ref.view(np.uint64), hdst.array.view(np.uint64)))
         ms = statistics.median(ts) * 1e3
-        print(json.dumps({"mode": mode, "ctas_per_sm": ctas, "chunks": ch, "ms": round(ms, 2),
+        print(json.dumps({"mode": mode, env: ctas, "chunks": ch, "ms": round(ms, 2),
                           "gpts_lev_s": round(m * L / (ms * 1e-3) / 1e9, 4), "bitwise": ok}), flush=True)
 
 
