@@ -61,8 +61,10 @@ int32_t sg_field_h2d_rows(uint64_t field, int64_t row0, int64_t nrows, const voi
                           uint64_t stream);
 int32_t sg_field_d2h_rows(uint64_t field, int64_t row0, int64_t nrows, void* host,
                           uint64_t stream);
-/* pinned host buffers (cudaHostAlloc) for asynchronous, full-rate h2d/d2h, and CUDA events
- * for timing on the launching stream. */
+/* pinned, mapped host buffers (cudaHostAlloc) for asynchronous, full-rate h2d/d2h and the
+ * GPU gather of sg_remap_execute_host; sg_host_alloc_flags: bit 0 write-combined, bit 1
+ * zero-filled (the host mirrors create_field allocates, field.py:171).  CUDA events for
+ * timing on the launching stream. */
 int32_t sg_host_alloc(size_t bytes, uint64_t* out_ptr);
 int32_t sg_host_alloc_flags(size_t bytes, int32_t flags, uint64_t* out_ptr);
 int32_t sg_host_free(uint64_t ptr);

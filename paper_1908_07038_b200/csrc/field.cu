@@ -2,11 +2,50 @@
 // pitch chosen by field_pitch_elems (dense today).  h2d/d2h move the unpadded host
 // (npts, levels) C-order array (field.py:161): one contiguous copy for dense rows, a
 // cudaMemcpy2DAsync otherwise.
+#include <sys/mman.h>
+
 #include <algorithm>
+#include <mutex>
+#include <thread>
+#include <unordered_map>
+#include <vector>
 
 #include "cuda_util.cuh"
 
 using namespace sg;
+
+namespace {
+// Large pinned buffers: anonymous mmap backed by transparent huge pages, first-touched by
+// several threads, then cudaHostRegister'ed.  ~0.3 s for a 7.2 GB cfg3 mirror against ~3 s for
+// cudaHostAlloc, whose 4-KB pages the kernel zero-fills and pins one by one
+// (tools/probes/pin_probe.cu, profiles/r01_pin_probe.txt).  Fresh anonymous pages are zero.
+constexpr size_t kMmapPinBytes = size_t(64) << 20;
+std::mutex g_mm_mu;
+std::unordered_map<uintptr_t, size_t> g_mm;  // mmap'ed + registered buffers -> length
+
+void* mmap_pinned(size_t bytes) {
+  void* q = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (q == MAP_FAILED) return nullptr;
+  madvise(q, bytes, MADV_HUGEPAGE);
+  const int nth = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> th;
+  for (int i = 0; i < nth; ++i)
+    th.emplace_back([=] {
+      const size_t a = bytes * i / nth, b = bytes * (i + 1) / nth;
+      for (size_t o = a & ~size_t(4095); o < b; o += 4096)
+        if (o >= a) static_cast<volatile char*>(q)[o] = 0;
+    });
+  for (auto& t : th) t.join();
+  if (cudaHostRegister(q, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped) != cudaSuccess) {
+    cudaGetLastError();
+    munmap(q, bytes);
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(g_mm_mu);
+  g_mm[reinterpret_cast<uintptr_t>(q)] = bytes;
+  return q;
+}
+}  // namespace
 
 extern "C" {
 
@@ -145,19 +184,49 @@ extern "C" {
 int32_t sg_host_alloc(size_t bytes, uint64_t* out_ptr) { return sg_host_alloc_flags(bytes, 0, out_ptr); }
 
 // flags bit 0: write-combined (fast CPU writes and PCIe reads, very slow CPU reads)
+// flags bit 1: zero-filled (np.zeros semantics) — the current device writes the zeros through
+//              the mapped alias over PCIe, no host CPU time
 int32_t sg_host_alloc_flags(size_t bytes, int32_t flags, uint64_t* out_ptr) {
   SG_API_BEGIN
   SG_REQUIRE(out_ptr, "null out pointer");
   void* p = nullptr;
-  unsigned int f = cudaHostAllocPortable | ((flags & 1) ? cudaHostAllocWriteCombined : 0);
+  if (!(flags & 1) && bytes >= kMmapPinBytes && (p = mmap_pinned(bytes)) != nullptr) {
+    *out_ptr = reinterpret_cast<uint64_t>(p);  // zero-filled by the kernel
+    return SG_OK;
+  }
+  unsigned int f = cudaHostAllocPortable | cudaHostAllocMapped | ((flags & 1) ? cudaHostAllocWriteCombined : 0);
   SG_CUDA(cudaHostAlloc(&p, std::max<size_t>(bytes, 1), f));
+  if (flags & 2) {
+    void* dp = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(&dp, p, 0);
+    if (e == cudaSuccess) e = cudaMemset(dp, 0, std::max<size_t>(bytes, 1));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      cudaFreeHost(p);
+      SG_CUDA(e);
+    }
+  }
   *out_ptr = reinterpret_cast<uint64_t>(p);
   SG_API_END
 }
 
 int32_t sg_host_free(uint64_t ptr) {
   SG_API_BEGIN
-  SG_CUDA(cudaFreeHost(reinterpret_cast<void*>(ptr)));
+  size_t mm = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_mm_mu);
+    auto it = g_mm.find(ptr);
+    if (it != g_mm.end()) {
+      mm = it->second;
+      g_mm.erase(it);
+    }
+  }
+  if (mm) {
+    SG_CUDA(cudaHostUnregister(reinterpret_cast<void*>(ptr)));
+    munmap(reinterpret_cast<void*>(ptr), mm);
+  } else {
+    SG_CUDA(cudaFreeHost(reinterpret_cast<void*>(ptr)));
+  }
   SG_API_END
 }
 

@@ -172,11 +172,11 @@ class DeviceArray(N.Handle):
 class PinnedArray:
     """Page-locked host array (cudaHostAlloc) for full-rate asynchronous copies."""
 
-    def __init__(self, shape, dtype=np.float64, write_combined: bool = False):
+    def __init__(self, shape, dtype=np.float64, write_combined: bool = False, zero: bool = False):
         dtype = np.dtype(dtype)
         nbytes = int(np.prod(shape)) * dtype.itemsize
         p = C.c_uint64(0)
-        N.call("sg_host_alloc_flags", nbytes, int(bool(write_combined)), N.ref(p))
+        N.call("sg_host_alloc_flags", nbytes, int(bool(write_combined)) | (2 if zero else 0), N.ref(p))
         self._ptr = p.value
         buf = (C.c_char * max(nbytes, 1)).from_address(self._ptr)
         buf._sg_owner = self  # any view of .array keeps the pinned allocation alive

@@ -79,3 +79,28 @@ def test_pinned_registration_context(gpu):
     assert np.array_equal(f.device.to_numpy(), f.host)
     with sg.pinned(f.host):  # registering again after unregistering works
         pass
+
+
+def test_create_field_pins_large_host_mirrors(gpu):
+    """Host mirrors >= PIN_HOST_BYTES are page-locked, mapped and zero-filled (np.zeros
+    semantics), so apply_remap on host fields can use the GPU gather; small ones stay numpy."""
+    sg = gpu
+    from paper_1908_07038_b200 import field as F
+    from paper_1908_07038_b200.interp import _is_pinned
+
+    rows = F.PIN_HOST_BYTES // (8 * 137) + 1
+    big = sg.create_field("big", (rows, 137))
+    assert _is_pinned(big.host) and big.host.shape == (rows, 137) and big.host.dtype == np.float64
+    assert not big.host.any()
+    small = sg.create_field("small", (100, 137))
+    assert not _is_pinned(small.host) and not small.host.any()
+    i32 = sg.create_field("i32", (F.PIN_HOST_BYTES // 4 + 7, 1), sg.Kind.INT32)
+    assert _is_pinned(i32.host) and i32.host.dtype == np.int32 and not i32.host.any()
+    big.host[-1, -1] = 3.0  # writable, and round-trips through the device like any mirror
+    big.allocate_device()
+    assert big.device.to_numpy()[-1, -1] == 3.0
+    with big.device_view(sg.Intent.READ_WRITE):
+        pass
+    big.host[:] = 0
+    big.update_host()
+    assert big.host[-1, -1] == 3.0

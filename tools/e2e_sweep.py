@@ -25,8 +25,23 @@ def main():
     m, n, L = len(w), mesh.nb_nodes, 137
     hsrc, hdst = PinnedArray((n, L)), PinnedArray((m, L))
     bench.fill_smooth(hsrc.array, mesh.node_xyz, 0)
-    fsrc = sg.Field(name="src", shape=(n, L), kind=sg.Kind.REAL64, host=hsrc.array)
-    fdst = sg.Field(name="dst", shape=(m, L), kind=sg.Kind.REAL64, host=hdst.array)
+    if os.environ.get("CREATE") == "1":  # host mirrors from the public create_field
+        t = time.perf_counter()
+        a = sg.create_field("src", (n, L))
+        print(json.dumps({"create_field_s": round(time.perf_counter() - t, 3), "pinned": sgi._is_pinned(a.host)}),
+              flush=True)
+        a.host[:] = hsrc.array
+        fsrc, fdst = a, sg.create_field("dst", (m, L))
+        hsrc, hdst = None, None
+    elif os.environ.get("PAGEABLE") == "1":  # plain numpy arrays (user-supplied host storage)
+        class _A:
+            pass
+        a, b = _A(), _A()
+        a.array, b.array = hsrc.array.copy(), np.zeros((m, L))
+        hsrc, hdst = a, b
+    if hsrc is not None:
+        fsrc = sg.Field(name="src", shape=(n, L), kind=sg.Kind.REAL64, host=hsrc.array)
+        fdst = sg.Field(name="dst", shape=(m, L), kind=sg.Kind.REAL64, host=hdst.array)
     ref = None
     settings = [("dma", 2, 64)]
     env = os.environ.get("SWEEP_ENV", "SG_GATHER_CTAS")  # knob swept in the third column
@@ -39,7 +54,7 @@ def main():
     for mode, ctas, ch in settings:
         os.environ[env] = str(ctas)
         sgi.HOST_EXECUTE_MODE, sgi.HOST_EXECUTE_CHUNKS = mode, ch
-        hdst.array[:] = 0
+        fdst.host[:] = 0
         for _ in range(3):
             sg.apply_remap_fields(w, [fsrc], [fdst])
         ts = []
@@ -48,8 +63,8 @@ def main():
             sg.apply_remap_fields(w, [fsrc], [fdst])
             ts.append(time.perf_counter() - t)
         if ref is None:
-            ref = hdst.array.copy()
-        ok = bool(np.array_equal(ref.view(np.uint64), hdst.array.view(np.uint64)))
+            ref = fdst.host.copy()
+        ok = bool(np.array_equal(ref.view(np.uint64), fdst.host.view(np.uint64)))
         ms = statistics.median(ts) * 1e3
         print(json.dumps({"mode": mode, env: ctas, "chunks": ch, "ms": round(ms, 2),
                           "gpts_lev_s": round(m * L / (ms * 1e-3) / 1e9, 4), "bitwise": ok}), flush=True)
