@@ -61,6 +61,11 @@ int32_t sg_field_h2d_rows(uint64_t field, int64_t row0, int64_t nrows, const voi
                           uint64_t stream);
 int32_t sg_field_d2h_rows(uint64_t field, int64_t row0, int64_t nrows, void* host,
                           uint64_t stream);
+/* runs: nruns (row0, nrows) pairs; copies host[row0 : row0+nrows] of the full (npts, levels)
+ * host array into the same device rows (the host-field halo exchange uploads only the rows
+ * its peers read, functionspace.py:107-118). */
+int32_t sg_field_h2d_row_runs(uint64_t field, const int64_t* runs, int64_t nruns, const void* host,
+                              uint64_t stream);
 /* pinned, mapped host buffers (cudaHostAlloc) for asynchronous, full-rate h2d/d2h and the
  * GPU gather of sg_remap_execute_host; sg_host_alloc_flags: bit 0 write-combined, bit 1
  * zero-filled (the host mirrors create_field allocates, field.py:171).  CUDA events for

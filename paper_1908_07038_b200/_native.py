@@ -36,6 +36,7 @@ _SIGS = {
     "sg_field_d2h": [u64, vp, u64],
     "sg_field_h2d_rows": [u64, i64, i64, vp, u64],
     "sg_field_d2h_rows": [u64, i64, i64, vp, u64],
+    "sg_field_h2d_row_runs": [u64, vp, i64, vp, u64],
     "sg_field_info": [u64, vp, vp, vp, vp, vp],
     "sg_host_alloc": [sz, vp],
     "sg_host_alloc_flags": [sz, i32, vp],

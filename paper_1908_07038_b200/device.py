@@ -79,6 +79,16 @@ class DeviceArray(N.Handle):
         if sync:
             synchronize(self.device, stream)
 
+    def upload_row_runs(self, host: np.ndarray, runs: np.ndarray, stream: int = 0, sync: bool = True) -> None:
+        """Rows ``[r0, r0 + n)`` of the full host array ``host`` for every (r0, n) in ``runs``
+        into the same device rows."""
+        if host.shape != self.shape or host.dtype != self.dtype or not host.flags["C_CONTIGUOUS"]:
+            raise ValueError("host array must be C-contiguous with the device array's shape and dtype")
+        runs = np.ascontiguousarray(runs, dtype=np.int64).reshape(-1, 2)
+        N.call("sg_field_h2d_row_runs", self.handle, N.ptr(runs), len(runs), N.ptr(host), stream)
+        if sync:
+            synchronize(self.device, stream)
+
     def download_rows(self, row0: int, nrows: int, stream: int = 0) -> np.ndarray:
         out = np.empty((nrows, self.shape[1]), dtype=self.dtype)
         N.call("sg_field_d2h_rows", self.handle, row0, nrows, N.ptr(out), stream)

@@ -48,6 +48,21 @@ class HaloExchangePlan:
     recv: Dict[int, np.ndarray] = dc_field(default_factory=dict)
     recv_remote: Dict[int, np.ndarray] = dc_field(default_factory=dict)
     _native: Dict[int, N.Handle] = dc_field(default_factory=dict, repr=False)
+    _send_runs: Optional[np.ndarray] = dc_field(default=None, repr=False)
+
+    def send_runs(self) -> np.ndarray:
+        """(row0, nrows) runs covering the union of the send lists, ascending."""
+        if self._send_runs is None:
+            rows = np.unique(np.concatenate([np.asarray(v, np.int64) for v in self.send.values()])) \
+                if self.send else np.empty(0, np.int64)
+            if len(rows) == 0:
+                self._send_runs = np.empty((0, 2), np.int64)
+            else:
+                cut = np.flatnonzero(np.diff(rows) != 1) + 1
+                starts = rows[np.concatenate([[0], cut])]
+                ends = rows[np.concatenate([cut - 1, [len(rows) - 1]])] + 1
+                self._send_runs = np.stack([starts, ends - starts], axis=1).astype(np.int64)
+        return self._send_runs
 
     @property
     def peers(self):
@@ -162,9 +177,13 @@ def halo_exchange(plan: HaloExchangePlan, f: Field, ctx) -> None:
     if ctx is not None and getattr(ctx, "nranks", 1) > 1:
         if f.state is MemoryState.SYNCED and f.device is not None and f.device.device == current_device():
             dev = f.device
-        else:
+        else:  # stage only the rows peers read (the union of the send lists), not the field
             dev = _staging(f)
-            dev.upload(f.host)
+            h = f.host
+            if h.dtype == dev.dtype and h.flags["C_CONTIGUOUS"]:
+                dev.upload_row_runs(h, plan.send_runs())
+            else:
+                dev.upload(h)
         ctx.device_exchange(plan, dev)
         span = plan.ghost_rows
         if span is not None:

@@ -104,3 +104,32 @@ def test_create_field_pins_large_host_mirrors(gpu):
     big.host[:] = 0
     big.update_host()
     assert big.host[-1, -1] == 3.0
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("dtype,levels", [(np.float64, 137), (np.float32, 3), (np.int32, 1), (np.int64, 5)])
+def test_upload_row_runs(gpu, pinned, dtype, levels):
+    """sg_field_h2d_row_runs: only the listed row runs change on the device (one DMA per run
+    from pageable memory, one pull kernel from pinned mapped memory when there are many)."""
+    sg = gpu
+    from paper_1908_07038_b200.device import DeviceArray, PinnedArray
+
+    n = 5000
+    rng = np.random.default_rng(levels)
+    src = PinnedArray((n, levels), dtype).array if pinned else np.empty((n, levels), dtype)
+    src[:] = rng.integers(-1000, 1000, size=(n, levels)).astype(dtype)
+    d = DeviceArray(n, levels, dtype)
+    base = np.full((n, levels), 7, dtype)
+    d.upload(base)
+    starts = np.sort(rng.choice(n - 10, 60, replace=False))
+    starts = starts[np.concatenate([[True], np.diff(starts) > 10])]
+    runs = np.stack([starts, rng.integers(0, 10, len(starts))], axis=1)
+    d.upload_row_runs(src, runs)
+    expect = base.copy()
+    for r0, k in runs:
+        expect[r0:r0 + k] = src[r0:r0 + k]
+    assert np.array_equal(d.to_numpy(), expect)
+    from paper_1908_07038_b200._native import NativeError
+
+    with pytest.raises(NativeError):  # run past the last row: invalid argument, nothing copied
+        d.upload_row_runs(src, np.array([[n - 1, 2]]))
