@@ -299,7 +299,7 @@ int32_t sg_host_free(uint64_t ptr) {
 int32_t sg_host_register(uint64_t ptr, size_t bytes) {
   SG_API_BEGIN
   SG_REQUIRE(ptr && bytes, "empty range");
-  SG_CUDA(cudaHostRegister(reinterpret_cast<void*>(ptr), bytes, cudaHostRegisterPortable));
+  SG_CUDA(cudaHostRegister(reinterpret_cast<void*>(ptr), bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
   SG_API_END
 }
 

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 import threading
+import weakref
 
 import numpy as np
 
@@ -289,3 +290,67 @@ class pinned:
             N.call("sg_host_unregister", a.ctypes.data)
         self._done = []
         return False
+
+
+# ---- page-locking user arrays for the host-field execute paths --------------------------
+# Host fields built on plain numpy arrays (Field(host=...)) would otherwise go through the
+# driver's pageable staging copies (apply_remap at cfg3: 270 ms instead of 116 ms,
+# profiles/r01_e2e_modes.md).  Large arrays are registered (cudaHostRegister, mapped) the first
+# time a host-field path sees them and stay registered for the life of the numpy array that
+# owns the memory: a weakref finalizer unregisters them when that array is deallocated (numpy
+# clears weak references before it frees the data).
+AUTO_PIN_BYTES = 64 << 20
+_pin_lock = threading.Lock()
+_pinned_ranges: dict = {}  # start address -> (end address, finalizer)
+
+
+def _owner(a: np.ndarray):
+    base = a
+    while isinstance(base, np.ndarray) and base.base is not None:
+        base = base.base
+    return base
+
+
+def is_pinned(a: np.ndarray) -> bool:
+    """True when ``a`` lies in a library pinned allocation (PinnedArray) or in a range
+    registered by :func:`ensure_pinned`."""
+    own = _owner(a)
+    if isinstance(getattr(own, "_sg_owner", None), PinnedArray):
+        return True
+    lo, hi = a.ctypes.data, a.ctypes.data + a.nbytes
+    with _pin_lock:
+        return any(s <= lo and hi <= e for s, (e, _) in _pinned_ranges.items())
+
+
+def _unregister(start: int) -> None:
+    with _pin_lock:
+        _pinned_ranges.pop(start, None)
+    if not N._shutting_down:
+        try:
+            N.call("sg_host_unregister", start)
+        except Exception:  # noqa: BLE001 - context already gone at interpreter exit
+            pass
+
+
+def ensure_pinned(a: np.ndarray, min_bytes: int = AUTO_PIN_BYTES) -> bool:
+    """Page-lock ``a`` in place (if it is large, C-contiguous and owned by a numpy array) for
+    the rest of the owning array's life.  Returns whether ``a`` is pinned afterwards."""
+    if a is None or a.nbytes == 0:
+        return False
+    if is_pinned(a):
+        return True
+    if a.nbytes < min_bytes or not a.flags["C_CONTIGUOUS"] or N.device_count() < 1:
+        return False
+    own = _owner(a)
+    if not isinstance(own, np.ndarray) or not own.flags["OWNDATA"]:
+        return False  # memory owned by something we cannot watch (mmap, buffer object)
+    start, end = a.ctypes.data, a.ctypes.data + a.nbytes
+    with _pin_lock:
+        if any(s < end and start < e for s, (e, _) in _pinned_ranges.items()):
+            return False  # overlaps another registration (a different view of the same data)
+        try:
+            N.call("sg_host_register", start, a.nbytes)
+        except Exception:  # noqa: BLE001 - not registrable (e.g. out of lockable memory)
+            return False
+        _pinned_ranges[start] = (end, weakref.finalize(own, _unregister, start))
+    return True

@@ -181,6 +181,9 @@ def halo_exchange(plan: HaloExchangePlan, f: Field, ctx) -> None:
             dev = _staging(f)
             h = f.host
             if h.dtype == dev.dtype and h.flags["C_CONTIGUOUS"]:
+                from .device import ensure_pinned
+
+                ensure_pinned(h)  # large mirrors: the pull kernel reads the rows straight from host
                 dev.upload_row_runs(h, plan.send_runs())
             else:
                 dev.upload(h)

@@ -307,13 +307,11 @@ def _auto_mode(weights: InterpolationWeights, mapped: bool) -> str:
 
 
 def _is_pinned(a: np.ndarray) -> bool:
-    """True when ``a`` lives in a library pinned allocation (device.PinnedArray)."""
-    from .device import PinnedArray
+    """True when ``a`` is page-locked by the library (PinnedArray, or registered by
+    device.ensure_pinned)."""
+    from .device import is_pinned
 
-    base = a
-    while isinstance(base, np.ndarray) and base.base is not None:
-        base = base.base
-    return getattr(base, "_sg_owner", None) is not None and isinstance(base._sg_owner, PinnedArray)
+    return is_pinned(a)
 
 
 def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], host_dst: Sequence[np.ndarray],
@@ -406,6 +404,11 @@ def apply_remap_fields(weights: InterpolationWeights, source_fields: Sequence[Fi
             out = th if direct else np.empty(t.shape, np.float64)
             outs.append(out)
             copy_back.append(None if direct else (th, out))
+        from .device import ensure_pinned
+
+        for s, t in group:  # the fields' own large numpy arrays: page-locked once, for their lifetime
+            ensure_pinned(s.host)
+            ensure_pinned(t.host)
         moved = execute_host(weights, host_src, outs, srcs, dsts, nchunks=HOST_EXECUTE_CHUNKS,
                              mode=HOST_EXECUTE_MODE)
         weights.__dict__["last_host_rows_moved"] = moved  # source rows per field that crossed PCIe

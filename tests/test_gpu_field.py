@@ -133,3 +133,48 @@ def test_upload_row_runs(gpu, pinned, dtype, levels):
 
     with pytest.raises(NativeError):  # run past the last row: invalid argument, nothing copied
         d.upload_row_runs(src, np.array([[n - 1, 2]]))
+
+
+def test_ensure_pinned_lifetime(gpu):
+    """Plain numpy host arrays are registered once (mapped) and unregistered when the owning
+    array dies; views, small arrays and overlapping ranges are left alone."""
+    import gc
+
+    from paper_1908_07038_b200 import device as D
+
+    a = np.zeros((1 << 24,))  # 128 MiB
+    assert not D.is_pinned(a)
+    assert D.ensure_pinned(a) and D.is_pinned(a) and D.is_pinned(a[10:20])
+    assert D.ensure_pinned(a)  # idempotent
+    b = a[1:]  # overlapping, not contained: different range, already covered -> pinned
+    assert D.is_pinned(b)
+    small = np.zeros(100)
+    assert not D.ensure_pinned(small)
+    start = a.ctypes.data
+    del a, b
+    gc.collect()
+    assert start not in D._pinned_ranges  # finalizer unregistered it
+    c = np.zeros((1 << 24,))
+    assert D.ensure_pinned(c)  # the range can be registered again (also if the address was reused)
+    d = np.frombuffer(bytearray(1 << 27), dtype=np.float64)  # memory not owned by numpy
+    assert not D.ensure_pinned(d)
+
+
+def test_apply_remap_on_plain_numpy_fields_pins_them(gpu):
+    """Field(host=np.zeros(...)) of >= 64 MiB: apply_remap registers the arrays and takes the
+    GPU-gather path; results bitwise equal to the oracle."""
+    sg = gpu
+    from oracle import oracle as O
+    from paper_1908_07038_b200 import device as D
+
+    S, T = sg.grid_from_name("O320"), sg.grid_from_name("O160")
+    dist = sg.blocks_partition(S, 1)
+    mesh = sg.generate_mesh(S, dist, 0, halo=2, include_pole=True)
+    w = sg.build_remap(sg.NodeColumns(mesh, None), T, sg.matching_partition(T, S, dist))
+    L = 160  # 421,122 x 160 x 8 B = 539 MB source, 138 MB target
+    hs = np.random.default_rng(3).normal(size=(mesh.nb_nodes, L))
+    src = sg.Field(name="s", shape=hs.shape, kind=sg.Kind.REAL64, host=hs)
+    dst = sg.Field(name="d", shape=(len(w), L), kind=sg.Kind.REAL64, host=np.zeros((len(w), L)))
+    sg.apply_remap(w, src, dst)
+    assert D.is_pinned(src.host) and D.is_pinned(dst.host)
+    assert np.array_equal(dst.host.view(np.uint64), O.apply_remap(w.nodes, w.weights, hs).view(np.uint64))
