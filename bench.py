@@ -493,7 +493,8 @@ def run_multi(args):
             "metric": metric_name(source, target, method, L), "value": value, "unit": "Gpts·lev/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
-            "config": {"workload": f"{source}->{target} FE remap, {L} levels, {args.partitioner} P={world}, halo 2; "
+            "config": {"workload": f"{source}->{target} {'structured-bilinear' if method == 'bilinear' else 'FE'} remap, "
+                                   f"{L} levels, {args.partitioner} P={world}, halo 2; "
                                    + (f"step = fused exchange+apply over peer memory ({args.transport} fences)"
                                       if args.fused else
                                       f"step = halo exchange ({args.transport}) + apply (interior block overlapped "

@@ -20,3 +20,11 @@ timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --mast
   --master-port 29520 bench.py --gpus 4 --steps 5 --warmup 3 --transport ipc --fused --partitioner equal_regions \
   --config cfg2 > gpurun_out/bench_multi_fused_eq4.json 2> gpurun_out/bench_multi_fused_eq4.err
 echo "rc=$?" >> gpurun_out/bench_multi_fused_eq4.err
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+  --master-port 29521 bench.py --gpus 2 --steps 5 --warmup 3 --transport ipc --config cfg3 \
+  > gpurun_out/bench_multi_cfg3.json 2> gpurun_out/bench_multi_cfg3.err
+echo "rc=$?" >> gpurun_out/bench_multi_cfg3.err
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+  --master-port 29522 bench.py --gpus 2 --steps 5 --warmup 3 --transport ipc --config cfg5 \
+  > gpurun_out/bench_multi_cfg5.json 2> gpurun_out/bench_multi_cfg5.err
+echo "rc=$?" >> gpurun_out/bench_multi_cfg5.err
