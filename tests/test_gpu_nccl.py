@@ -95,3 +95,36 @@ def test_fork_join_capture_with_single_rank_nccl(gpu):
     main.synchronize()
     exp = O.apply_remap(w.nodes, w.weights, hsrc)
     assert np.array_equal(dst.to_numpy().view(np.uint64), exp.view(np.uint64))
+
+
+@pytest.mark.parametrize("dtype,levels", [(np.float64, 137), (np.float32, 5), (np.int64, 1)])
+def test_nccl_self_exchange_payloads(gpu, dtype, levels):
+    """Non-empty grouped ncclSend/ncclRecv through the real pack -> NCCL -> unpack path: a
+    single-rank communicator whose plan sends rows to itself (NCCL allows self send/recv), so
+    the payload offsets, pack order (requester's order) and unpack rows are exercised on one
+    GPU.  ghost rows <- owner rows, bitwise."""
+    sg = gpu
+    import paper_1908_07038_b200._native as N
+    from paper_1908_07038_b200.device import DeviceArray, Stream
+    from paper_1908_07038_b200.functionspace import HaloExchangePlan
+
+    uid = (C.c_uint8 * 128)()
+    N.call("sg_nccl_unique_id", N.ref(uid), 128)
+    h = C.c_uint64(0)
+    N.call("sg_comm_create", 0, 1, 0, N.ref(uid), 128, N.ref(h))
+    comm = N.Handle(h.value)
+    n, nghost = 20000, 3000
+    rng = np.random.default_rng(levels)
+    owned = n - nghost
+    send = rng.permutation(owned)[:nghost].astype(np.int64)  # permuted, like the reference's lists
+    recv = np.arange(owned, n, dtype=np.int64)
+    plan = HaloExchangePlan(nnodes=n, send={0: send}, recv={0: recv}, recv_remote={0: send})
+    host = rng.integers(-10**6, 10**6, size=(n, levels)).astype(dtype)
+    dev = DeviceArray(n, levels, dtype)
+    dev.upload(host)
+    st = Stream(0)
+    plan.exchange_nccl(dev, comm.handle, st.stream)
+    st.synchronize()
+    expect = host.copy()
+    expect[recv] = host[send]
+    assert np.array_equal(dev.to_numpy(), expect)
