@@ -295,6 +295,21 @@ def run_single(args):
     value = units / (ms * 1e-3) / 1e9
     device_out = ddst[F - 1].to_numpy()  # checked against the CPU baseline's result below
 
+    # ---- PCIe h2d peak on this box (the e2e path's roofline): one 2 GiB pinned DMA ----------
+    prow = (2 << 30) // (L * 8)
+    pdev = DeviceArray(prow, L, np.float64)
+    phost = PinnedArray((prow, L))
+    phost.array[:] = 1.0
+    pcie = []
+    for _ in range(3):
+        p0, p1 = Event(dev), Event(dev)
+        p0.record()
+        pdev.upload(phost.array, sync=False)
+        p1.record()
+        pcie.append(prow * L * 8 / (Event.elapsed_ms(p0, p1) * 1e-3) / 1e9)
+    pcie_h2d_gbs = max(pcie)
+    del pdev, phost
+
     # ---- e2e through the public API: host fields in pinned memory -------------------------
     import paper_1908_07038_b200.interp as sgi
 
@@ -336,6 +351,7 @@ def run_single(args):
                   "device_bitwise_vs_cpu": bool(np.array_equal(device_out.view(np.uint64), out.view(np.uint64))),
                   "e2e_bitwise_vs_cpu": bool(np.array_equal(hdst[F - 1].array.view(np.uint64), out.view(np.uint64)))}
 
+    h2d_moved = int(w.__dict__.get("last_host_rows_moved", n)) * L * 8 * F
     peak, peak_src = measured_peak()
     B = algorithmic_bytes(U, m, L, F, w.nodes.shape[1])
     kern_ms = statistics.mean(launch_ms)
@@ -353,11 +369,16 @@ def run_single(args):
                      "traffic": ncu_traffic(args.config), "algorithmic_bytes_per_launch": B,
                      "kernel_ms": kern_ms, "peak_source": peak_src},
         "e2e": {"value": units / e2e_s / 1e9, "unit": "Gpts·lev/s",
-                "h2d_bytes_per_step": int(w.__dict__.get("last_host_rows_moved", n)) * L * 8 * F,
+                "h2d_bytes_per_step": h2d_moved,
                 "input_bytes_per_step": n * L * 8 * F,
                 "d2h_bytes_per_step": m * L * 8 * F, "ms_per_step": e2e_s * 1e3, "statistic": "median",
                 "ms_per_step_mean": 1e3 * sum(e2e_times) / len(e2e_times),
                 "api": "paper_1908_07038_b200.apply_remap_fields(weights, host Fields, host Fields)",
+                "roofline": {"bound": "pcie h2d", "achieved": h2d_moved / e2e_s / 1e9, "peak": pcie_h2d_gbs,
+                             "unit": "GB/s", "frac": h2d_moved / e2e_s / 1e9 / pcie_h2d_gbs,
+                             "peak_source": "measured here: 2 GiB pinned h2d DMA, best of 3",
+                             "note": "source rows that must cross PCIe each step / step time; the d2h of the "
+                                     "target rows runs concurrently in the other direction"},
                 "mode": args.e2e_mode, "chunks": args.e2e_chunks, "direct_period": args.e2e_period,
                 "auto_trials_s": {k: [round(x, 4) for x in v] for k, v in w.__dict__.get("_auto_s", {}).items()}},
         "cpu_baseline": cpu,
