@@ -90,6 +90,13 @@ class DeviceArray(N.Handle):
         if sync:
             synchronize(self.device, stream)
 
+    def download_rows_into(self, row0: int, out: np.ndarray, stream: int = 0) -> None:
+        """Rows ``[row0, row0 + len(out))`` into the C-contiguous host array ``out``."""
+        if out.ndim != 2 or out.shape[1] != self.shape[1] or out.dtype != self.dtype or not out.flags["C_CONTIGUOUS"]:
+            raise ValueError("out must be C-contiguous (rows, levels) of the device array's dtype")
+        N.call("sg_field_d2h_rows", self.handle, row0, len(out), N.ptr(out), stream)
+        synchronize(self.device, stream)
+
     def download_rows(self, row0: int, nrows: int, stream: int = 0) -> np.ndarray:
         out = np.empty((nrows, self.shape[1]), dtype=self.dtype)
         N.call("sg_field_d2h_rows", self.handle, row0, nrows, N.ptr(out), stream)

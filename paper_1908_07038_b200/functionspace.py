@@ -191,7 +191,11 @@ def halo_exchange(plan: HaloExchangePlan, f: Field, ctx) -> None:
         span = plan.ghost_rows
         if span is not None:
             lo, hi = span
-            f.host[lo:hi] = dev.download_rows(lo, hi - lo)
+            out = f.host[lo:hi]
+            if out.dtype == dev.dtype and out.flags["C_CONTIGUOUS"]:
+                dev.download_rows_into(lo, out)  # straight into the (page-locked) mirror
+            else:
+                out[...] = dev.download_rows(lo, hi - lo)
         _count_messages(plan, f, ctx)
     if f.state is MemoryState.SYNCED:
         f.state = MemoryState.HOST_DIRTY
