@@ -320,7 +320,7 @@ def run_single(args):
     fsrc = [sg.Field(name=f"src{f}", shape=(n, L), kind=sg.Kind.REAL64, host=hsrc[f].array) for f in range(F)]
     fdst = [sg.Field(name=f"dst{f}", shape=(m, L), kind=sg.Kind.REAL64, host=hdst[f].array) for f in range(F)]
     e2e_steps = max(3, min(args.steps, 10))
-    for _ in range(6):  # warm: staging buffers, pipeline plans, the auto mode's two trials per path
+    for _ in range(4):  # warm: staging buffers, pipeline plans (auto: gather for pinned sources)
         sg.apply_remap_fields(w, fsrc, fdst)
     clocks.active = True
     e2e_times = []
@@ -546,8 +546,8 @@ def main():
     ap.add_argument("--e2e-period", type=int, default=-1,
                     help="compact e2e: copy every n-th chunk directly instead of packing (-1 = library default)")
     ap.add_argument("--e2e-mode", default="auto", choices=["auto", "dma", "compact", "gather", "gather_warp", "zerocopy"],
-                    help="host-buffer execute path for e2e (auto = time gather/compact/dma on the first "
-                         "calls and keep the fastest)")
+                    help="host-buffer execute path for e2e (auto = GPU gather for page-locked sources, "
+                         "else the faster of compact / dma timed on the first calls)")
     ap.add_argument("--partitioner", default="equal_regions", choices=["blocks", "equal_regions"],
                     help="N>1 source decomposition: equal regions (BASELINE configs[2]; EQ zonal "
                          "equal-area parts sized like blocks) or the reference pipeline's blocks bands")

@@ -290,15 +290,18 @@ def apply_remap_fused(weights: InterpolationWeights, plan, source: DeviceArray, 
 
 
 def _auto_mode(weights: InterpolationWeights, mapped: bool) -> str:
-    """Host-execute path chooser.  Moving only the referenced rows (gather / compact) pays
-    when the stencil skips a good share of the source rows (cfg5 bilinear reads every row ->
-    dma); which way wins depends on the host (profiles/r01_e2e_modes.md: compact 124 vs dma
-    134 ms on one box, 142 vs 135 on another), so the first calls time each candidate and the
-    fastest is kept.  gather needs pinned, mapped source arrays (device.PinnedArray)."""
+    """Host-execute path chooser.  Moving only the referenced rows pays when the stencil skips
+    a good share of the source rows (cfg5 bilinear reads every row -> dma).  Page-locked,
+    mapped sources take the GPU gather, which needs no host CPU and was fastest on every box
+    measured (profiles/r01_e2e_modes.md: 116 ms vs compact 124-143 ms vs dma 134-136 ms at cfg3).
+    Pageable sources choose between host packing (compact) and plain DMA by timing the first
+    calls, because host memory bandwidth decides it and differs between hosts."""
     n = max(weights.source_nnodes, 1)
     if weights.distinct_sources() >= 0.85 * n:
         return "dma"
-    modes = ("gather", "compact", "dma") if mapped else ("compact", "dma")
+    if mapped:
+        return "gather"
+    modes = ("compact", "dma")
     seen = weights.__dict__.setdefault("_auto_s", {})
     for m in modes:
         if len(seen.get(m, [])) < 2:  # the first call of a mode also builds its plan
