@@ -149,3 +149,30 @@ def test_distcontext_gloo_world3_plan_build():
     assert out[0][3] == [b"\x00", b"\x01", b"\x02"]
     assert all(o[4] == b"xy" for o in out)
     assert all(o[5] == [100, 101, 102] for o in out)
+
+
+def test_send_runs_cover_the_union_of_send_lists():
+    """HaloExchangePlan.send_runs: ascending (row0, nrows) runs of the union of every peer's
+    send list — the rows the host-field halo_exchange stages on the device."""
+    from paper_1908_07038_b200.functionspace import HaloExchangePlan
+
+    rng = np.random.default_rng(0)
+    send = {p: rng.choice(5000, 700, replace=False).astype(np.int64) for p in (1, 3, 6)}
+    plan = HaloExchangePlan(nnodes=6000, send=send)
+    runs = plan.send_runs()
+    assert runs.dtype == np.int64 and (runs[:, 1] > 0).all()
+    covered = np.concatenate([np.arange(r0, r0 + n) for r0, n in runs])
+    assert np.array_equal(covered, np.unique(np.concatenate(list(send.values()))))
+    assert (runs[1:, 0] > runs[:-1, 0] + runs[:-1, 1]).all()  # maximal runs: gaps between them
+    assert HaloExchangePlan(nnodes=10).send_runs().shape == (0, 2)
+
+
+def test_create_field_without_gpu_is_plain_numpy():
+    """No device: create_field keeps np.zeros host storage at any size (no pinning attempt)."""
+    import paper_1908_07038_b200 as sg
+    from paper_1908_07038_b200 import field as F
+
+    if sg._native.device_count() > 0:
+        pytest.skip("a GPU is present")
+    f = sg.create_field("x", (F.PIN_HOST_BYTES // 8 + 1, 1))
+    assert isinstance(f.host, np.ndarray) and f.host.base is None and not f.host.any()
