@@ -176,7 +176,12 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields,
  * stencil — PCIe carries U rows instead of every row (77 % at cfg3/cfg2).
  * flags bit 1 (zero-copy): the apply kernel reads source rows directly from the pinned host
  * array over PCIe and writes target rows directly into the pinned host array (mapped
- * pinned memory required, e.g. sg_host_alloc); no staging and no copy engines. */
+ * pinned memory required, e.g. sg_host_alloc); no staging and no copy engines.
+ * flags bit 2 (gather, the default for page-locked sources): a GPU kernel pulls exactly the
+ * referenced source rows out of the pinned, mapped host array with cp.async.bulk copies into a
+ * compact device copy (no host CPU work), pipelined with the apply and the d2h.
+ * flags bit 3 (with bit 2): warp-per-row loads instead of bulk copies (comparison only).
+ * flags bits 8-15 (compact): every n-th chunk copied whole by one DMA instead of packed. */
 
 /* ---- halo exchange (functionspace.py:58-118) ---------------------------------------------
  * sg_halo_plan_create <- HaloExchangePlan (functionspace.py:47-55): per peer (ascending),

@@ -91,3 +91,23 @@ def test_domain_error_maps_to_reference_class():
     z = [C.c_int64(0) for _ in range(4)]
     with pytest.raises(sg.InvalidDistribution):
         N.call("sg_meshgen_create", 2, N.ptr(nl), 0, N.ptr(part), 7, 1, 0, 0, N.ref(h), *[N.ref(x) for x in z])
+
+
+def build_c_program(out_path):
+    """tests/c_abi/remap_c.c: a plain C99 client of include/spheregrid_b200.h linked against
+    libsgb200.so (what a non-Python binding compiles)."""
+    import subprocess
+
+    lib = os.path.join(ROOT, "paper_1908_07038_b200", "_lib")
+    cmd = ["gcc", "-std=c99", "-O2", "-ffp-contract=off", "-Wall", "-Wextra", "-Werror",
+           "-I", os.path.join(ROOT, "include"), os.path.join(ROOT, "tests", "c_abi", "remap_c.c"),
+           "-o", str(out_path), "-L", lib, "-lsgb200", f"-Wl,-rpath,{lib}", "-lm"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return out_path
+
+
+def test_header_and_c_client_compile_and_link(tmp_path):
+    """The header is valid C99 and every symbol the client uses resolves at link time."""
+    exe = build_c_program(tmp_path / "remap_c")
+    assert os.path.exists(exe)
