@@ -168,3 +168,51 @@ def test_fused_exchange_apply_equals_exchange_then_apply(gpu, P):
     res = sg.run_ranks(P, prog)
     assert all(r[0] for r in res)
     assert all(r[1] for r in res)
+
+
+def _random_halo_cases(n, seed=7031):
+    rng = np.random.default_rng(seed)
+    grids = ["O16", "O32", "O48", "O80", "F8", "F16", "F32"]
+    kinds = ["REAL64", "REAL32", "INT32", "INT64"]
+    return [(str(rng.choice(grids)), int(rng.integers(2, 9)), int(rng.integers(1, 4)),
+             str(rng.choice(["blocks", "equal_regions"])), str(rng.choice(kinds)), int(rng.choice([1, 3, 137])))
+            for _ in range(n)]
+
+
+@pytest.mark.parametrize("grid,P,halo,part,kind,levels", _random_halo_cases(16))
+def test_random_halo_exchanges_host_and_device(gpu, grid, P, halo, part, kind, levels):
+    """Seeded random sweep (grids, parts, halo 1-3, both decompositions, every field kind,
+    1/3/137 levels): the host-field halo_exchange (staged send rows + pull kernel) and the
+    device-resident halo_exchange_device both leave every ghost row equal to its owner's values,
+    owned rows untouched, and count one message per peer with the payload length."""
+    sg = gpu
+    from paper_1908_07038_b200.partition import PARTITIONERS
+
+    S = sg.grid_from_name(grid)
+    dist = PARTITIONERS[part](S, P)
+    K = getattr(sg.Kind, kind)
+
+    def prog(ctx):
+        mesh = sg.generate_mesh(S, dist, ctx.rank, halo=halo, include_pole=True)
+        fs = sg.NodeColumns(mesh, ctx)
+        expect = (mesh.node_global[:, None] * 7 + np.arange(levels)[None, :] % 5).astype(K.dtype)
+        own = fs.owned_row_index()
+        f = fs.create_field("h", levels, K)
+        f.host[own] = expect[own]
+        before, before_b = ctx.messages_sent, ctx.bytes_sent
+        fs.halo_exchange(f, ctx)
+        ok_host = bool(np.array_equal(f.host, expect))
+        nbytes = sum(len(v) for v in fs.exchange_plan.send.values()) * levels * np.dtype(K.dtype).itemsize
+        msgs = ctx.messages_sent - before
+        assert ctx.bytes_sent - before_b == nbytes
+        g = fs.create_field("d", levels, K)
+        g.host[own] = expect[own]
+        g.allocate_device()
+        fs.halo_exchange_device(g, ctx)
+        g.update_host()
+        ok_dev = bool(np.array_equal(g.host, expect))
+        return ok_host, ok_dev, msgs, len(fs.exchange_plan.send), nbytes
+
+    res = sg.run_ranks(P, prog, devices=[0])
+    assert all(r[0] for r in res) and all(r[1] for r in res)
+    assert all(r[2] == r[3] for r in res)  # one message per peer per exchange
