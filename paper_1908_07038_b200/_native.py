@@ -20,6 +20,28 @@ from . import errors as E
 
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libsgb200.so")
 
+
+def _nccl_library() -> Optional[str]:
+    """The NCCL the installed torch links (the nvidia-nccl wheel), so the library's lazy dlopen
+    and a later ``import torch`` share one libnccl.so.2 (halo.cu nccl())."""
+    try:
+        import importlib.util
+
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return None
+    for d in (list(spec.submodule_search_locations or []) if spec else []):
+        path = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(path):
+            return path
+    return None
+
+
+if "SG_NCCL_LIBRARY" not in os.environ:
+    _nccl = _nccl_library()
+    if _nccl:
+        os.environ["SG_NCCL_LIBRARY"] = _nccl
+
 u64, i64, i32, u8p = C.c_uint64, C.c_int64, C.c_int32, C.POINTER(C.c_uint8)
 vp, sz, dp = C.c_void_p, C.c_size_t, C.c_void_p
 

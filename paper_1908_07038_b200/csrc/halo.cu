@@ -17,6 +17,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <numeric>
 #include <type_traits>
@@ -29,26 +30,48 @@ namespace {
 
 // Rows are moved as words of the field's item size (8 B for real64/int64, 4 B otherwise):
 // W words per row, pitches in words.  Dense rows are item-aligned only, so no wider moves.
-template <typename Wd>
-__global__ void pack_rows(const Wd* __restrict__ f, int64_t pitch_w, int W, const int32_t* __restrict__ rows,
-                          int64_t n, Wd* __restrict__ out) {
-  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (r >= n) return;
-  const Wd* src = f + (int64_t)rows[r] * pitch_w;
-  Wd* dst = out + r * W;
-  for (int l = lane; l < W; l += 32) dst[l] = src[l];
+// A warp moves one row; every lane issues all its loads of the row before its stores
+// (IT = ceil(W / 32) words per lane, 5 at 137 levels), so a row costs one memory latency —
+// HBM, or NVLink for the peer reads of pull_rows — instead of one per 32-word slice.  Rows
+// wider than 8 slices go in chunks of 4 slices.
+template <typename Wd, int IT>
+__device__ __forceinline__ void copy_row(Wd* __restrict__ dst, const Wd* __restrict__ src, int W, int lane) {
+  if (IT > 0) {
+    Wd v[IT > 0 ? IT : 1];
+#pragma unroll
+    for (int i = 0; i < IT; ++i)
+      if (lane + 32 * i < W) v[i] = src[lane + 32 * i];
+#pragma unroll
+    for (int i = 0; i < IT; ++i)
+      if (lane + 32 * i < W) dst[lane + 32 * i] = v[i];
+    return;
+  }
+  for (int b = 0; b < W; b += 128) {
+    Wd v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (b + lane + 32 * i < W) v[i] = src[b + lane + 32 * i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (b + lane + 32 * i < W) dst[b + lane + 32 * i] = v[i];
+  }
 }
 
-template <typename Wd>
-__global__ void unpack_rows(Wd* __restrict__ f, int64_t pitch_w, int W, const int32_t* __restrict__ rows, int64_t n,
-                            const Wd* __restrict__ in) {
+template <typename Wd, int IT>
+__global__ void __launch_bounds__(256) pack_rows(const Wd* __restrict__ f, int64_t pitch_w, int W,
+                                                 const int32_t* __restrict__ rows, int64_t n, Wd* __restrict__ out) {
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
   if (r >= n) return;
-  Wd* dst = f + (int64_t)rows[r] * pitch_w;
-  const Wd* src = in + r * W;
-  for (int l = lane; l < W; l += 32) dst[l] = src[l];
+  copy_row<Wd, IT>(out + r * W, f + (int64_t)rows[r] * pitch_w, W, threadIdx.x & 31);
+}
+
+template <typename Wd, int IT>
+__global__ void __launch_bounds__(256) unpack_rows(Wd* __restrict__ f, int64_t pitch_w, int W,
+                                                   const int32_t* __restrict__ rows, int64_t n,
+                                                   const Wd* __restrict__ in) {
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= n) return;
+  copy_row<Wd, IT>(f + (int64_t)rows[r] * pitch_w, in + r * W, W, threadIdx.x & 31);
 }
 
 struct PeerPtrs {
@@ -58,18 +81,32 @@ struct PeerPtrs {
 
 // Fused exchange: ghost row k (peer slot s) <- the owner's row recv_remote[k], read through a
 // peer pointer (same device, NVLink P2P or CUDA IPC): pack, transfer and unpack in one pass.
-template <typename Wd>
-__global__ void pull_rows(Wd* __restrict__ f, int64_t pitch_w, int W, const int32_t* __restrict__ rows,
-                          const int32_t* __restrict__ remote, const int32_t* __restrict__ slot, int64_t n,
-                          PeerPtrs peers) {
+template <typename Wd, int IT>
+__global__ void __launch_bounds__(256) pull_rows(Wd* __restrict__ f, int64_t pitch_w, int W,
+                                                 const int32_t* __restrict__ rows, const int32_t* __restrict__ remote,
+                                                 const int32_t* __restrict__ slot, int64_t n, PeerPtrs peers) {
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
   if (r >= n) return;
   const int s = slot[r];
   const Wd* src = static_cast<const Wd*>(peers.base[s]) + (int64_t)remote[r] * peers.pitch_w[s];
-  Wd* dst = f + (int64_t)rows[r] * pitch_w;
-  for (int l = lane; l < W; l += 32) dst[l] = src[l];
+  copy_row<Wd, IT>(f + (int64_t)rows[r] * pitch_w, src, W, threadIdx.x & 31);
 }
+
+// Launches KERNEL<Wd, IT> with IT = ceil(W / 32) (0 = chunked loop beyond 8 slices).
+#define SG_ROW_KERNEL(KERNEL, Wd, W, GRID, STREAM, ...)                          \
+  do {                                                                           \
+    switch (((W) + 31) / 32) {                                                   \
+      case 1: KERNEL<Wd, 1><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;       \
+      case 2: KERNEL<Wd, 2><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;       \
+      case 3: KERNEL<Wd, 3><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;       \
+      case 4: KERNEL<Wd, 4><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;       \
+      case 5: KERNEL<Wd, 5><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;       \
+      case 6: KERNEL<Wd, 6><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;       \
+      case 7: KERNEL<Wd, 7><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;       \
+      case 8: KERNEL<Wd, 8><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;       \
+      default: KERNEL<Wd, 0><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;      \
+    }                                                                            \
+  } while (0)
 
 inline unsigned warps_grid(int64_t n) { return (unsigned)((n + 7) / 8); }
 
@@ -98,7 +135,12 @@ Nccl g_nccl;
 Nccl& nccl() {
   std::lock_guard<std::mutex> lk(g_nccl_mu);
   if (!g_nccl.lib) {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    // SG_NCCL_LIBRARY (set by _native.py to the NCCL wheel torch links, when installed) first:
+    // a process that later imports torch must find the same libnccl.so.2 already loaded —
+    // an older system NCCL loaded under that soname breaks libtorch_cuda's symbol binding
+    void* h = nullptr;
+    if (const char* env = getenv("SG_NCCL_LIBRARY")) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (!h) throw_error(SG_DOMAIN_ERROR, "NcclUnavailable: cannot dlopen libnccl.so.2: %s", dlerror());
 #define SG_NCCL_SYM(field, name)                                                   \
@@ -234,9 +276,8 @@ int32_t sg_halo_pack(uint64_t plan, uint64_t field, void* dev_sendbuf, uint64_t 
   DeviceScope ds(p->device);
   by_word(f, [&](auto* tag) {
     using Wd = std::remove_pointer_t<decltype(tag)>;
-    pack_rows<Wd><<<warps_grid(n), 256, 0, as_stream(stream)>>>(f->buf.as<Wd>(), f->pitch, f->levels,
-                                                                p->send_rows.as<int32_t>(), n,
-                                                                static_cast<Wd*>(dev_sendbuf));
+    SG_ROW_KERNEL(pack_rows, Wd, f->levels, warps_grid(n), as_stream(stream), f->buf.as<Wd>(), f->pitch, f->levels,
+                  p->send_rows.as<int32_t>(), n, static_cast<Wd*>(dev_sendbuf));
   });
   SG_CUDA_LAUNCH();
   SG_API_END
@@ -253,9 +294,8 @@ int32_t sg_halo_unpack(uint64_t plan, uint64_t field, const void* dev_recvbuf, u
   DeviceScope ds(p->device);
   by_word(f, [&](auto* tag) {
     using Wd = std::remove_pointer_t<decltype(tag)>;
-    unpack_rows<Wd><<<warps_grid(n), 256, 0, as_stream(stream)>>>(f->buf.as<Wd>(), f->pitch, f->levels,
-                                                                  p->recv_rows.as<int32_t>(), n,
-                                                                  static_cast<const Wd*>(dev_recvbuf));
+    SG_ROW_KERNEL(unpack_rows, Wd, f->levels, warps_grid(n), as_stream(stream), f->buf.as<Wd>(), f->pitch, f->levels,
+                  p->recv_rows.as<int32_t>(), n, static_cast<const Wd*>(dev_recvbuf));
   });
   SG_CUDA_LAUNCH();
   SG_API_END
@@ -279,10 +319,8 @@ int32_t sg_halo_pull(uint64_t plan, uint64_t field, const uint64_t* peer_ptrs, c
   DeviceScope ds(p->device);
   by_word(f, [&](auto* tag) {
     using Wd = std::remove_pointer_t<decltype(tag)>;
-    pull_rows<Wd><<<warps_grid(n), 256, 0, as_stream(stream)>>>(f->buf.as<Wd>(), f->pitch, f->levels,
-                                                                p->recv_rows.as<int32_t>(),
-                                                                p->recv_remote.as<int32_t>(),
-                                                                p->recv_peer.as<int32_t>(), n, pp);
+    SG_ROW_KERNEL(pull_rows, Wd, f->levels, warps_grid(n), as_stream(stream), f->buf.as<Wd>(), f->pitch, f->levels,
+                  p->recv_rows.as<int32_t>(), p->recv_remote.as<int32_t>(), p->recv_peer.as<int32_t>(), n, pp);
   });
   SG_CUDA_LAUNCH();
   SG_API_END
@@ -343,8 +381,8 @@ int32_t sg_halo_exchange_nccl(uint64_t plan, uint64_t field, uint64_t comm, uint
   if (ns) {
     by_word(f, [&](auto* tag) {
       using Wd = std::remove_pointer_t<decltype(tag)>;
-      pack_rows<Wd><<<warps_grid(ns), 256, 0, st>>>(f->buf.as<Wd>(), f->pitch, f->levels, p->send_rows.as<int32_t>(),
-                                                    ns, p->sendbuf.as<Wd>());
+      SG_ROW_KERNEL(pack_rows, Wd, f->levels, warps_grid(ns), st, f->buf.as<Wd>(), f->pitch, f->levels,
+                    p->send_rows.as<int32_t>(), ns, p->sendbuf.as<Wd>());
     });
     SG_CUDA_LAUNCH();
   }
@@ -360,8 +398,8 @@ int32_t sg_halo_exchange_nccl(uint64_t plan, uint64_t field, uint64_t comm, uint
   if (nr) {
     by_word(f, [&](auto* tag) {
       using Wd = std::remove_pointer_t<decltype(tag)>;
-      unpack_rows<Wd><<<warps_grid(nr), 256, 0, st>>>(f->buf.as<Wd>(), f->pitch, f->levels, p->recv_rows.as<int32_t>(),
-                                                      nr, p->recvbuf.as<Wd>());
+      SG_ROW_KERNEL(unpack_rows, Wd, f->levels, warps_grid(nr), st, f->buf.as<Wd>(), f->pitch, f->levels,
+                    p->recv_rows.as<int32_t>(), nr, p->recvbuf.as<Wd>());
     });
     SG_CUDA_LAUNCH();
   }

@@ -128,3 +128,22 @@ def test_nccl_self_exchange_payloads(gpu, dtype, levels):
     expect = host.copy()
     expect[recv] = host[send]
     assert np.array_equal(dev.to_numpy(), expect)
+
+
+def test_nccl_before_torch_import(gpu):
+    """A fresh process that creates the library's NCCL communicator BEFORE importing torch can
+    still import torch: the lazy dlopen loads the same libnccl.so.2 torch links
+    (SG_NCCL_LIBRARY), not an older system NCCL under the same soname."""
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    code = (
+        "import ctypes as C, sys; sys.path.insert(0, %r)\n"
+        "import paper_1908_07038_b200._native as N\n"
+        "uid = (C.c_uint8 * 128)(); N.call('sg_nccl_unique_id', N.ref(uid), 128)\n"
+        "h = C.c_uint64(0); N.call('sg_comm_create', 0, 1, 0, N.ref(uid), 128, N.ref(h))\n"
+        "import torch; assert torch.cuda.is_available(); print('ok', torch.cuda.nccl.version())\n" % ROOT)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr[-2000:]
