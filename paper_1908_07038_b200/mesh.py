@@ -13,7 +13,6 @@ from __future__ import annotations
 import ctypes as C
 import enum
 from dataclasses import dataclass
-import math
 from typing import List, Optional, Tuple
 
 import numpy as np

@@ -1,7 +1,7 @@
 """Host arithmetic probe: prints digests of the numpy
 ufunc results that the bit-exact coordinate path depends on, so a run here and
 a run on the GPU box host can be compared."""
-import ctypes, ctypes.util, hashlib, json, math, os, platform
+import ctypes, ctypes.util, hashlib, json, os, platform
 import numpy as np
 
 def digest(a):

@@ -5,7 +5,6 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_1908_07038_b200 as sg
-from paper_1908_07038_b200.device import Event
 from oracle import oracle as O
 
 sg.set_device(0)
