@@ -15,8 +15,10 @@
 #include <algorithm>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <vector>
 
+#include "host_pool.h"
 #include "sg_internal.h"
 
 namespace sg {
@@ -101,6 +103,34 @@ std::shared_ptr<Topology> serial_topology(const std::vector<int64_t>& nlons, boo
   return t;
 }
 
+// Element and node passes run in blocks on a host thread pool (results are independent of the
+// block split: every pass writes per-element slots, or sets node flags to one value per pass).
+HostPool& mesh_pool() {
+  static HostPool pool((int)std::max(1u, std::min(16u, std::thread::hardware_concurrency())) - 1);
+  return pool;
+}
+
+template <class F>
+void pfor(int64_t n, F&& body) {  // body(lo, hi) over [0, n) in blocks
+  if (n <= 0) return;
+  HostPool& pool = mesh_pool();
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(pool.size() * 4, (n + 32767) / 32768));
+  if (nb == 1) {
+    body((int64_t)0, n);
+    return;
+  }
+  pool.parallel_for(nb, [&](int b) { body(n * b / nb, n * (b + 1) / nb); });
+}
+
+template <class T>
+inline void set_relaxed(T* p, T v) {
+  __atomic_store_n(p, v, __ATOMIC_RELAXED);
+}
+template <class T>
+inline T get_relaxed(const T* p) {
+  return __atomic_load_n(p, __ATOMIC_RELAXED);
+}
+
 struct MeshGen : Object {
   MeshGen() : Object(ObjKind::MeshGen) {}
   std::vector<int64_t> node_global, node_remote, elem_off, elem_idx, elem_serial;
@@ -149,54 +179,73 @@ int32_t sg_meshgen_create(int32_t nrows, const int64_t* nlons, int32_t include_p
     owner[npts + 1] = owner[npts - 1];
   }
   std::vector<uint8_t> owned(nn);
-  for (int64_t g = 0; g < nn; ++g) owned[g] = owner[g] == part;
+  pfor(nn, [&](int64_t lo, int64_t hi) {
+    for (int64_t g = lo; g < hi; ++g) owned[g] = owner[g] == part;
+  });
   // element levels 0/1
   std::vector<int16_t> level(nelem, -1);
   const int64_t* off = topo->off.data();
   const int32_t* en = topo->nodes.data();
-  for (int64_t e = 0; e < nelem; ++e) {
-    int64_t c = 0, k = off[e + 1] - off[e];
-    for (int64_t i = off[e]; i < off[e + 1]; ++i) c += owned[en[i]];
-    if (c == k) level[e] = 0;
-    else if (c > 0 && halo >= 1) level[e] = 1;
-  }
+  pfor(nelem, [&](int64_t lo, int64_t hi) {
+    for (int64_t e = lo; e < hi; ++e) {
+      int64_t c = 0, k = off[e + 1] - off[e];
+      for (int64_t i = off[e]; i < off[e + 1]; ++i) c += owned[en[i]];
+      if (c == k) level[e] = 0;
+      else if (c > 0 && halo >= 1) level[e] = 1;
+    }
+  });
+  // nodes of kept elements: present; ghosts remember the first level that brings them in
+  // (every writer of a pass stores the same value, so the block split does not matter)
   std::vector<uint8_t> present(nn, 0);
   std::vector<int16_t> intro(nn, 99);
-  for (int64_t e = 0; e < nelem; ++e) {
-    if (level[e] < 0) continue;
-    const int16_t lv = std::max<int16_t>(level[e], 1);
-    for (int64_t i = off[e]; i < off[e + 1]; ++i) {
-      const int32_t g = en[i];
-      present[g] = 1;
-      if (!owned[g]) intro[g] = std::min(intro[g], lv);
-    }
-  }
-  std::vector<int64_t> added;
-  for (int32_t depth = 2; depth <= halo; ++depth) {
-    added.clear();
-    for (int64_t e = 0; e < nelem; ++e) {
-      if (level[e] >= 0) continue;
-      for (int64_t i = off[e]; i < off[e + 1]; ++i)
-        if (present[en[i]]) {
-          added.push_back(e);
-          break;
-        }
-    }
-    for (int64_t e : added) level[e] = (int16_t)depth;
-    for (int64_t e : added)
+  pfor(nelem, [&](int64_t lo, int64_t hi) {
+    for (int64_t e = lo; e < hi; ++e) {
+      if (level[e] < 0) continue;
       for (int64_t i = off[e]; i < off[e + 1]; ++i) {
         const int32_t g = en[i];
-        present[g] = 1;
-        if (!owned[g]) intro[g] = std::min(intro[g], (int16_t)depth);
+        set_relaxed(&present[g], (uint8_t)1);
+        if (!owned[g]) set_relaxed(&intro[g], (int16_t)1);  // max(level, 1) == 1 here
       }
+    }
+  });
+  std::vector<uint8_t> fresh(nelem, 0);
+  for (int32_t depth = 2; depth <= halo; ++depth) {
+    pfor(nelem, [&](int64_t lo, int64_t hi) {  // elements touching a present node
+      for (int64_t e = lo; e < hi; ++e) {
+        fresh[e] = 0;
+        if (level[e] >= 0) continue;
+        for (int64_t i = off[e]; i < off[e + 1]; ++i)
+          if (present[en[i]]) {
+            fresh[e] = 1;
+            break;
+          }
+      }
+    });
+    pfor(nelem, [&](int64_t lo, int64_t hi) {
+      for (int64_t e = lo; e < hi; ++e) {
+        if (!fresh[e]) continue;
+        level[e] = (int16_t)depth;
+        for (int64_t i = off[e]; i < off[e + 1]; ++i) {
+          const int32_t g = en[i];
+          set_relaxed(&present[g], (uint8_t)1);
+          if (!owned[g] && get_relaxed(&intro[g]) > depth) set_relaxed(&intro[g], (int16_t)depth);
+        }
+      }
+    });
   }
-  // kept elements: ascending level, serial order within a level (stable)
+  // kept elements: ascending level, serial order within a level (counting sort, stable)
   int16_t maxlv = 0;
   for (int64_t e = 0; e < nelem; ++e) maxlv = std::max(maxlv, level[e]);
   auto M = std::make_unique<MeshGen>();
-  for (int16_t lv = 0; lv <= maxlv; ++lv)
+  {
+    std::vector<int64_t> cnt((size_t)maxlv + 2, 0);
     for (int64_t e = 0; e < nelem; ++e)
-      if (level[e] == lv) M->elem_serial.push_back(e);
+      if (level[e] >= 0) ++cnt[(size_t)level[e] + 1];
+    for (size_t l = 1; l < cnt.size(); ++l) cnt[l] += cnt[l - 1];
+    M->elem_serial.resize((size_t)cnt.back());
+    for (int64_t e = 0; e < nelem; ++e)
+      if (level[e] >= 0) M->elem_serial[(size_t)cnt[(size_t)level[e]]++] = e;
+  }
   // local nodes
   for (int64_t g = 0; g < nn; ++g)
     if (owned[g]) M->node_global.push_back(g);
@@ -224,13 +273,24 @@ int32_t sg_meshgen_create(int32_t nrows, const int64_t* nlons, int32_t include_p
     M->node_halo[i] = gh ? ghosts[i - M->nowned].first : 0;
     M->node_remote[i] = gh ? rank_in_part[g] : i;
   }
-  M->elem_off.reserve(M->elem_serial.size() + 1);
-  M->elem_off.push_back(0);
-  for (int64_t e : M->elem_serial) {
-    for (int64_t i = off[e]; i < off[e + 1]; ++i) M->elem_idx.push_back(local_of[en[i]]);
-    M->elem_off.push_back((int64_t)M->elem_idx.size());
-    M->elem_halo.push_back(level[e]);
+  // local connectivity (CSR): offsets by prefix sum, indices filled in blocks
+  const int64_t nkept = (int64_t)M->elem_serial.size();
+  M->elem_off.resize((size_t)nkept + 1);
+  M->elem_halo.resize((size_t)nkept);
+  M->elem_off[0] = 0;
+  for (int64_t k = 0; k < nkept; ++k) {
+    const int64_t e = M->elem_serial[(size_t)k];
+    M->elem_off[(size_t)k + 1] = M->elem_off[(size_t)k] + (off[e + 1] - off[e]);
+    M->elem_halo[(size_t)k] = level[e];
   }
+  M->elem_idx.resize((size_t)M->elem_off[(size_t)nkept]);
+  pfor(nkept, [&](int64_t lo, int64_t hi) {
+    for (int64_t k = lo; k < hi; ++k) {
+      const int64_t e = M->elem_serial[(size_t)k];
+      int64_t o = M->elem_off[(size_t)k];
+      for (int64_t i = off[e]; i < off[e + 1]; ++i) M->elem_idx[(size_t)o++] = local_of[en[i]];
+    }
+  });
   if (out_nnodes) *out_nnodes = nloc;
   if (out_nowned) *out_nowned = M->nowned;
   if (out_nelems) *out_nelems = (int64_t)M->elem_serial.size();
