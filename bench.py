@@ -53,7 +53,17 @@ def metric_name(source, target, method, L):
 def config(name):
     c = CONFIGS[name]
     return c[0], c[1], c[2], c[3], (c[4] if len(c) > 4 else "fe")
-METRIC = "Gpts·lev/s O1280→O640 FE interp, 137 lev fp64"
+def _baseline_metric() -> str:
+    """BASELINE.json's metric string verbatim (the roofline fraction and the halo GB/s it
+    names are the line's ``roofline.frac`` and, at N>1, ``halo.GB_per_s``)."""
+    try:
+        with open(os.path.join(ROOT, "BASELINE.json")) as fh:
+            return json.load(fh)["metric"]
+    except (OSError, KeyError, ValueError):
+        return "Gpts·lev/s O1280→O640 FE interp, 137 lev fp64; % HBM roofline; halo GB/s"
+
+
+METRIC = _baseline_metric()
 
 
 def log(*a):
