@@ -244,7 +244,7 @@ def run_reference(args):
     value = units / (ms * 1e-3) / 1e9
     line = {
         "metric": metric_name(source, target, method, L), "value": value, "unit": "Gpts·lev/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
         "impl": "reference",
         "config": {"workload": f"{source}->{target} {'structured-bilinear' if method == 'bilinear' else 'FE'} remap "
@@ -369,7 +369,7 @@ def run_single(args):
     line = {
         "metric": metric_name(source, target, method, L), "value": value, "unit": "Gpts·lev/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "ms_per_step_median": ms_median, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
         "config": {"workload": f"{source}->{target} {'structured-bilinear' if method == 'bilinear' else 'FE'} remap "
                                f"apply, {L} levels x {F} field(s), P=1",
                    "levels": L, "fields": F, "targets": m, "source_nodes": n, "distinct_sources": U,
