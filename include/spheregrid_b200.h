@@ -229,6 +229,9 @@ int32_t sg_halo_exchange_nccl(uint64_t plan, uint64_t field, uint64_t comm,
 /* Stream-ordered barrier (ncclAllReduce of one word on `stream`): fences the fused
  * exchange+apply's peer reads without a host round trip; graph-capturable. */
 int32_t sg_comm_barrier(uint64_t comm, uint64_t stream);
+/* one process, several GPUs (in-process ranks): ncclCommInitAll over devices[0..ndev), one
+ * communicator handle per device in out_comms[rank] (SURVEY.md §8(b) sg_comm_init_all). */
+int32_t sg_comm_init_all(int32_t ndev, const int32_t* devices, uint64_t* out_comms);
 
 /* Partition-invariant digest of owned rows [row0, row0+nrows) whose global ids are gids
  * (functionspace.py:233-254): the wrapping u64 sum of splitmix64(gid*G + (level+1)*Lv ^ bits);

@@ -121,6 +121,7 @@ struct Nccl {
   void* lib = nullptr;
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
@@ -148,6 +149,7 @@ Nccl& nccl() {
   if (!g_nccl.field) throw_error(SG_DOMAIN_ERROR, "NcclUnavailable: missing %s", name);
     SG_NCCL_SYM(GetUniqueId, "ncclGetUniqueId");
     SG_NCCL_SYM(CommInitRank, "ncclCommInitRank");
+    SG_NCCL_SYM(CommInitAll, "ncclCommInitAll");
     SG_NCCL_SYM(CommDestroy, "ncclCommDestroy");
     SG_NCCL_SYM(GroupStart, "ncclGroupStart");
     SG_NCCL_SYM(GroupEnd, "ncclGroupEnd");
@@ -351,6 +353,29 @@ int32_t sg_comm_create(int32_t device, int32_t nranks, int32_t rank, const uint8
   c->token.alloc(device, 16);  // barrier word: allocated here, never inside a graph capture
   SG_CUDA(cudaMemset(c->token.ptr, 0, 16));
   *out_comm = registry_put(c.release());
+  SG_API_END
+}
+
+// One process driving several GPUs (in-process ranks, one host thread per GPU): one
+// communicator per device from ncclCommInitAll; rank r of the set runs on devices[r].
+int32_t sg_comm_init_all(int32_t ndev, const int32_t* devices, uint64_t* out_comms) {
+  SG_API_BEGIN
+  SG_REQUIRE(ndev >= 1 && devices && out_comms, "bad arguments");
+  std::vector<ncclComm_t> comms((size_t)ndev, nullptr);
+  std::vector<int> devs(devices, devices + ndev);
+  SG_NCCL(nccl().CommInitAll(comms.data(), ndev, devs.data()));
+  for (int r = 0; r < ndev; ++r) {
+    DeviceScope ds(devs[(size_t)r]);
+    auto c = std::make_unique<Comm>();
+    c->device = devs[(size_t)r];
+    c->nranks = ndev;
+    c->rank = r;
+    c->comm = comms[(size_t)r];
+    comms[(size_t)r] = nullptr;
+    c->token.alloc(c->device, 16);
+    SG_CUDA(cudaMemset(c->token.ptr, 0, 16));
+    out_comms[r] = registry_put(c.release());
+  }
   SG_API_END
 }
 

@@ -147,3 +147,32 @@ def test_nccl_before_torch_import(gpu):
         "import torch; assert torch.cuda.is_available(); print('ok', torch.cuda.nccl.version())\n" % ROOT)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr[-2000:]
+
+
+def test_comm_init_all_single_process(gpu):
+    """sg_comm_init_all (ncclCommInitAll, one process driving its GPUs): the communicator of
+    device 0 carries a real self-exchange and the stream-ordered barrier."""
+    sg = gpu
+    import paper_1908_07038_b200._native as N
+    from paper_1908_07038_b200.device import DeviceArray, Stream
+    from paper_1908_07038_b200.functionspace import HaloExchangePlan
+
+    devs = np.array([0], np.int32)
+    out = np.zeros(1, np.uint64)
+    N.call("sg_comm_init_all", 1, N.ptr(devs), N.ptr(out))
+    comm = N.Handle(int(out[0]))
+    n, levels = 4000, 137
+    rng = np.random.default_rng(11)
+    send = rng.permutation(3000)[:1000].astype(np.int64)
+    recv = np.arange(3000, n, dtype=np.int64)
+    plan = HaloExchangePlan(nnodes=n, send={0: send}, recv={0: recv}, recv_remote={0: send})
+    host = rng.normal(size=(n, levels))
+    dev = DeviceArray(n, levels, np.float64)
+    dev.upload(host)
+    st = Stream(0)
+    N.call("sg_comm_barrier", comm.handle, st.stream)
+    plan.exchange_nccl(dev, comm.handle, st.stream)
+    st.synchronize()
+    expect = host.copy()
+    expect[recv] = host[send]
+    assert np.array_equal(dev.to_numpy(), expect)
