@@ -180,11 +180,14 @@ def halo_exchange(plan: HaloExchangePlan, f: Field, ctx) -> None:
         else:  # stage only the rows peers read (the union of the send lists), not the field
             dev = _staging(f)
             h = f.host
-            if h.dtype == dev.dtype and h.flags["C_CONTIGUOUS"]:
-                from .device import ensure_pinned
+            from .device import ensure_pinned
 
-                ensure_pinned(h)  # large mirrors: the pull kernel reads the rows straight from host
-                dev.upload_row_runs(h, plan.send_runs())
+            runs = plan.send_runs()
+            # page-locked mirrors (large ones are pinned here): one pull kernel reads the runs
+            # straight from host memory; few runs: one DMA each; many runs from a small pageable
+            # array: one DMA of the whole field beats a staged copy per run
+            if h.dtype == dev.dtype and h.flags["C_CONTIGUOUS"] and (ensure_pinned(h) or len(runs) <= 16):
+                dev.upload_row_runs(h, runs)
             else:
                 dev.upload(h)
         ctx.device_exchange(plan, dev)
