@@ -182,3 +182,27 @@ def test_serial_topology_is_global_sweep():
     assert len(topo.elem_nodes) == m.nb_elements
     assert sum(len(e) for e in topo.elem_nodes) == len(m.element_connectivity.indices)
     assert topo.node_lonlat.shape == (g.npts + 2, 2)
+
+
+def test_runtime_initialise_finalise(monkeypatch):
+    """initialise / finalise (runtime.py of the reference): DoubleInitialise on a second
+    initialise, the debug channel from SPHEREGRID_DEBUG, warning/error on the error stream."""
+    import io
+
+    monkeypatch.setenv("SPHEREGRID_DEBUG", "1")
+    out, err = io.StringIO(), io.StringIO()
+    lib = sg.initialise(out=out, err=err)
+    try:
+        with pytest.raises(sg.DoubleInitialise):
+            sg.initialise()
+        assert lib.config.debug and "debug: version" in out.getvalue()
+        lib.log.warning("w")
+        lib.log.info("i")
+        assert "warning: w" in err.getvalue() and "info: i" in out.getvalue()
+    finally:
+        sg.finalise()
+    sg.finalise()  # idempotent
+    monkeypatch.setenv("SPHEREGRID_DEBUG", "0")
+    lib = sg.initialise(out=io.StringIO())
+    assert not lib.config.debug
+    sg.finalise()
