@@ -382,20 +382,27 @@ void launch_bulk(ApplyArgs a, int L, int64_t m, size_t budget, cudaStream_t st) 
 }  // namespace
 
 namespace detail {
+// Threads per block of the warp-per-target kernels: 2 warps (targets).  Register use caps a
+// SM at 32 resident warps either way; small blocks retire and refill at target granularity
+// instead of waiting for the slowest of 8 gathers (cfg3: 1.085 vs 1.096 ms with 8-warp blocks,
+// profiles/r01_apply_variant_sweep2.jsonl).  Variant 16 keeps 8-warp blocks for comparison.
+static int warp_block_threads(int variant) { return variant == 16 ? 256 : 64; }
+
 void launch_apply(ApplyArgs a, int variant, cudaStream_t st) {
   const int64_t m = a.t1 - a.t0;
   if (m <= 0) return;
   const int L = a.levels;
   if (a.k == 4) {
-    const unsigned grid = (unsigned)((m + 7) / 8);
+    const int tpb = warp_block_threads(variant);
+    const unsigned grid = (unsigned)((m * 32 + tpb - 1) / tpb);
     switch ((L + 31) / 32) {
-      case 1: apply4_warp<1><<<grid, 256, 0, st>>>(a); break;
-      case 2: apply4_warp<2><<<grid, 256, 0, st>>>(a); break;
-      case 3: apply4_warp<3><<<grid, 256, 0, st>>>(a); break;
-      case 4: apply4_warp<4><<<grid, 256, 0, st>>>(a); break;
-      case 5: apply4_warp<5><<<grid, 256, 0, st>>>(a); break;
-      case 6: apply4_warp<6><<<grid, 256, 0, st>>>(a); break;
-      default: apply4_warp<0><<<grid, 256, 0, st>>>(a); break;
+      case 1: apply4_warp<1><<<grid, tpb, 0, st>>>(a); break;
+      case 2: apply4_warp<2><<<grid, tpb, 0, st>>>(a); break;
+      case 3: apply4_warp<3><<<grid, tpb, 0, st>>>(a); break;
+      case 4: apply4_warp<4><<<grid, tpb, 0, st>>>(a); break;
+      case 5: apply4_warp<5><<<grid, tpb, 0, st>>>(a); break;
+      case 6: apply4_warp<6><<<grid, tpb, 0, st>>>(a); break;
+      default: apply4_warp<0><<<grid, tpb, 0, st>>>(a); break;
     }
     SG_CUDA_LAUNCH();
     return;
@@ -409,30 +416,31 @@ void launch_apply(ApplyArgs a, int variant, cudaStream_t st) {
   } else if (L <= 8) {
     apply_thread_short<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(a);
   } else {
-    const unsigned grid = (unsigned)((m + 7) / 8);  // 8 warps per block, warp per target
+    const int tpb = warp_block_threads(variant);  // warp per target
+    const unsigned grid = (unsigned)((m * 32 + tpb - 1) / tpb);
     const int nv = (L + 1) / 2;
     if (even && variant != 3) {
       switch (nv <= 32 ? 1 : nv <= 64 ? 2 : nv <= 96 ? 3 : nv <= 128 ? 4 : 0) {
-        case 1: apply_warp_v2<1><<<grid, 256, 0, st>>>(a); break;
-        case 2: apply_warp_v2<2><<<grid, 256, 0, st>>>(a); break;
-        case 3: apply_warp_v2<3><<<grid, 256, 0, st>>>(a); break;
-        case 4: apply_warp_v2<4><<<grid, 256, 0, st>>>(a); break;
-        default: apply_warp_loop<<<grid, 256, 0, st>>>(a); break;
+        case 1: apply_warp_v2<1><<<grid, tpb, 0, st>>>(a); break;
+        case 2: apply_warp_v2<2><<<grid, tpb, 0, st>>>(a); break;
+        case 3: apply_warp_v2<3><<<grid, tpb, 0, st>>>(a); break;
+        case 4: apply_warp_v2<4><<<grid, tpb, 0, st>>>(a); break;
+        default: apply_warp_loop<<<grid, tpb, 0, st>>>(a); break;
       }
     } else if ((variant == 4 || variant == 5) && (L + 31) / 32 == 5) {
-      if (variant == 4) apply_warp_v1<5, 2><<<grid, 256, 0, st>>>(a);  // L2::256B prefetch
-      else apply_warp_v1<5, 1><<<grid, 256, 0, st>>>(a);                // L2::128B prefetch
+      if (variant == 4) apply_warp_v1<5, 2><<<grid, tpb, 0, st>>>(a);  // L2::256B prefetch
+      else apply_warp_v1<5, 1><<<grid, tpb, 0, st>>>(a);                // L2::128B prefetch
     } else {
       switch ((L + 31) / 32) {
-        case 1: apply_warp_v1<1><<<grid, 256, 0, st>>>(a); break;
-        case 2: apply_warp_v1<2><<<grid, 256, 0, st>>>(a); break;
-        case 3: apply_warp_v1<3><<<grid, 256, 0, st>>>(a); break;
-        case 4: apply_warp_v1<4><<<grid, 256, 0, st>>>(a); break;
-        case 5: apply_warp_v1<5><<<grid, 256, 0, st>>>(a); break;
-        case 6: apply_warp_v1<6><<<grid, 256, 0, st>>>(a); break;
-        case 7: apply_warp_v1<7><<<grid, 256, 0, st>>>(a); break;
-        case 8: apply_warp_v1<8><<<grid, 256, 0, st>>>(a); break;
-        default: apply_warp_loop<<<grid, 256, 0, st>>>(a); break;
+        case 1: apply_warp_v1<1><<<grid, tpb, 0, st>>>(a); break;
+        case 2: apply_warp_v1<2><<<grid, tpb, 0, st>>>(a); break;
+        case 3: apply_warp_v1<3><<<grid, tpb, 0, st>>>(a); break;
+        case 4: apply_warp_v1<4><<<grid, tpb, 0, st>>>(a); break;
+        case 5: apply_warp_v1<5><<<grid, tpb, 0, st>>>(a); break;
+        case 6: apply_warp_v1<6><<<grid, tpb, 0, st>>>(a); break;
+        case 7: apply_warp_v1<7><<<grid, tpb, 0, st>>>(a); break;
+        case 8: apply_warp_v1<8><<<grid, tpb, 0, st>>>(a); break;
+        default: apply_warp_loop<<<grid, tpb, 0, st>>>(a); break;
       }
     }
   }

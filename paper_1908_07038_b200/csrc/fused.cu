@@ -152,15 +152,15 @@ void fused_impl(uint64_t stencil, uint64_t plan, uint64_t src_field, uint64_t ds
   const int64_t m = t1 - t0;
   if (m <= 0) return;
   DeviceScope ds(s->device);
-  const unsigned grid = (unsigned)((m + 7) / 8);
+  const unsigned grid = (unsigned)((m + 1) / 2);  // 2 warps (targets) per block, like apply.cu
   cudaStream_t st = as_stream(stream);
   switch ((a.levels + 31) / 32) {
-    case 1: apply_fused<1><<<grid, 256, 0, st>>>(a); break;
-    case 2: apply_fused<2><<<grid, 256, 0, st>>>(a); break;
-    case 3: apply_fused<3><<<grid, 256, 0, st>>>(a); break;
-    case 4: apply_fused<4><<<grid, 256, 0, st>>>(a); break;
-    case 5: apply_fused<5><<<grid, 256, 0, st>>>(a); break;
-    default: apply_fused_loop<<<grid, 256, 0, st>>>(a); break;
+    case 1: apply_fused<1><<<grid, 64, 0, st>>>(a); break;
+    case 2: apply_fused<2><<<grid, 64, 0, st>>>(a); break;
+    case 3: apply_fused<3><<<grid, 64, 0, st>>>(a); break;
+    case 4: apply_fused<4><<<grid, 64, 0, st>>>(a); break;
+    case 5: apply_fused<5><<<grid, 64, 0, st>>>(a); break;
+    default: apply_fused_loop<<<grid, 64, 0, st>>>(a); break;
   }
   SG_CUDA_LAUNCH();
 }
