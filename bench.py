@@ -260,6 +260,44 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------------------
+def emulated_halo(sg, S, L, flush, parts=8, halo=2, partitioner="equal_regions", reps=5):
+    """The halo exchange of the N>1 step at one point of cfg4 (BASELINE configs[3]), emulated
+    on ONE GPU: every rank's field lives in this GPU's HBM and each rank's fused pull kernel
+    (pack + transfer + unpack in one pass over peer pointers) is timed on its own, with L2
+    flushed before every launch by an apply of the main workload.  On P GPUs the ranks run
+    concurrently and the peer reads cross NVLink, so the exchange time there is the max over
+    ranks of NVLink-bound pulls; here it is the max over ranks of HBM-bound pulls."""
+    from paper_1908_07038_b200.device import DeviceArray, Event
+    from paper_1908_07038_b200.partition import PARTITIONERS
+
+    dist = PARTITIONERS[partitioner](S, parts)
+    meshes = [sg.generate_mesh(S, dist, r, halo=halo, include_pole=True) for r in range(parts)]
+    plans = sg.run_ranks(parts, lambda ctx: sg.NodeColumns(meshes[ctx.rank], ctx).exchange_plan, devices=[0])
+    fields = [DeviceArray(m.nb_nodes, L, np.float64) for m in meshes]
+    info = [(d.ptr, d.pitch, d.device) for d in fields]
+    ms, nbytes = [], []
+    for r in range(parts):
+        plans[r].pull(fields[r], info)
+        t = []
+        for _ in range(reps):
+            flush()
+            e0, e1 = Event(0), Event(0)
+            e0.record()
+            plans[r].pull(fields[r], info)
+            e1.record()
+            t.append(Event.elapsed_ms(e0, e1))
+        ms.append(statistics.median(t))
+        nbytes.append(sum(len(v) for v in plans[r].recv.values()) * L * 8)
+    for d in fields:
+        d.close()
+    worst = max(ms)
+    return {"bytes_per_exchange": int(sum(nbytes)), "ms": worst, "GB_per_s": sum(nbytes) / (worst * 1e-3) / 1e9,
+            "worst_rank_bytes": int(nbytes[int(np.argmax(ms))]), "per_rank_ms": [round(x, 4) for x in ms],
+            "scope": f"cfg4 point O1280, {L} lev, halo {halo}, {partitioner} P={parts}, EMULATED on one GPU: "
+                     "all ranks' fields in this GPU's HBM, each rank's fused pull kernel timed alone with L2 "
+                     "flushed; ms = max over ranks. Not NVLink (needs >1 GPU)"}
+
+
 def run_single(args):
     import paper_1908_07038_b200 as sg
     from paper_1908_07038_b200.device import DeviceArray, Event, PinnedArray
@@ -342,6 +380,10 @@ def run_single(args):
     clocks.active = False
     clocks.stop()
 
+    halo = None
+    if args.config == "cfg3" and not args.no_halo:
+        halo = emulated_halo(sg, S, L, lambda: sg.apply_remap_device(w, dsrc, ddst, variant=args.variant))
+
     # ---- CPU baseline: the reference's apply (oracle port), 1 thread, same workload; its
     # result (last field) is also the parity check of the device and e2e outputs ------------
     cpu = None
@@ -391,6 +433,7 @@ def run_single(args):
                                      "target rows runs concurrently in the other direction"},
                 "mode": args.e2e_mode, "chunks": args.e2e_chunks, "direct_period": args.e2e_period,
                 "auto_trials_s": {k: [round(x, 4) for x in v] for k, v in w.__dict__.get("_auto_s", {}).items()}},
+        "halo": halo,
         "cpu_baseline": cpu,
         "gpu_launches": args.steps,
         "parity": parity,
@@ -571,6 +614,7 @@ def main():
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     ap.add_argument("--variant", type=int, default=0, help="apply kernel: 0 default, 1 warp LDG, 2 TMA bulk")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-halo", action="store_true", help="N=1: skip the one-GPU emulation of the cfg4 halo exchange")
     ap.add_argument("--e2e-chunks", type=int, default=0, help="host-execute pipeline depth (0 = auto)")
     ap.add_argument("--e2e-period", type=int, default=-1,
                     help="compact e2e: copy every n-th chunk directly instead of packing (-1 = library default)")
