@@ -382,7 +382,10 @@ def run_single(args):
 
     halo = None
     if args.config == "cfg3" and not args.no_halo:
-        halo = emulated_halo(sg, S, L, lambda: sg.apply_remap_device(w, dsrc, ddst, variant=args.variant))
+        try:  # auxiliary evidence: never lose the bench line over it
+            halo = emulated_halo(sg, S, L, lambda: sg.apply_remap_device(w, dsrc, ddst, variant=args.variant))
+        except Exception as exc:  # noqa: BLE001
+            halo = {"error": f"{type(exc).__name__}: {exc}"}
 
     # ---- CPU baseline: the reference's apply (oracle port), 1 thread, same workload; its
     # result (last field) is also the parity check of the device and e2e outputs ------------
