@@ -1,0 +1,53 @@
+"""The bench JSON contract, checked on CPU against the committed line of the last B200 run
+(profiles/r01_bench_cfg3.json, written by ``python bench.py``): every key the driver and the
+judge read, with consistent values."""
+import json
+import os
+
+from conftest import ROOT
+
+
+def load_line():
+    with open(os.path.join(ROOT, "profiles", "r01_bench_cfg3.json")) as fh:
+        return json.load(fh)
+
+
+def test_top_level_keys_and_types():
+    d = load_line()
+    with open(os.path.join(ROOT, "BASELINE.json")) as fh:
+        baseline = json.load(fh)
+    assert d["metric"] == baseline["metric"]
+    for k in ("value", "ms_per_step"):
+        assert isinstance(d[k], float) and d[k] > 0
+    assert d["unit"] == "Gpts·lev/s" and d["n_gpus"] == 1 and d["higher_is_better"] is True
+    assert d["steps"] >= 1 and d["warmup"] >= 3 and d["scaling"] in ("weak", "strong")
+    assert d["vs_baseline"] is None  # BASELINE.md publishes no number for this metric
+    assert d["dtype"] == "f64" and "synthetic" in d["data"]
+    assert "workload" in d["config"] and "model" not in d["config"]
+    assert d["gpu_launches"] == d["steps"]  # one apply launch per step
+    # value is units / time: targets x levels x fields per step
+    units = d["config"]["targets"] * d["config"]["levels"] * d["config"]["fields"]
+    assert abs(units / (d["ms_per_step"] * 1e-3) / 1e9 - d["value"]) / d["value"] < 1e-9
+
+
+def test_roofline_object():
+    r = load_line()["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s"
+    assert abs(r["achieved"] / r["peak"] - r["frac"]) < 1e-12
+    # achieved = algorithmic bytes per launch / measured kernel time
+    assert abs(r["algorithmic_bytes_per_launch"] / (r["kernel_ms"] * 1e-3) / 1e9 - r["achieved"]) / r["achieved"] < 1e-9
+    assert r["traffic"] >= r["algorithmic_bytes_per_launch"]  # ncu DRAM bytes include over-fetch
+
+
+def test_e2e_cpu_baseline_clocks_parity():
+    d = load_line()
+    e = d["e2e"]
+    assert e["unit"] == d["unit"] and 0 < e["value"] < d["value"]
+    assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert e["h2d_bytes_per_step"] <= e["input_bytes_per_step"]
+    c = d["cpu_baseline"]
+    assert c["kind"] in ("port", "reference") and c["cores"] >= 1 and c["unit"] == d["unit"] and c["sample"]
+    k = d["clocks"]
+    assert k["sm_mhz"] > 0.8 * k["sm_max_mhz"]
+    assert not {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(k["reasons"])
+    assert d["parity"]["checked"] and d["parity"]["device_bitwise_vs_cpu"] and d["parity"]["e2e_bitwise_vs_cpu"]
