@@ -559,19 +559,27 @@ def run_multi(args):
     send_bytes = float(sum(len(v) for v in fs.exchange_plan.send.values()) * L * 8)
     hmax = allreduce([halo_ms], dist.ReduceOp.MAX)[0]
     hsum = allreduce([send_bytes], dist.ReduceOp.SUM)[0]
-    # e2e: owned source rows host -> device, exchange + apply, target rows device -> host
+    # e2e: the owned source rows this step needs (read by the rank's own stencils or sent to a
+    # peer) host -> device, exchange + apply, target rows device -> host.  The pinned source is
+    # mapped, so one kernel pulls the row runs over PCIe (sg_field_h2d_row_runs).
+    from paper_1908_07038_b200.functionspace import row_runs
+
+    nd = w.nodes[w.nodes < n_owned].ravel()
+    sends = [np.asarray(v, np.int64) for v in fs.exchange_plan.send.values()]
+    runs = row_runs(np.concatenate([nd] + sends))
+    h2d_rows = int(runs[:, 1].sum()) if len(runs) else 0
     ctx.barrier()
     e2e_steps = max(3, min(args.steps, 10))
     tt = time.perf_counter()
     for _ in range(e2e_steps):
-        f.device.upload_rows(0, hsrc.array[:n_owned], stream=run.main.stream, sync=False)
+        f.device.upload_row_runs(hsrc.array, runs, stream=run.main.stream, sync=False)
         run.step()
         tf.device.download(hdst.array, stream=run.main.stream, sync=False)
         run.synchronize()
     my_e2e = (time.perf_counter() - tt) / e2e_steps
     ctx.barrier()
     e2e_max = allreduce([my_e2e], dist.ReduceOp.MAX)[0]
-    h2d = allreduce([float(n_owned * L * 8)], dist.ReduceOp.SUM)[0]
+    h2d = allreduce([float(h2d_rows * L * 8)], dist.ReduceOp.SUM)[0]
     d2h = allreduce([float(m * L * 8)], dist.ReduceOp.SUM)[0]
     if clocks:
         clocks.active = False

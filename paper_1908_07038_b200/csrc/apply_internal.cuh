@@ -35,5 +35,13 @@ ApplyArgs make_args(const Stencil* s, const FieldPairs& p, int f0, int64_t t0, i
 // Chooses and launches the apply kernel for `variant`.
 void launch_apply(ApplyArgs a, int variant, cudaStream_t st);
 
+// GPU gather of row pieces out of pinned, mapped host memory (execute_host.cu): piece p =
+// (first host row, rows) -> device rows from pdst[p]; rows of `levels` doubles, dense.
+// cp.async.bulk copies through a shared-memory ring; pieces of <= gather_piece_rows rows.
+int gather_piece_rows(int levels);
+bool gather_fits(int levels);
+void launch_gather_tma(const double* host, int64_t host_rows, const int2* pieces, const int64_t* pdst, double* out,
+                       int64_t p0, int64_t p1, int levels, int piece_rows, cudaStream_t st);
+
 }  // namespace detail
 }  // namespace sg

@@ -184,6 +184,12 @@ void launch_gather_rows(const double* host, const int32_t* gsrc, double* out, in
 
 int gather_slot(int levels, int piece_rows) { return (piece_rows * levels + 2 + 1) & ~1; }  // doubles, 16-B multiple
 
+}  // namespace
+
+namespace detail {
+int gather_piece_rows(int levels) { return std::max(1, kGatherPieceDoubles / levels); }
+bool gather_fits(int levels) { return (size_t)levels * 8 + 16 <= (size_t)kGatherPieceDoubles * 8; }
+
 void launch_gather_tma(const double* host, int64_t host_rows, const int2* pieces, const int64_t* pdst, double* out,
                        int64_t p0, int64_t p1, int levels, int piece_rows, cudaStream_t st) {
   if (p1 <= p0) return;
@@ -195,10 +201,13 @@ void launch_gather_tma(const double* host, int64_t host_rows, const int2* pieces
   gather_tma<<<grid, 160, smem, st>>>(host, host_rows, pieces, pdst, out, p0, p1, levels, slot);
   SG_CUDA_LAUNCH();
 }
+}  // namespace detail
+
+namespace {
 
 // Pieces of the referenced runs for `levels` (rebuilt when the level count changes).
 void build_pieces(int device, HostPlan* hp, int levels) {
-  const int prows = std::max(1, kGatherPieceDoubles / levels);
+  const int prows = gather_piece_rows(levels);
   if (hp->piece_levels == levels && hp->piece_rows == prows) return;
   std::vector<int2> pcs;
   std::vector<int64_t> dst;
@@ -431,7 +440,7 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
   const bool compact = (flags & 1) != 0 || gather;
   // TMA ring stage must hold at least one 16-B aligned row superset; flags bit 3 forces the
   // warp-per-row gather (kept for comparison)
-  const bool tma_gather = gather && !(flags & 8) && (size_t)p.levels * 8 + 16 <= (size_t)kGatherPieceDoubles * 8;
+  const bool tma_gather = gather && !(flags & 8) && gather_fits(p.levels);
   std::vector<const double*> gsrc_host(gather ? nfields : 0);
   for (int f = 0; f < (int)gsrc_host.size(); ++f)
     gsrc_host[f] = static_cast<const double*>(mapped(host_src[f], "gather"));

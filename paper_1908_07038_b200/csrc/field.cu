@@ -10,6 +10,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "apply_internal.cuh"
 #include "cuda_util.cuh"
 
 using namespace sg;
@@ -197,6 +198,31 @@ int32_t sg_field_h2d_row_runs(uint64_t field, const int64_t* runs, int64_t nruns
                       cudaPointerGetAttributes(&at, host) == cudaSuccess && at.type == cudaMemoryTypeHost &&
                       at.devicePointer != nullptr;
   cudaGetLastError();
+  if (mapped && f->itemsize * f->levels % 8 == 0 && detail::gather_fits((int)(row_bytes / 8))) {
+    // rows as doubles: bulk-copy pieces (cp.async.bulk, the e2e gather) into the same rows
+    const int words = (int)(row_bytes / 8), prows = detail::gather_piece_rows(words);
+    std::vector<int2> pcs;
+    std::vector<int64_t> dst;
+    for (int64_t r = 0; r < nruns; ++r)
+      for (int64_t q = 0; q < runs[2 * r + 1]; q += prows) {
+        pcs.push_back(make_int2((int)(runs[2 * r] + q), (int)std::min<int64_t>(prows, runs[2 * r + 1] - q)));
+        dst.push_back(runs[2 * r] + q);
+      }
+    thread_local DevBuf sp, sd;
+    if (sp.bytes < pcs.size() * sizeof(int2) || sp.device != f->device)
+      sp.alloc(f->device, std::max<size_t>(pcs.size() * sizeof(int2), 4096));
+    if (sd.bytes < dst.size() * sizeof(int64_t) || sd.device != f->device)
+      sd.alloc(f->device, std::max<size_t>(dst.size() * sizeof(int64_t), 4096));
+    cudaStream_t st = as_stream(stream);
+    if (!pcs.empty()) {
+      SG_CUDA(cudaMemcpyAsync(sp.ptr, pcs.data(), pcs.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+      SG_CUDA(cudaMemcpyAsync(sd.ptr, dst.data(), dst.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+      detail::launch_gather_tma(static_cast<const double*>(at.devicePointer), f->npts, sp.as<int2>(), sd.as<int64_t>(),
+                                f->buf.as<double>(), 0, (int64_t)pcs.size(), words, prows, st);
+    }
+    SG_CUDA(cudaStreamSynchronize(st));  // the piece lists are reused by the next call on this thread
+    return SG_OK;
+  }
   if (mapped) {
     thread_local DevBuf scratch;
     const size_t need = (size_t)nruns * 2 * sizeof(int64_t);

@@ -37,6 +37,17 @@ _TAG_PLAN_REQUEST = 101  # functionspace.py:24
 _TAG_EXCHANGE = 102  # functionspace.py:25
 
 
+def row_runs(rows: np.ndarray) -> np.ndarray:
+    """(row0, nrows) runs, ascending and maximal, covering the distinct values of ``rows``."""
+    rows = np.unique(np.asarray(rows, np.int64))
+    if len(rows) == 0:
+        return np.empty((0, 2), np.int64)
+    cut = np.flatnonzero(np.diff(rows) != 1) + 1
+    starts = rows[np.concatenate([[0], cut])]
+    ends = rows[np.concatenate([cut - 1, [len(rows) - 1]])] + 1
+    return np.stack([starts, ends - starts], axis=1).astype(np.int64)
+
+
 @dataclass
 class HaloExchangePlan:
     """Per peer: owned local rows to send (requester's order) and ghost local rows to
@@ -53,15 +64,8 @@ class HaloExchangePlan:
     def send_runs(self) -> np.ndarray:
         """(row0, nrows) runs covering the union of the send lists, ascending."""
         if self._send_runs is None:
-            rows = np.unique(np.concatenate([np.asarray(v, np.int64) for v in self.send.values()])) \
-                if self.send else np.empty(0, np.int64)
-            if len(rows) == 0:
-                self._send_runs = np.empty((0, 2), np.int64)
-            else:
-                cut = np.flatnonzero(np.diff(rows) != 1) + 1
-                starts = rows[np.concatenate([[0], cut])]
-                ends = rows[np.concatenate([cut - 1, [len(rows) - 1]])] + 1
-                self._send_runs = np.stack([starts, ends - starts], axis=1).astype(np.int64)
+            self._send_runs = row_runs(np.concatenate([np.asarray(v, np.int64) for v in self.send.values()])
+                                       if self.send else np.empty(0, np.int64))
         return self._send_runs
 
     @property
