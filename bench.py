@@ -142,14 +142,23 @@ def fill_smooth(out: np.ndarray, xyz: np.ndarray, field_index: int, rows=None) -
     """Synthetic analytic field into ``out`` (rows ``rows`` or all), in row chunks."""
     from paper_1908_07038_b200.analytic import HARMONICS, spherical_harmonic
 
+    from concurrent.futures import ThreadPoolExecutor
+
     L = out.shape[1]
     cols = [(field_index * L + k) % 25 for k in range(L)]
     fac = 1.0 + np.arange(L) / L
     idx = np.arange(len(xyz)) if rows is None else rows
-    for s in range(0, len(idx), 262144):
-        r = idx[s:s + 262144]
+
+    def chunk(s):  # numpy releases the GIL in these ufuncs and copies
+        r = slice(s, min(s + 65536, len(idx))) if rows is None else idx[s:s + 65536]
         basis = np.stack([spherical_harmonic(l, m, xyz[r]) for l, m in HARMONICS], axis=1)
-        out[r] = basis[:, cols] * fac
+        if rows is None:
+            np.multiply(basis[:, cols], fac, out=out[r])
+        else:
+            out[r] = basis[:, cols] * fac
+
+    with ThreadPoolExecutor(min(16, os.cpu_count() or 1)) as ex:
+        list(ex.map(chunk, range(0, len(idx), 65536)))
 
 
 def setup_remap(sg, source, target, nparts, rank, ctx, method="fe", partitioner="blocks"):
