@@ -67,3 +67,26 @@ def test_ipc_pull_exchange_processes(gpu, world):
     for p in procs:
         p.join(timeout=60)
     assert all(o[1] and o[2] for o in out), out
+
+
+@pytest.mark.parametrize("extra", [[], ["--fused"]])
+def test_bench_torchrun_two_processes(gpu, extra):
+    """The driver's N>1 launch line (torch.distributed.run, one process per rank) end to end on
+    the one GPU of the test box: bench.py --gpus 2 with the CUDA-IPC transport on cfg2 (equal
+    regions, halo 2) prints one JSON line with the multi-GPU keys (halo, roofline, e2e)."""
+    import json
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--transport", "ipc", "--config", "cfg2"] + extra
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["scaling"] == "strong"
+    assert line["halo"]["bytes_per_exchange"] > 0 and line["roofline"]["bound"] == "hbm"
+    assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
+    assert line["config"]["fused"] == ("--fused" in extra)
