@@ -40,6 +40,9 @@ CONFIGS = {
     "cfg1": ("O32", "O16", 10, 1),
     # structured bilinear: no reference method (parity vs oracle.bilinear_stencil only)
     "cfg5": ("O2560", "O1280", 137, 1, "bilinear"),
+    # the finite-element method at cfg5's size (stencils bit-exact vs the scaled oracle,
+    # profiles/r01_scale_parity_o2560.json)
+    "cfg5fe": ("O2560", "O1280", 137, 1),
 }
 
 
