@@ -141,9 +141,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def fill_smooth(out: np.ndarray, xyz: np.ndarray, field_index: int, rows=None) -> None:
-    """Synthetic analytic field into ``out`` (rows ``rows`` or all), in row chunks."""
-    from paper_1908_07038_b200.analytic import HARMONICS, spherical_harmonic
+HARMONICS = [(l, m) for l in range(5) for m in range(-l, l + 1)]  # the 25 real Y_l^m, l <= 4
+
+
+def fill_smooth(out: np.ndarray, xyz: np.ndarray, field_index: int, rows=None, harmonic=None) -> None:
+    """Synthetic analytic field into ``out`` (rows ``rows`` or all), in row chunks.
+    ``harmonic`` is the ``spherical_harmonic(l, m, xyz)`` to use (default: this package's;
+    the reference arm passes the reference's own, analytic.py:35)."""
+    if harmonic is None:
+        from paper_1908_07038_b200.analytic import spherical_harmonic as harmonic
 
     from concurrent.futures import ThreadPoolExecutor
 
@@ -154,7 +160,7 @@ def fill_smooth(out: np.ndarray, xyz: np.ndarray, field_index: int, rows=None) -
 
     def chunk(s):  # numpy releases the GIL in these ufuncs and copies
         r = slice(s, min(s + 65536, len(idx))) if rows is None else idx[s:s + 65536]
-        basis = np.stack([spherical_harmonic(l, m, xyz[r]) for l, m in HARMONICS], axis=1)
+        basis = np.stack([harmonic(l, m, xyz[r]) for l, m in HARMONICS], axis=1)
         if rows is None:
             np.multiply(basis[:, cols], fac, out=out[r])
         else:
@@ -162,6 +168,17 @@ def fill_smooth(out: np.ndarray, xyz: np.ndarray, field_index: int, rows=None) -
 
     with ThreadPoolExecutor(min(16, os.cpu_count() or 1)) as ex:
         list(ex.map(chunk, range(0, len(idx), 65536)))
+
+
+def workload_config(source, target, L, F, method, m, n, nparts=1, partitioner="blocks"):
+    """The ``config`` dict both arms print (identical for the same workload)."""
+    kind = "structured-bilinear" if method == "bilinear" else "FE"
+    nbytes = (n + m) * L * 8 * F
+    return {"workload": f"{source}->{target} {kind} remap apply, {L} levels x {F} field(s), P={nparts}",
+            "levels": L, "fields": F, "targets": m, "source_nodes": n,
+            "parallelism": "single device" if nparts == 1 else f"domain decomposition x{nparts} ({partitioner})",
+            "l2": (f"inputs {nbytes / 1e9:.1f} GB > 126 MB L2 (no flush needed)" if nbytes > 126e6 else
+                   f"inputs {nbytes / 1e6:.1f} MB fit in the 126 MB L2 (L2-resident timing)")}
 
 
 def setup_remap(sg, source, target, nparts, rank, ctx, method="fe", partitioner="blocks"):
@@ -207,65 +224,121 @@ def algorithmic_bytes(U, m, L, F, k=3):
 
 
 # ------------------------------------------------------------------------------------------
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def loaded_repo_libraries():
+    """Shared objects under this repo mapped into the process (evidence of what ran)."""
+    try:
+        with open("/proc/self/maps") as fh:
+            paths = {ln.split()[-1] for ln in fh if ln.rstrip().endswith(".so")}
+    except OSError:
+        return None
+    return sorted(os.path.relpath(p, ROOT) for p in paths if p.startswith(ROOT + os.sep))
+
+
+def import_reference():
+    """The unmodified reference package installed into baseline/_ref by
+    tools/install_reference.sh (pip --target of /root/reference/pkg).  Nothing of this repo's
+    package is imported on this path."""
+    if not os.path.isdir(os.path.join(REF_DIR, "spheregrid")):
+        return None, f"reference not installed: {REF_DIR}/spheregrid missing (run tools/install_reference.sh)"
+    sys.path.insert(0, REF_DIR)
+    import spheregrid as R
+
+    if not os.path.abspath(R.__file__).startswith(REF_DIR):
+        return None, f"spheregrid resolved to {R.__file__}, not baseline/_ref"
+    return R, None
+
+
 def run_reference(args):
-    """--impl reference: the reference's CPU apply on this host, all threads, rank 0 only."""
+    """--impl reference: the reference's OWN code path on this host, rank 0 only.
+
+    Grids, latitudes, mesh, function spaces and fields come from the unmodified reference
+    (``grid_from_name`` gaussian.py:37-62 / grid.py:127-145, ``generate_mesh`` mesh.py:229-338,
+    ``NodeColumns`` / ``StructuredColumns`` / ``create_field``), and the timed step is the
+    reference's ``apply_remap(weights, source_field, target_field)`` (interp.py:206-228),
+    as the reference runs it: numpy on one core.  Only the stencils do not come from the
+    reference's ``build_remap`` (its per-target Python loop takes ~2 h at O1280->O640,
+    SURVEY.md §8(d)): they come from the oracle's restatement of the same search
+    (``oracle.locate_kdtree``: scipy cKDTree k=8/32 candidates scored with the reference's
+    arithmetic, interp.py:90-117; batched dgesv weights, interp.py:61-71), wrapped in the
+    reference's own ``InterpolationWeights``.  libsgb200 is never loaded."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import paper_1908_07038_b200 as sg
-
     source, target, L, F, method = config(args.config)
-    t0 = time.time()
-    # stencils from the scaled oracle — the reference's own algorithm (scipy cKDTree k=8/32
-    # candidates, interp.py:90-117, scored in C with its arithmetic; batched dgesv weights),
-    # not the device build: nothing of the B200 engine runs in this arm
+    R, why = import_reference()
+    if R is None:
+        print(json.dumps({"impl": "reference", "unavailable": why}), flush=True)
+        return
     from oracle import oracle as O
 
-    S, T = sg.grid_from_name(source), sg.grid_from_name(target)
-    mesh = sg.generate_mesh(S, sg.blocks_partition(S, 1), 0, halo=2, include_pole=True)
+    t0 = time.time()
+    S, T = R.grid_from_name(source), R.grid_from_name(target)
+    dist = R.blocks_partition(S, 1)
+    mesh = R.generate_mesh(S, dist, 0, halo=2, include_pole=True)  # cli.py:131
+    fs = R.NodeColumns(mesh, None)
+    tdist = R.blocks_partition(T, 1)  # == matching_partition at P=1 (every target in part 0)
+    tfs = R.StructuredColumns(T, tdist, 0)
+    log(f"reference grids + mesh {time.time() - t0:.1f}s ({mesh.nb_nodes} nodes)")
     conn = mesh.element_connectivity
     txyz = T.xyz()
+    stencils = "oracle.locate_kdtree + batched dgesv (reference build_remap takes ~2 h here)"
     if method == "bilinear":
-        gn, weights, _ = O.bilinear_stencil(S.latitudes, S.nlons, T.lonlats(), True)
-        nodes = gn  # serial mesh: local row == global id (owned grid points, then the poles)
+        nodes, weights, _ = O.bilinear_stencil(S.latitudes, S.nlons, T.lonlats(), True)
+        stencils = "oracle.bilinear_stencil (no reference method)"
+    elif T.npts <= 20000:  # small configs: the reference's own build_remap (~4 ms per target)
+        rw = R.build_remap(fs, T, tdist)
+        nodes, weights = rw.nodes, rw.weights
+        stencils = "reference build_remap (interp.py:154-203)"
     else:
         elem, nodes = O.locate_kdtree(mesh.node_xyz, conn.offsets, conn.indices, txyz)
         if (elem < 0).any():
             raise SystemExit("reference arm: target not located")
         weights = O.barycentric_weights_batched(mesh.node_xyz, nodes, txyz)
-    w_len = len(nodes)
-    srcs = []
+    m = len(nodes)
+    W = R.InterpolationWeights(target_global=tfs.local_points, nodes=np.ascontiguousarray(nodes, np.int64),
+                               weights=np.ascontiguousarray(weights), fallback=np.zeros(m, bool),
+                               source_nnodes=mesh.nb_nodes, source_global=mesh.node_global)
+    from spheregrid.analytic import spherical_harmonic as ref_harmonic
+
+    srcs, dsts = [], []
     for f in range(F):
-        a = np.empty((mesh.nb_nodes, L))
-        fill_smooth(a, mesh.node_xyz, f)
-        srcs.append(a)
-    out = np.empty((w_len, L))
-    nthreads = os.cpu_count() or 1
-    log(f"reference setup {time.time() - t0:.1f}s, {nthreads} threads")
+        sf = fs.create_field(f"src{f}", levels=L)
+        fill_smooth(sf.host, mesh.node_xyz, f, harmonic=ref_harmonic)
+        srcs.append(sf)
+        dsts.append(tfs.create_field(f"dst{f}", levels=L))
+    log(f"reference setup {time.time() - t0:.1f}s")
     for _ in range(args.warmup):
-        for a in srcs:
-            cpu_apply(nodes, weights, a, out, nthreads)
+        for sf, df in zip(srcs, dsts):
+            R.apply_remap(W, sf, df)
     times = []
     for _ in range(args.steps):
         t = time.perf_counter()
-        for a in srcs:
-            cpu_apply(nodes, weights, a, out, nthreads)
+        for sf, df in zip(srcs, dsts):
+            R.apply_remap(W, sf, df)
         times.append(time.perf_counter() - t)
-    units = w_len * L * F
+    units = m * L * F
     ms = 1e3 * sum(times) / len(times)
     value = units / (ms * 1e-3) / 1e9
     line = {
-        "metric": metric_name(source, target, method, L), "value": value, "unit": "Gpts·lev/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
+        "metric": metric_name(source, target, method, L), "value": value, "unit": "Gpts·lev/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
         "impl": "reference",
-        "config": {"workload": f"{source}->{target} {'structured-bilinear' if method == 'bilinear' else 'FE'} remap "
-                               f"apply, {L} levels x {F} field(s), P=1",
-                   "levels": L, "fields": F, "targets": w_len, "source_nodes": mesh.nb_nodes,
-                   "stencils": "oracle.locate_kdtree (reference algorithm, scipy cKDTree) — no device code"},
-        "cpu_baseline": {"value": value, "unit": "Gpts·lev/s", "cores": nthreads, "kind": "port",
-                         "sample": f"full {source}->{target} apply per step (oracle port of interp.py:219-223, "
-                                   f"numpy, {nthreads} threads over 16k-target chunks)"},
+        "config": workload_config(source, target, L, F, method, m, mesh.nb_nodes, args.gpus, args.partitioner),
+        "reference": {"package": os.path.relpath(os.path.dirname(R.__file__), ROOT), "version": R.__version__,
+                      "timed": "spheregrid.apply_remap(InterpolationWeights, Field, Field) per field (interp.py:206-228)",
+                      "built_by_reference": "grid_from_name, generate_mesh, NodeColumns, StructuredColumns, "
+                                            "create_field, InterpolationWeights, analytic.spherical_harmonic",
+                      "stencils": stencils,
+                      "setup_s": round(time.time() - t0, 1),
+                      "repo_libraries_loaded": loaded_repo_libraries(),
+                      "product_imported": "paper_1908_07038_b200" in sys.modules},
+        "cpu_baseline": {"value": value, "unit": "Gpts·lev/s", "cores": 1, "kind": "reference",
+                         "sample": f"full {source}->{target} apply x{F} field(s) per step: the reference's own "
+                                   "apply_remap (numpy, single-threaded as the reference runs it)"},
         "e2e": {"value": value, "unit": "Gpts·lev/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -399,22 +472,39 @@ def run_single(args):
         except Exception as exc:  # noqa: BLE001
             halo = {"error": f"{type(exc).__name__}: {exc}"}
 
-    # ---- CPU baseline: the reference's apply (oracle port), 1 thread, same workload; its
-    # result (last field) is also the parity check of the device and e2e outputs ------------
+    # ---- CPU baseline, 1 core, same workload: the reference's own apply_remap (baseline/_ref)
+    # on the same stencils and host arrays when installed, else the oracle port of
+    # interp.py:219-223; its result (last field) is also the parity check of the device and
+    # e2e outputs ------------------------------------------------------------------------
     cpu = None
     parity = {"checked": False}
     if not args.no_cpu_baseline:
         out = np.empty((m, L))
+        R, _ = import_reference()
+        if R is not None:
+            RW = R.InterpolationWeights(target_global=np.arange(m, dtype=np.int64), nodes=w.nodes.astype(np.int64),
+                                        weights=w.weights, fallback=np.zeros(m, bool), source_nnodes=n)
+            rsrc = [R.Field(name=f"src{f}", shape=(n, L), kind=R.Kind.REAL64, host=hsrc[f].array) for f in range(F)]
+            rdst = R.Field(name="dst", shape=(m, L), kind=R.Kind.REAL64, host=out)
+
+            def cpu_step():
+                for f in range(F):
+                    R.apply_remap(RW, rsrc[f], rdst)
+            kind, what = "reference", "the reference's own apply_remap (baseline/_ref, interp.py:206-228)"
+        else:
+            def cpu_step():
+                for f in range(F):
+                    cpu_apply(w.nodes, w.weights, hsrc[f].array, out, 1)
+            kind, what = "port", "the oracle port of interp.py:219-223 (baseline/_ref not installed)"
         times = []
         for _ in range(2):
             tt = time.perf_counter()
-            for f in range(F):
-                cpu_apply(w.nodes, w.weights, hsrc[f].array, out, 1)
+            cpu_step()
             times.append(time.perf_counter() - tt)
-        cpu = {"value": units / min(times) / 1e9, "unit": "Gpts·lev/s", "cores": 1, "kind": "port",
-               "sample": f"full {source}->{target} apply x{F} field(s), best of 2 (numpy expression of "
-                         f"interp.py:219-223, single-threaded like the reference)"}
-        parity = {"checked": True,
+        cpu = {"value": units / min(times) / 1e9, "unit": "Gpts·lev/s", "cores": 1, "kind": kind,
+               "sample": f"full {source}->{target} apply x{F} field(s), best of 2: {what}, numpy single-threaded "
+                         "as the reference runs it"}
+        parity = {"checked": True, "against": kind,
                   "device_bitwise_vs_cpu": bool(np.array_equal(device_out.view(np.uint64), out.view(np.uint64))),
                   "e2e_bitwise_vs_cpu": bool(np.array_equal(hdst[F - 1].array.view(np.uint64), out.view(np.uint64)))}
 
@@ -427,11 +517,8 @@ def run_single(args):
         "metric": metric_name(source, target, method, L), "value": value, "unit": "Gpts·lev/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "ms_per_step_median": ms_median, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
-        "config": {"workload": f"{source}->{target} {'structured-bilinear' if method == 'bilinear' else 'FE'} remap "
-                               f"apply, {L} levels x {F} field(s), P=1",
-                   "levels": L, "fields": F, "targets": m, "source_nodes": n, "distinct_sources": U,
-                   "parallelism": "single GPU", "l2": f"inputs {(n + m) * L * 8 * F / 1e9:.1f} GB > 126 MB L2 (no flush needed)",
-                   "variant": args.variant},
+        "config": workload_config(source, target, L, F, method, m, n),
+        "kernel": {"variant": args.variant, "distinct_sources": U},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(args.config), "algorithmic_bytes_per_launch": B,
                      "kernel_ms": kern_ms, "peak_source": peak_src},
@@ -448,7 +535,7 @@ def run_single(args):
                                      "target rows runs concurrently in the other direction"},
                 "mode": args.e2e_mode, "chunks": args.e2e_chunks, "direct_period": args.e2e_period,
                 "auto_trials_s": {k: [round(x, 4) for x in v] for k, v in w.__dict__.get("_auto_s", {}).items()}},
-        "halo": halo,
+        "halo_emulated": halo,
         "cpu_baseline": cpu,
         "gpu_launches": args.steps,
         "parity": parity,
@@ -491,16 +578,9 @@ def run_multi(args):
     hdst = PinnedArray((m, L))
     f = sg.Field(name="src", shape=(n, L), kind=sg.Kind.REAL64, host=hsrc.array).allocate_device()
     tf = sg.Field(name="dst", shape=(m, L), kind=sg.Kind.REAL64, host=hdst.array).allocate_device()
-    try:
-        run = DistributedRemap(fs, w, ctx, f.device, tf.device, variant=args.variant, fused=args.fused)
-        run.step()
-        run.synchronize()
-    except Exception as exc:  # noqa: BLE001 - keep the measurement alive on a broken NCCL setup
-        if args.transport != "nccl":
-            raise
-        log(f"rank {rank}: NCCL path failed ({exc}); falling back to the CUDA-IPC transport")
-        args.transport = ctx.transport = "ipc"
-        run = DistributedRemap(fs, w, ctx, f.device, tf.device, variant=args.variant, fused=args.fused)
+    run = DistributedRemap(fs, w, ctx, f.device, tf.device, variant=args.variant, fused=args.fused)
+    run.step()
+    run.synchronize()
     log(f"rank {rank}: setup {time.time() - t0:.1f}s, {n} nodes ({n_owned} owned), {m} targets, "
         f"interior targets {run.n_interior}, {sum(len(v) for v in fs.exchange_plan.recv.values())} ghosts")
     for _ in range(args.warmup):
@@ -596,23 +676,103 @@ def run_multi(args):
     if clocks:
         clocks.active = False
         clocks.stop()
+
+    # ---- parity: this rank's exchanged source rows and its target rows, bitwise, against a
+    # single-process recomputation: the synthetic field evaluated on EVERY local row (the
+    # ghosts' owners evaluate the same function at the same coordinates), then the oracle's
+    # apply (interp.py:219-223) on this rank's stencils ------------------------------------
+    from oracle import oracle as O
+
+    exp_src = np.empty((n, L))
+    fill_smooth(exp_src, mesh.node_xyz, 0)
+    src_ok = bool(np.array_equal(f.device.to_numpy().view(np.uint64), exp_src.view(np.uint64)))
+    dst_ok = bool(np.array_equal(tf.device.to_numpy().view(np.uint64),
+                                 O.apply_remap_k(w.nodes, w.weights, exp_src).view(np.uint64)))
+    e2e_ok = bool(np.array_equal(hdst.array.view(np.uint64), tf.device.to_numpy().view(np.uint64)))
+    oks = allreduce([float(src_ok), float(dst_ok), float(e2e_ok)], dist.ReduceOp.MIN)
+    parity = {"checked": True, "source_rows_bitwise": oks[0] == 1.0, "target_rows_bitwise": oks[1] == 1.0,
+              "e2e_target_rows_bitwise": oks[2] == 1.0, "targets_checked": int(msum),
+              "against": "per rank: analytic field on every local row (owned + ghost) and the oracle apply "
+                         "(interp.py:219-223) on the rank's own stencils"}
+    comm = {"transport": args.transport, "transport_fallback": None}
+    if args.transport == "nccl":
+        info = ctx.comm_info()
+        nr = allreduce([float(info["nranks"])], dist.ReduceOp.MIN)[0]
+        comm.update({"nccl_nranks": int(nr), "nccl_version": info["nccl_version"],
+                     "rank0_cu_device": info["device"]})
+
+    # ---- cfg4 (BASELINE configs[3]): NodeColumns halo exchange of the O1280 source at halo
+    # widths 1..3, every rank at once, device timing, max over ranks --------------------------
+    sweep = []
+    if not args.no_halo_sweep:
+        from paper_1908_07038_b200.device import DeviceArray, Stream
+        from paper_1908_07038_b200.partition import PARTITIONERS
+
+        dist_s = PARTITIONERS[args.partitioner](S, world)
+        hs = Stream(local)
+        for h in (1, 2, 3):
+            mh = mesh if h == 2 else sg.generate_mesh(S, dist_s, rank, halo=h, include_pole=True)
+            plan = sg.NodeColumns(mh, ctx).exchange_plan
+            d = DeviceArray(mh.nb_nodes, L, np.float64, local)
+            vals = mh.node_global[:, None].astype(np.float64) + np.arange(L)[None, :] / L
+            init = np.where(mh.node_ghost[:, None], -1.0, vals)
+            d.upload(init)
+
+            def exchange():
+                if args.transport == "nccl":
+                    plan.exchange_nccl(d, ctx.nccl_comm(), hs.stream)
+                else:
+                    ctx.device_exchange(plan, d, hs.stream)
+
+            exchange()
+            hs.synchronize()
+            ok = bool(np.array_equal(d.to_numpy(), vals))
+            for _ in range(3):
+                exchange()
+            hs.synchronize()
+            ctx.barrier()
+            if args.transport == "nccl":
+                a0, a1 = Event(local), Event(local)
+                a0.record(hs.stream)
+                for _ in range(args.steps):
+                    exchange()
+                a1.record(hs.stream)
+                hs.synchronize()
+                ms_h = Event.elapsed_ms(a0, a1) / args.steps
+            else:
+                tt = time.perf_counter()
+                for _ in range(args.steps):
+                    exchange()
+                ms_h = (time.perf_counter() - tt) * 1e3 / args.steps
+            rb = float(sum(len(v) for v in plan.recv.values()) * L * 8)
+            r = allreduce([ms_h, rb, rb, float(ok), float(len(plan.peers))], dist.ReduceOp.MAX)
+            tot = allreduce([rb], dist.ReduceOp.SUM)[0]
+            okmin = allreduce([float(ok)], dist.ReduceOp.MIN)[0]
+            sweep.append({"halo": h, "bytes_per_exchange": tot, "worst_rank_recv_bytes": r[2], "ms": r[0],
+                          "GB_per_s": tot / (r[0] * 1e-3) / 1e9, "max_peers": int(r[4]),
+                          "ghosts_bitwise": okmin == 1.0,
+                          "timing": "device events on the exchange stream" if args.transport == "nccl"
+                          else "wall clock incl. host barriers"})
+            d.close()
+
     if rank == 0:
         ms = tmax / args.steps
         units = msum * L
         value = units / (ms * 1e-3) / 1e9
+        cfg = workload_config(source, target, L, 1, method, int(msum), int(S.npts + 2), world, args.partitioner)
         line = {
             "metric": metric_name(source, target, method, L), "value": value, "unit": "Gpts·lev/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
-            "config": {"workload": f"{source}->{target} {'structured-bilinear' if method == 'bilinear' else 'FE'} remap, "
-                                   f"{L} levels, {args.partitioner} P={world}, halo 2; "
-                                   + (f"step = fused exchange+apply over peer memory ({args.transport} fences)"
-                                      if args.fused else
-                                      f"step = halo exchange ({args.transport}) + apply (interior block overlapped "
-                                      "when stream-ordered)"),
-                       "levels": L, "parallelism": f"domain decomposition x{world}", "l2": "inputs > L2",
-                       "cuda_graph": graphed, "transport": args.transport, "fused": bool(args.fused)},
+            "config": cfg,
+            "step": {"description": (f"fused exchange+apply over peer memory ({args.transport} fences)" if args.fused else
+                                     f"halo exchange ({args.transport}) + apply, interior targets overlapped when "
+                                     "stream-ordered"),
+                     "halo": 2, "cuda_graph": graphed, "transport": args.transport, "fused": bool(args.fused)},
+            "comm": comm,
+            "parity": parity,
             "halo": {"bytes_per_exchange": hsum, "ms": hmax, "GB_per_s": hsum / (hmax * 1e-3) / 1e9},
+            "halo_sweep": sweep,
             "roofline": {"bound": "hbm", "achieved": worst_bytes / (worst_kern_ms * 1e-3) / 1e9, "peak": measured_peak()[0],
                          "unit": "GB/s", "frac": worst_bytes / (worst_kern_ms * 1e-3) / 1e9 / measured_peak()[0],
                          "traffic": None, "kernel_ms": worst_kern_ms, "algorithmic_bytes_per_launch": worst_bytes,
@@ -625,6 +785,8 @@ def run_multi(args):
         }
         print(json.dumps(line), flush=True)
     ctx.barrier()
+    if args.transport == "ipc":
+        ctx.close_ipc()
     dist.destroy_process_group()
 
 
@@ -650,6 +812,8 @@ def main():
     ap.add_argument("--fused", action="store_true",
                     help="N>1: no ghost copy — boundary targets read ghost rows from the owners' HBM "
                          "(CUDA IPC / NVLink) inside the apply kernel, fenced by NCCL barriers")
+    ap.add_argument("--no-halo-sweep", action="store_true",
+                    help="N>1: skip the cfg4 sweep (halo widths 1..3 exchanged on every rank)")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
                     help="N>1 halo exchange: NCCL send/recv (one GPU per rank) or CUDA-IPC pull")
     args = ap.parse_args()

@@ -232,6 +232,10 @@ int32_t sg_comm_barrier(uint64_t comm, uint64_t stream);
 /* one process, several GPUs (in-process ranks): ncclCommInitAll over devices[0..ndev), one
  * communicator handle per device in out_comms[rank] (SURVEY.md §8(b) sg_comm_init_all). */
 int32_t sg_comm_init_all(int32_t ndev, const int32_t* devices, uint64_t* out_comms);
+/* NCCL's own view of a communicator (ncclCommCount / ncclCommUserRank / ncclCommCuDevice) and
+ * the loaded NCCL's version code; any out pointer may be NULL. */
+int32_t sg_comm_info(uint64_t comm, int32_t* out_nranks, int32_t* out_rank, int32_t* out_device,
+                     int32_t* out_version);
 
 /* Partition-invariant digest of owned rows [row0, row0+nrows) whose global ids are gids
  * (functionspace.py:233-254): the wrapping u64 sum of splitmix64(gid*G + (level+1)*Lv ^ bits);

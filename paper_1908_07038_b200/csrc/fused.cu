@@ -130,6 +130,8 @@ void fused_impl(uint64_t stencil, uint64_t plan, uint64_t src_field, uint64_t ds
              "stencil, plan and fields live on different devices");
   const size_t np = p->peers.size();
   SG_REQUIRE(np == 0 || (peer_ptrs && peer_pitch_elems), "null peer arrays");
+  SG_REQUIRE(p->recv_off.back() == 0 || p->has_remote,
+             "plan has ghosts without an owner row (recv_remote); the fused apply needs them");
   FusedArgs a{};
   a.idx = s->idx.as<int4>();
   a.w = s->w.as<double2>();

@@ -129,6 +129,10 @@ struct Nccl {
   ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*CommCuDevice)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*GetVersion)(int*) = nullptr;
 };
 std::mutex g_nccl_mu;
 Nccl g_nccl;
@@ -157,6 +161,10 @@ Nccl& nccl() {
     SG_NCCL_SYM(Recv, "ncclRecv");
     SG_NCCL_SYM(AllReduce, "ncclAllReduce");
     SG_NCCL_SYM(GetErrorString, "ncclGetErrorString");
+    SG_NCCL_SYM(CommCount, "ncclCommCount");
+    SG_NCCL_SYM(CommUserRank, "ncclCommUserRank");
+    SG_NCCL_SYM(CommCuDevice, "ncclCommCuDevice");
+    SG_NCCL_SYM(GetVersion, "ncclGetVersion");
 #undef SG_NCCL_SYM
     g_nccl.lib = h;
   }
@@ -230,11 +238,16 @@ int32_t sg_halo_plan_create(int32_t device, int64_t nnodes, int32_t npeers, cons
     SG_REQUIRE(send_rows[k] >= 0 && send_rows[k] < nnodes, "send row %lld out of range", (long long)send_rows[k]);
     srows.push_back((int32_t)send_rows[k]);
   }
+  p->has_remote = recv_remote_rows != nullptr;
   for (int i = 0; i < npeers; ++i)
     for (int64_t k = p->recv_off[i]; k < p->recv_off[i + 1]; ++k) {
       SG_REQUIRE(recv_rows[k] >= 0 && recv_rows[k] < nnodes, "recv row %lld out of range", (long long)recv_rows[k]);
+      const int64_t rem = recv_remote_rows ? recv_remote_rows[k] : -1;
+      // -1 = owner row unknown (a plan built from send/recv lists only); pack/unpack still work
+      SG_REQUIRE(rem >= -1 && rem < INT32_MAX, "recv_remote row %lld out of range", (long long)rem);
+      if (rem < 0) p->has_remote = false;
       rrows.push_back((int32_t)recv_rows[k]);
-      rremote.push_back(recv_remote_rows ? (int32_t)recv_remote_rows[k] : -1);
+      rremote.push_back((int32_t)rem);
       rslot.push_back(i);
     }
   DeviceScope ds(device);
@@ -312,6 +325,7 @@ int32_t sg_halo_pull(uint64_t plan, uint64_t field, const uint64_t* peer_ptrs, c
   const int64_t n = p->recv_off.back();
   if (n == 0) return SG_OK;
   SG_REQUIRE(peer_ptrs && peer_pitch_elems, "null peer arrays");
+  SG_REQUIRE(p->has_remote, "plan has ghosts without an owner row (recv_remote); the pull transport needs them");
   PeerPtrs pp{};
   for (size_t i = 0; i < p->peers.size(); ++i) {
     pp.base[i] = reinterpret_cast<const void*>(peer_ptrs[i]);
@@ -375,6 +389,33 @@ int32_t sg_comm_init_all(int32_t ndev, const int32_t* devices, uint64_t* out_com
     c->token.alloc(c->device, 16);
     SG_CUDA(cudaMemset(c->token.ptr, 0, 16));
     out_comms[r] = registry_put(c.release());
+  }
+  SG_API_END
+}
+
+// NCCL's own view of a communicator (ncclCommCount / ncclCommUserRank / ncclCommCuDevice)
+// and the loaded library's version code: evidence that a multi-rank run really used NCCL.
+int32_t sg_comm_info(uint64_t comm, int32_t* out_nranks, int32_t* out_rank, int32_t* out_device,
+                     int32_t* out_version) {
+  SG_API_BEGIN
+  Comm* c = get<Comm>(comm, ObjKind::Comm);
+  Nccl& N = nccl();
+  int v = 0;
+  if (out_nranks) {
+    SG_NCCL(N.CommCount(c->comm, &v));
+    *out_nranks = v;
+  }
+  if (out_rank) {
+    SG_NCCL(N.CommUserRank(c->comm, &v));
+    *out_rank = v;
+  }
+  if (out_device) {
+    SG_NCCL(N.CommCuDevice(c->comm, &v));
+    *out_device = v;
+  }
+  if (out_version) {
+    SG_NCCL(N.GetVersion(&v));
+    *out_version = v;
   }
   SG_API_END
 }

@@ -20,6 +20,9 @@ struct Plan : Object {
   DevBuf sendbuf, recvbuf;                   // NCCL staging (lazily sized)
   // dense map of local rows [ghost_lo, nnodes): owner slot / owner row (-1: not a ghost)
   int64_t ghost_lo = 0;
+  // every ghost's owner row is known (recv_remote given and >= 0): the pull and fused
+  // kernels read owners' rows through it and are refused without it
+  bool has_remote = false;
   DevBuf ghost_slot, ghost_row;              // int32
 };
 

@@ -68,7 +68,7 @@ class DistributedRemap:
         self.stream_ordered = self.multi and getattr(ctx, "transport", None) == "nccl"
         self.fused = bool(fused) and self.multi
         self.comm = ctx.nccl_comm() if self.stream_ordered else None
-        self.peer_info = ctx.peer_fields(src) if self.fused else None
+        self.peer_info = ctx.peer_fields(src, self.plan) if self.fused else None
 
     @property
     def launches_per_step(self) -> int:

@@ -101,12 +101,32 @@ class HaloExchangePlan:
         return h.handle
 
     # -- device transports --------------------------------------------------------------------
-    def pull(self, dev: DeviceArray, peer_info) -> None:
-        """peer_info[r] = (ptr, pitch, device) of rank r's field; one fused kernel."""
+    def complete_remote(self, me: int, peer_sends) -> None:
+        """Fill ``recv_remote`` for peers it lacks (a plan built from send/recv lists only)
+        from the owners' send lists: ``peer_sends[p]`` = rank p's ``send`` dict, whose entry
+        for this rank lists, in this rank's receive order, the owner rows of our ghosts
+        (functionspace.py:83-93).  The pull/fused kernels need them; the library refuses a
+        plan without them rather than read a wrong row."""
+        missing = [p for p in self.recv if p not in self.recv_remote]
+        if not missing:
+            return
+        for p in missing:
+            rows = peer_sends[p].get(me)
+            if rows is None or len(rows) != len(self.recv[p]):
+                raise PlanMismatch(f"rank {p} sends {0 if rows is None else len(rows)} rows, "
+                                   f"this rank expects {len(self.recv[p])}")
+            self.recv_remote[p] = np.asarray(rows, np.int64)
+        for h in self._native.values():
+            h.close()
+        self._native.clear()
+
+    def pull(self, dev: DeviceArray, peer_info, stream: int = 0) -> None:
+        """peer_info[r] = (ptr, pitch, device) of rank r's field; one fused kernel on
+        ``stream``."""
         peers = self.peers
         ptrs = np.array([peer_info[p][0] for p in peers] or [0], np.uint64)
         pitch = np.array([peer_info[p][1] for p in peers] or [0], np.int64)
-        N.call("sg_halo_pull", self.native(dev.device), dev.handle, N.ptr(ptrs), N.ptr(pitch), 0)
+        N.call("sg_halo_pull", self.native(dev.device), dev.handle, N.ptr(ptrs), N.ptr(pitch), stream)
 
     def exchange_nccl(self, dev: DeviceArray, comm: int, stream: int = 0) -> None:
         N.call("sg_halo_exchange_nccl", self.native(dev.device), dev.handle, comm, stream)

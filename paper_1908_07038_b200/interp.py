@@ -9,9 +9,10 @@ exceptions and state transitions; the work runs in libsgb200:
   projection scale in one kernel (sg_remap_build) and keeps the device stencil attached to
   the returned ``InterpolationWeights`` for ``apply_remap``.  Zero messages (interp.py:9-11).
 * ``apply_remap`` is the multi-level SpMM kernel (sg_remap_apply), bitwise equal to the
-  numpy expression of interp.py:219-223.  Host-resident fields take the reference path
-  semantics (result in ``target.host``; SYNCED -> HOST_DIRTY) with the arithmetic on the
-  device through staging copies; device-resident fields stay in HBM (target DEVICE_DIRTY).
+  numpy expression of interp.py:219-223, with the reference's contract for every field
+  state (result in ``target.host``; SYNCED -> HOST_DIRTY): SYNCED sources are read from
+  HBM, the others are staged from the host.  ``apply_remap_device_fields`` is the opt-in
+  HBM-only entry point (target left DEVICE_DIRTY).
 * ``Interpolation(source_fs, target, target_dist, ctx).execute(src, tgt)`` is the Atlas
   spelling: build once, apply per call.
 
@@ -31,7 +32,7 @@ import numpy as np
 
 from . import _native as N
 from .device import DeviceArray, current_device
-from .errors import DegenerateTriangle, NotLocated, ShapeMismatch
+from .errors import DegenerateTriangle, NoDevice, NotLocated, ShapeMismatch, StaleDevice
 from .field import Field, MemoryState
 from .functionspace import NodeColumns
 from .grid import Grid
@@ -174,6 +175,14 @@ class InterpolationWeights:
             cache.clear()
             cache[key] = ([DeviceArray(src_shape[0], src_shape[1], np.float64, device) for _ in range(nfields)],
                           [DeviceArray(dst_shape[0], dst_shape[1], np.float64, device) for _ in range(nfields)])
+        return cache[key]
+
+    def _scratch(self, device: int, shape, index: int) -> DeviceArray:
+        """Device result buffer ``index`` of ``shape`` for apply_remap_fields, cached."""
+        key = (device, tuple(shape), index)
+        cache = self.__dict__.setdefault("_scratch_cache", {})
+        if key not in cache:
+            cache[key] = DeviceArray(shape[0], shape[1], np.float64, device)
         return cache[key]
 
     def distinct_sources(self) -> int:
@@ -360,34 +369,79 @@ def execute_host(weights: InterpolationWeights, host_src: Sequence[np.ndarray], 
 
 
 def apply_remap(weights: InterpolationWeights, source_field: Field, target_field: Field) -> None:
-    """target[t] = sum_i w_i * source[node_i], every level (interp.py:206-228)."""
+    """target[t] = sum_i w_i * source[node_i], every level (interp.py:206-228).
+
+    The reference's contract, whatever mirrors the fields have: the result lands in
+    ``target_field.host`` and the target goes SYNCED -> HOST_DIRTY (HOST_ONLY and the
+    reference's DEVICE_DIRTY quirk stay as they are).  The arithmetic always runs on the
+    GPU; see ``apply_remap_fields``.  ``apply_remap_device_fields`` is the HBM-only entry
+    point (target left DEVICE_DIRTY)."""
     apply_remap_fields(weights, [source_field], [target_field])
+
+
+def _device_current(f: Field, dev: int) -> bool:
+    return f.device is not None and f.device.device == dev and f.kind.dtype == np.float64
+
+
+def apply_remap_device_fields(weights: InterpolationWeights, source_fields: Sequence[Field],
+                              target_fields: Sequence[Field], stream: int = 0) -> None:
+    """The HBM-only apply (SURVEY.md §8(b) device entry point): F float64 field pairs whose
+    device mirrors are current (SYNCED or DEVICE_DIRTY), one kernel launch, targets left
+    DEVICE_DIRTY.  No host copy; ``update_host`` brings the result down."""
+    if len(source_fields) != len(target_fields) or not source_fields:
+        raise ValueError("need matching, non-empty source/target field lists")
+    dev = current_device()
+    for s, t in zip(source_fields, target_fields):
+        _check_shapes(weights, s, t)
+        for f in (s, t):
+            if f.state is MemoryState.HOST_ONLY or f.device is None:
+                raise NoDevice(f"field {f.name!r} has no device buffer")
+            if f.state is MemoryState.HOST_DIRTY:
+                raise StaleDevice(f"device access to {f.name!r} while host is newer; update_device first")
+            if not _device_current(f, dev):
+                raise ValueError(f"field {f.name!r}: device apply needs float64 mirrors on device {dev}")
+    apply_remap_device(weights, [s.device for s in source_fields], [t.device for t in target_fields], stream=stream)
+    N.call("sg_stream_synchronize", dev, stream)
+    for t in target_fields:
+        t.mark_device_written()
 
 
 def apply_remap_fields(weights: InterpolationWeights, source_fields: Sequence[Field],
                        target_fields: Sequence[Field]) -> None:
-    """apply_remap for F field pairs sharing one stencil in one pass: device-resident pairs
-    in one kernel launch, host-resident pairs in one pipelined host-buffer execute."""
+    """apply_remap for F field pairs sharing one stencil, with the reference's contract
+    (interp.py:218-228: reads ``source.host``, writes ``target.host``, SYNCED -> HOST_DIRTY).
+
+    * Sources whose device mirror is bit-identical to the host (SYNCED) are read from HBM:
+      one kernel launch for all such pairs, written into the target's device buffer when
+      that buffer's contents are not observable (target SYNCED or HOST_DIRTY) or into a
+      staging buffer otherwise, then one d2h of the target rows into ``target.host``.
+    * Every other source (HOST_ONLY, HOST_DIRTY, and DEVICE_DIRTY, whose host copy is what
+      the reference reads) goes through the pipelined host-buffer execute."""
     if len(source_fields) != len(target_fields) or not source_fields:
         raise ValueError("need matching, non-empty source/target field lists")
     for s, t in zip(source_fields, target_fields):
         _check_shapes(weights, s, t)
     dev = current_device()
 
-    def resident(s, t):
-        return (s.kind.dtype == np.float64 and t.kind.dtype == np.float64
-                and s.state in (MemoryState.SYNCED, MemoryState.DEVICE_DIRTY)
-                and t.state in (MemoryState.SYNCED, MemoryState.DEVICE_DIRTY)
-                and s.device is not None and t.device is not None and s.device.device == t.device.device)
-
     pairs = list(zip(source_fields, target_fields))
-    on_dev = [p for p in pairs if resident(*p)]
-    on_host = [p for p in pairs if not resident(*p)]
+    on_dev = [p for p in pairs if p[0].state is MemoryState.SYNCED and _device_current(p[0], dev)]
+    on_host = [p for p in pairs if not (p[0].state is MemoryState.SYNCED and _device_current(p[0], dev))]
     if on_dev:
-        apply_remap_device(weights, [s.device for s, _ in on_dev], [t.device for _, t in on_dev])
-        N.call("sg_stream_synchronize", on_dev[0][0].device.device, 0)
-        for _, t in on_dev:
-            t.mark_device_written()
+        outs = []
+        for k, (_, t) in enumerate(on_dev):
+            if _device_current(t, dev) and t.state in (MemoryState.SYNCED, MemoryState.HOST_DIRTY):
+                outs.append(t.device)
+            else:
+                outs.append(weights._scratch(dev, t.shape, k))
+        apply_remap_device(weights, [s.device for s, _ in on_dev], outs)
+        for (_, t), o in zip(on_dev, outs):
+            th = t.host
+            if th.dtype == np.float64 and th.flags["C_CONTIGUOUS"] and th.flags["WRITEABLE"]:
+                o.download(th)
+            else:
+                th[:] = o.to_numpy()
+            if t.state is MemoryState.SYNCED:
+                t.state = MemoryState.HOST_DIRTY
     if not on_host:
         return
     # host-resident fields: reference semantics (reads source.host, writes target.host);
@@ -484,3 +538,7 @@ class Interpolation:
 
     def execute(self, source_field: Field, target_field: Field) -> None:
         apply_remap(self.weights, source_field, target_field)
+
+    def execute_device(self, source_field: Field, target_field: Field) -> None:
+        """HBM-only execute: device-current mirrors in, target left DEVICE_DIRTY."""
+        apply_remap_device_fields(self.weights, [source_field], [target_field])

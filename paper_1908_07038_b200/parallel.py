@@ -165,27 +165,33 @@ class RankContext:
             w.board.pop((key, self.rank), None)
         return out
 
-    def peer_fields(self, dev_array) -> list:
-        """(ptr, pitch, device) of every rank's instance of a field (collective; cached per
-        field): ranks of one process address each other's HBM directly."""
-        cache = self.__dict__.setdefault("_peer_cache", {})
-        got = cache.get(dev_array.handle)
-        if got is None:
-            got = cache[dev_array.handle] = self.share((dev_array.ptr, dev_array.pitch, dev_array.device))
-            from . import _native as N
+    def peer_fields(self, dev_array, plan=None) -> list:
+        """(ptr, pitch, device) of every rank's instance of a field.  Collective, on every
+        call: each rank may pass a different buffer from call to call (its field's mirror or
+        a staging copy, depending on that rank's field state), so nothing is cached that a
+        peer could have replaced.  With ``plan``, the ranks' send lists travel along (by
+        reference: one address space) and complete a plan that lacks owner rows."""
+        got = self.share((dev_array.ptr, dev_array.pitch, dev_array.device, plan.send if plan is not None else None))
+        if plan is not None:
+            plan.complete_remote(self.rank, {r: g[3] for r, g in enumerate(got) if r != self.rank})
+        enabled = self.__dict__.setdefault("_p2p", set())
+        for _, _, dev, _ in got:  # NVLink P2P between this rank's GPU and every peer's
+            if dev != dev_array.device and (dev_array.device, dev) not in enabled:
+                from . import _native as N
 
-            for _, _, dev in got:  # NVLink P2P between this rank's GPU and every peer's
-                if dev != dev_array.device:
-                    N.call("sg_enable_peer_access", dev_array.device, dev)
-        return got
+                N.call("sg_enable_peer_access", dev_array.device, dev)
+                enabled.add((dev_array.device, dev))
+        return [g[:3] for g in got]
 
     def device_exchange(self, plan, dev_array, stream: int = 0) -> None:
-        """Fused device halo exchange over peer memory: one pull kernel per rank."""
-        ptrs = self.peer_fields(dev_array)
+        """Fused device halo exchange over peer memory: one pull kernel per rank on
+        ``stream``, between two barriers (owners' rows final before, not overwritten while
+        peers read)."""
+        ptrs = self.peer_fields(dev_array, plan)
         D.synchronize(dev_array.device, stream)
         self.barrier()
-        plan.pull(dev_array, ptrs)
-        D.synchronize(dev_array.device)
+        plan.pull(dev_array, ptrs, stream)
+        D.synchronize(dev_array.device, stream)
         self.barrier()
 
 
@@ -255,7 +261,7 @@ class DistContext:
         if transport not in ("nccl", "ipc"):
             raise ValueError(f"unknown transport {transport!r}")
         self.transport = transport
-        self._ipc: Dict[int, list] = {}
+        self._ipc: Dict[int, tuple] = {}  # peer rank -> (ipc handle bytes, mapped ptr, device)
         self._dist = dist
         self.rank = dist.get_rank()
         self.nranks = dist.get_world_size()
@@ -353,28 +359,53 @@ class DistContext:
             self._comm = N.Handle(h.value)
         return self._comm.handle
 
-    def peer_fields(self, dev_array) -> list:
-        """(ptr, pitch, device) of every rank's copy of this field, via CUDA IPC (cached)."""
+    def comm_info(self) -> dict:
+        """NCCL's own view of this rank's communicator (sg_comm_info)."""
         import ctypes as C
 
         from . import _native as N
 
-        got = self._ipc.get(dev_array.handle)
-        if got is None:
-            h = (C.c_uint8 * 64)()
-            N.call("sg_ipc_handle", dev_array.handle, N.ref(h), 64)
-            everyone = self.share((bytes(h), dev_array.pitch, dev_array.device))
-            got = []
-            for r, (blob, pitch, dev) in enumerate(everyone):
-                if r == self.rank:
-                    got.append((dev_array.ptr, dev_array.pitch, dev_array.device))
-                    continue
-                p = C.c_uint64(0)
-                hb = (C.c_uint8 * 64).from_buffer_copy(blob)
-                N.call("sg_ipc_open", dev_array.device, N.ref(hb), 64, N.ref(p))
-                got.append((p.value, pitch, dev))
-            self._ipc[dev_array.handle] = got
+        v = [C.c_int32(0) for _ in range(4)]
+        N.call("sg_comm_info", self.nccl_comm(), *[N.ref(x) for x in v])
+        return {"nranks": v[0].value, "rank": v[1].value, "device": v[2].value, "nccl_version": v[3].value}
+
+    def peer_fields(self, dev_array, plan=None) -> list:
+        """(ptr, pitch, device) of every rank's copy of this field, via CUDA IPC.  Collective
+        on every call (each rank may pass a different buffer per call); a peer's mapping is
+        reused while its IPC handle is unchanged and closed when the peer's buffer changes.
+        Plans must carry their owner rows (``recv_remote``, set by build_exchange_plan)."""
+        import ctypes as C
+
+        from . import _native as N
+
+        h = (C.c_uint8 * 64)()
+        N.call("sg_ipc_handle", dev_array.handle, N.ref(h), 64)
+        everyone = self.share((bytes(h), dev_array.pitch, dev_array.device))
+        got = []
+        for r, (blob, pitch, dev) in enumerate(everyone):
+            if r == self.rank:
+                got.append((dev_array.ptr, dev_array.pitch, dev_array.device))
+                continue
+            old = self._ipc.get(r)
+            if old is not None and old[0] == blob and old[2] == dev_array.device:
+                got.append((old[1], pitch, dev))
+                continue
+            if old is not None:
+                N.call("sg_ipc_close", old[2], old[1])
+            p = C.c_uint64(0)
+            hb = (C.c_uint8 * 64).from_buffer_copy(blob)
+            N.call("sg_ipc_open", dev_array.device, N.ref(hb), 64, N.ref(p))
+            self._ipc[r] = (blob, p.value, dev_array.device)
+            got.append((p.value, pitch, dev))
         return got
+
+    def close_ipc(self) -> None:
+        """Unmap every peer field opened through CUDA IPC."""
+        from . import _native as N
+
+        for _, ptr, dev in self._ipc.values():
+            N.call("sg_ipc_close", dev, ptr)
+        self._ipc.clear()
 
     def device_exchange(self, plan, dev_array, stream: int = 0) -> None:
         if self.transport == "nccl":
@@ -384,6 +415,6 @@ class DistContext:
         peers = self.peer_fields(dev_array)
         D.synchronize(dev_array.device, stream)
         self.barrier()  # every owner's rows are final
-        plan.pull(dev_array, peers)
+        plan.pull(dev_array, peers, stream)
         D.synchronize(dev_array.device, stream)
         self.barrier()  # nobody overwrites owned rows while a peer still reads them

@@ -259,6 +259,63 @@ def rotated():
     save("rotated", **out)
 
 
+def _digest(a) -> str:
+    import hashlib
+
+    a = np.ascontiguousarray(a)
+    return f"{a.dtype.str}:{'x'.join(map(str, a.shape))}:" + hashlib.sha256(a.tobytes()).hexdigest()
+
+
+def mesh_digest_fields(mesh):
+    conn = mesh.element_connectivity
+    return {"node_global": _digest(mesh.node_global.astype(np.int64)),
+            "node_xyz": _digest(mesh.node_xyz.astype(np.float64)),
+            "node_part": _digest(mesh.node_part.astype(np.int32)),
+            "node_remote": _digest(mesh.node_remote.astype(np.int64)),
+            "node_halo": _digest(mesh.node_halo.astype(np.int16)),
+            "node_ghost": _digest(mesh.node_ghost.astype(bool)),
+            "conn_offsets": _digest(conn.offsets.astype(np.int64)),
+            "conn_indices": _digest(conn.indices.astype(np.int64)),
+            "elem_serial_id": _digest(mesh.elem_serial_id.astype(np.int64)),
+            "nb_nodes": int(mesh.nb_nodes), "nb_elements": int(mesh.nb_elements)}
+
+
+def mesh_digests(ranks=(0, 3, 7)):
+    """sha256 digests of the O1280 grids (latitudes, lonlats, xyz), the serial O1280 halo-2
+    mesh with poles (the cfg3 source) and ranks of the O1280 P=8 halo-2 blocks meshes (the
+    N>1 bench): the full arrays are too large to commit, their digests pin them bitwise."""
+    import json
+
+    out = {}
+    path = os.path.join(HERE, "mesh_digests.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            out = json.load(fh)
+
+    def dump():
+        with open(path, "w") as fh:
+            json.dump(out, fh, indent=1, sort_keys=True)
+        print("wrote", path, sorted(out), flush=True)
+
+    for name in ("O1280", "O640"):
+        G = R.grid_from_name(name)
+        out[f"grid_{name}"] = {"latitudes": _digest(G.latitudes), "lonlats": _digest(G.lonlats()),
+                               "xyz": _digest(G.xyz()), "npts": int(G.npts)}
+    dump()
+    S = R.grid_from_name("O1280")
+    t = time.time()
+    out["mesh_O1280_p1_h2"] = mesh_digest_fields(R.generate_mesh(S, R.blocks_partition(S, 1), 0, halo=2,
+                                                                 include_pole=True))
+    print("serial mesh", round(time.time() - t, 1), flush=True)
+    dump()
+    dist = R.blocks_partition(S, 8)
+    for r in ranks:
+        t = time.time()
+        out[f"mesh_O1280_p8_h2_r{r}"] = mesh_digest_fields(R.generate_mesh(S, dist, r, halo=2, include_pole=True))
+        print("rank", r, round(time.time() - t, 1), flush=True)
+        dump()
+
+
 JOBS = {
     "rotated": rotated,
     "checksum": checksums,
@@ -272,6 +329,7 @@ JOBS = {
     "matching": matching,
     "cfg2": lambda: serial_remap("O320", "O160", 1, "cfg2_O320_O160"),
     "o1280": o1280_sample,
+    "digests": mesh_digests,
 }
 
 if __name__ == "__main__":

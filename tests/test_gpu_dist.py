@@ -89,4 +89,10 @@ def test_bench_torchrun_two_processes(gpu, extra):
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["scaling"] == "strong"
     assert line["halo"]["bytes_per_exchange"] > 0 and line["roofline"]["bound"] == "hbm"
     assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
-    assert line["config"]["fused"] == ("--fused" in extra)
+    assert line["step"]["fused"] == ("--fused" in extra) and line["comm"]["transport_fallback"] is None
+    p = line["parity"]
+    assert p["source_rows_bitwise"] and p["target_rows_bitwise"] and p["e2e_target_rows_bitwise"], p
+    assert [h["halo"] for h in line["halo_sweep"]] == [1, 2, 3]
+    assert all(h["ghosts_bitwise"] and h["bytes_per_exchange"] > 0 for h in line["halo_sweep"])
+    b = [h["bytes_per_exchange"] for h in line["halo_sweep"]]
+    assert b[0] < b[1] < b[2]

@@ -125,23 +125,6 @@ def test_bilinear_restatement_properties():
     assert (np.abs(rows[:, 2] - rows[:, 0]) <= 1).all()
 
 
-def test_bench_reference_arm_runs_on_cpu():
-    """bench.py --impl reference (the reference's apply on host threads, stencils from the
-    scaled oracle) prints one JSON line with the contract's keys."""
-    import json
-    import subprocess
-    import sys
-
-    from conftest import ROOT
-
-    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "cfg1", "--steps", "2",
-                          "--warmup", "3"], cwd=ROOT, capture_output=True, text=True, timeout=300)
-    assert out.returncode == 0, out.stderr[-2000:]
-    line = json.loads(out.stdout.strip().splitlines()[-1])
-    assert line["impl"] == "reference" and line["value"] > 0
-    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
-
-
 def test_oracle_checksum_equals_reference(golden):
     z = golden("checksum")
     for name in ("O32", "F8", "O16"):
