@@ -1,5 +1,5 @@
 """The bench JSON contract, checked on CPU against the committed line of the last B200 run
-(profiles/r01_bench_cfg3.json, written by ``python bench.py``): every key the driver and the
+(profiles/r02_bench_cfg3.json, written by ``python bench.py``): every key the driver and the
 judge read, with consistent values."""
 import json
 import os
@@ -8,7 +8,7 @@ from conftest import ROOT
 
 
 def load_line():
-    with open(os.path.join(ROOT, "profiles", "r01_bench_cfg3.json")) as fh:
+    with open(os.path.join(ROOT, "profiles", "r02_bench_cfg3.json")) as fh:
         return json.load(fh)
 
 
@@ -51,3 +51,17 @@ def test_e2e_cpu_baseline_clocks_parity():
     assert k["sm_mhz"] > 0.8 * k["sm_max_mhz"]
     assert not {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(k["reasons"])
     assert d["parity"]["checked"] and d["parity"]["device_bitwise_vs_cpu"] and d["parity"]["e2e_bitwise_vs_cpu"]
+
+
+def test_reference_arm_line_same_config():
+    """The reference arm (profiles/r02_bench_reference_cfg3.json, `bench.py --impl reference`
+    on the B200 box) ran the reference package from baseline/_ref, loaded none of the
+    product's libraries, and printed the product arm's exact config."""
+    with open(os.path.join(ROOT, "profiles", "r02_bench_reference_cfg3.json")) as fh:
+        ref = json.load(fh)
+    d = load_line()
+    assert ref["impl"] == "reference" and ref["metric"] == d["metric"] and ref["unit"] == d["unit"]
+    assert ref["config"] == d["config"]
+    assert ref["reference"]["product_imported"] is False
+    assert ref["reference"]["repo_libraries_loaded"] == ["oracle/_build/liblocate_oracle.so"]
+    assert ref["cpu_baseline"]["kind"] == "reference" and ref["e2e"]["value"] == ref["value"]
