@@ -383,6 +383,83 @@ def emulated_halo(sg, S, L, flush, parts=8, halo=2, partitioner="equal_regions",
                      "flushed; ms = max over ranks. Not NVLink (needs >1 GPU)"}
 
 
+def emulated_fused_step(sg, source, target, L, parts=8, partitioner="equal_regions", reps=10):
+    """The N>1 fused step (csrc/step.cu: exchange over peer memory + apply, device-side ready /
+    done signals, one kernel per rank) for ``parts`` ranks EMULATED on one GPU as ONE launch
+    over every rank's data (ranks whose kernels wait on each other must not be separate
+    launches on one GPU).  Compared with the same ranks' work as plain apply launches over
+    pre-exchanged fields (interior + boundary targets, one launch per rank, summed): the
+    difference is what the fused exchange and the signalling cost.  Parity: every rank's
+    target rows bitwise against the oracle apply (interp.py:219-223) on the analytic field."""
+    from oracle import oracle as O
+    from paper_1908_07038_b200.device import DeviceArray, Event
+    from paper_1908_07038_b200.execute import emulated_fused_steps, launch_fused_steps
+    from paper_1908_07038_b200.interp import apply_remap_range
+    from paper_1908_07038_b200.partition import PARTITIONERS
+
+    S, T = sg.grid_from_name(source), sg.grid_from_name(target)
+    dist = PARTITIONERS[partitioner](S, parts)
+    td = sg.matching_partition(T, S, dist)
+
+    def prog(ctx):
+        mesh = sg.generate_mesh(S, dist, ctx.rank, halo=2, include_pole=True)
+        fs = sg.NodeColumns(mesh, ctx)
+        return mesh, fs.exchange_plan, sg.build_remap(fs, T, td, ctx)
+
+    built = sg.run_ranks(parts, prog, devices=[0])
+    ranks, full = [], []
+    for mesh, plan, w in built:
+        host = np.zeros((mesh.nb_nodes, L))
+        fill_smooth(host, mesh.node_xyz, 0, rows=np.arange(mesh.nb_owned_nodes))
+        src = DeviceArray(mesh.nb_nodes, L, np.float64)
+        src.upload(host)
+        ranks.append((w, plan, src, DeviceArray(len(w), L, np.float64)))
+    steps = emulated_fused_steps(ranks)
+    for _ in range(3):
+        launch_fused_steps(steps)
+    e0, e1 = Event(0), Event(0)
+    e0.record()
+    for _ in range(reps):
+        launch_fused_steps(steps)
+    e1.record()
+    fused_ms = Event.elapsed_ms(e0, e1) / reps
+    epochs = [st.check() for st in steps]
+    # parity of the fused result, then the plain applies over exchanged fields for comparison
+    ok = True
+    for (w, plan, src, dst), (mesh, _, _) in zip(ranks, built):
+        exp_src = np.empty((mesh.nb_nodes, L))
+        fill_smooth(exp_src, mesh.node_xyz, 0)
+        exp = O.apply_remap_k(w.nodes, w.weights, exp_src)
+        ok &= bool(np.array_equal(dst.to_numpy().view(np.uint64), exp.view(np.uint64)))
+    info = [(r[2].ptr, r[2].pitch, 0) for r in ranks]
+    for (w, plan, src, dst) in ranks:
+        plan.pull(src, info)
+    for _ in range(3):
+        for (w, plan, src, dst) in ranks:
+            apply_remap_range(w, [src], [dst], 0, len(w), 0, 0)
+    e0.record()
+    for _ in range(reps):
+        for (w, plan, src, dst) in ranks:
+            apply_remap_range(w, [src], [dst], 0, len(w), 0, 0)
+    e1.record()
+    plain_ms = Event.elapsed_ms(e0, e1) / reps
+    m_tot = sum(len(r[0]) for r in ranks)
+    nbound = sum(st.n_boundary for st in steps)
+    ghost_bytes = sum(sum(len(v) for v in r[1].recv.values()) for r in ranks) * L * 8
+    for r in ranks:
+        r[2].close()
+        r[3].close()
+    return {"parts": parts, "partitioner": partitioner, "halo": 2, "targets": m_tot, "boundary_targets": nbound,
+            "ghost_bytes_per_exchange": ghost_bytes, "fused_step_ms": fused_ms,
+            "plain_apply_ms": plain_ms, "overhead_ms": fused_ms - plain_ms,
+            "Gpts_lev_per_s": m_tot * L / (fused_ms * 1e-3) / 1e9, "epochs": epochs,
+            "target_rows_bitwise": ok,
+            "scope": f"{source}->{target}, {L} lev: {parts} ranks EMULATED on one GPU as ONE launch of the fused "
+                     "step (signal kernel + step kernel over all ranks' data, ghost rows read from the owners' "
+                     "fields, ready/done words in HBM) vs the same ranks as one plain apply launch each over "
+                     "fields whose ghosts were exchanged beforehand; not NVLink (needs >1 GPU)"}
+
+
 def run_single(args):
     import paper_1908_07038_b200 as sg
     from paper_1908_07038_b200.device import DeviceArray, Event, PinnedArray
@@ -465,12 +542,16 @@ def run_single(args):
     clocks.active = False
     clocks.stop()
 
-    halo = None
+    halo = fstep = None
     if args.config == "cfg3" and not args.no_halo:
         try:  # auxiliary evidence: never lose the bench line over it
             halo = emulated_halo(sg, S, L, lambda: sg.apply_remap_device(w, dsrc, ddst, variant=args.variant))
         except Exception as exc:  # noqa: BLE001
             halo = {"error": f"{type(exc).__name__}: {exc}"}
+        try:
+            fstep = emulated_fused_step(sg, source, target, L)
+        except Exception as exc:  # noqa: BLE001
+            fstep = {"error": f"{type(exc).__name__}: {exc}"}
 
     # ---- CPU baseline, 1 core, same workload: the reference's own apply_remap (baseline/_ref)
     # on the same stencils and host arrays when installed, else the oracle port of
@@ -536,6 +617,7 @@ def run_single(args):
                 "mode": args.e2e_mode, "chunks": args.e2e_chunks, "direct_period": args.e2e_period,
                 "auto_trials_s": {k: [round(x, 4) for x in v] for k, v in w.__dict__.get("_auto_s", {}).items()}},
         "halo_emulated": halo,
+        "fused_step_emulated": fstep,
         "cpu_baseline": cpu,
         "gpu_launches": args.steps,
         "parity": parity,
@@ -578,9 +660,28 @@ def run_multi(args):
     hdst = PinnedArray((m, L))
     f = sg.Field(name="src", shape=(n, L), kind=sg.Kind.REAL64, host=hsrc.array).allocate_device()
     tf = sg.Field(name="dst", shape=(m, L), kind=sg.Kind.REAL64, host=hdst.array).allocate_device()
+    def allreduce(vals, op):
+        t = torch.tensor(vals, dtype=torch.float64)
+        dist.all_reduce(t, op=op)
+        return t.tolist()
+
     run = DistributedRemap(fs, w, ctx, f.device, tf.device, variant=args.variant, fused=args.fused)
-    run.step()
-    run.synchronize()
+    fallback, err = None, ""
+    try:
+        run.step()
+        run.synchronize()  # raises if a device-side wait of the fused step timed out
+        ok = 1.0
+    except sg.SpheregridError as exc:
+        ok, err = 0.0, str(exc)
+    if allreduce([ok], dist.ReduceOp.MIN)[0] == 0.0:
+        if not args.fused:
+            raise SystemExit(f"rank {rank}: first step failed: {err}")
+        # explicit, reported: the line carries transport_fallback and step.fused = false
+        fallback = f"fused step failed ({err or 'on another rank'}); pack -> {args.transport} -> unpack used"
+        log(f"rank {rank}: {fallback}")
+        run = DistributedRemap(fs, w, ctx, f.device, tf.device, variant=args.variant, fused=False)
+        run.step()
+        run.synchronize()
     log(f"rank {rank}: setup {time.time() - t0:.1f}s, {n} nodes ({n_owned} owned), {m} targets, "
         f"interior targets {run.n_interior}, {sum(len(v) for v in fs.exchange_plan.recv.values())} ghosts")
     for _ in range(args.warmup):
@@ -611,11 +712,6 @@ def run_multi(args):
     run.synchronize()
     my_ms = Event.elapsed_ms(e0, e1)
     ctx.barrier()
-
-    def allreduce(vals, op):
-        t = torch.tensor(vals, dtype=torch.float64)
-        dist.all_reduce(t, op=op)
-        return t.tolist()
 
     tmax = allreduce([my_ms], dist.ReduceOp.MAX)[0]
     msum = allreduce([float(m)], dist.ReduceOp.SUM)[0]
@@ -694,7 +790,7 @@ def run_multi(args):
               "e2e_target_rows_bitwise": oks[2] == 1.0, "targets_checked": int(msum),
               "against": "per rank: analytic field on every local row (owned + ghost) and the oracle apply "
                          "(interp.py:219-223) on the rank's own stencils"}
-    comm = {"transport": args.transport, "transport_fallback": None}
+    comm = {"transport": args.transport, "transport_fallback": fallback}
     if args.transport == "nccl":
         info = ctx.comm_info()
         nr = allreduce([float(info["nranks"])], dist.ReduceOp.MIN)[0]
@@ -765,10 +861,15 @@ def run_multi(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic spherical harmonics)",
             "config": cfg,
-            "step": {"description": (f"fused exchange+apply over peer memory ({args.transport} fences)" if args.fused else
-                                     f"halo exchange ({args.transport}) + apply, interior targets overlapped when "
-                                     "stream-ordered"),
-                     "halo": 2, "cuda_graph": graphed, "transport": args.transport, "fused": bool(args.fused)},
+            "step": {"description": (
+                "fused exchange+apply: one signal kernel + one step kernel per rank; boundary targets read ghost "
+                "rows from the owners' HBM (CUDA IPC over NVLink), ready/done flag words in peer memory, no "
+                "host or NCCL barrier" if run.signalled else
+                "fused exchange+apply over peer memory, host barriers (ranks share a GPU)" if run.fused else
+                f"halo exchange ({args.transport}) + apply, interior targets overlapped when stream-ordered"),
+                     "halo": 2, "cuda_graph": graphed, "transport": args.transport, "fused": bool(run.fused),
+                     "device_signalled": bool(run.signalled)},
+            "transport_fallback": fallback,
             "comm": comm,
             "parity": parity,
             "halo": {"bytes_per_exchange": hsum, "ms": hmax, "GB_per_s": hsum / (hmax * 1e-3) / 1e9},
@@ -809,9 +910,11 @@ def main():
     ap.add_argument("--partitioner", default="equal_regions", choices=["blocks", "equal_regions"],
                     help="N>1 source decomposition: equal regions (BASELINE configs[2]; EQ zonal "
                          "equal-area parts sized like blocks) or the reference pipeline's blocks bands")
-    ap.add_argument("--fused", action="store_true",
-                    help="N>1: no ghost copy — boundary targets read ghost rows from the owners' HBM "
-                         "(CUDA IPC / NVLink) inside the apply kernel, fenced by NCCL barriers")
+    ap.add_argument("--fused", action=argparse.BooleanOptionalAction, default=True,
+                    help="N>1 (default): no ghost copy — boundary targets read ghost rows from the owners' HBM "
+                         "(CUDA IPC / NVLink) inside one step kernel per rank, fenced by device-side flag words "
+                         "(one GPU per rank) or host barriers (ranks sharing a GPU); --no-fused: pack -> "
+                         "transport -> unpack with the interior apply overlapped")
     ap.add_argument("--no-halo-sweep", action="store_true",
                     help="N>1: skip the cfg4 sweep (halo widths 1..3 exchanged on every rank)")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],

@@ -43,6 +43,7 @@ int32_t sg_last_error(char* buf, size_t n);
 int32_t sg_registry_count(int64_t* out_live);
 int32_t sg_release(uint64_t handle);
 int32_t sg_device_count(int32_t* out_count);
+int32_t sg_device_uuid(int32_t device, uint8_t* out_uuid, size_t n);
 int32_t sg_stream_synchronize(int32_t device, uint64_t stream);
 
 /* ---- Field device mirror (field.py:77-162) ---------------------------------------------
@@ -236,6 +237,31 @@ int32_t sg_comm_init_all(int32_t ndev, const int32_t* devices, uint64_t* out_com
  * the loaded NCCL's version code; any out pointer may be NULL. */
 int32_t sg_comm_info(uint64_t comm, int32_t* out_nranks, int32_t* out_rank, int32_t* out_device,
                      int32_t* out_version);
+
+/* Fused distributed step with device-side signalling (csrc/step.cu): the halo exchange of
+ * functionspace.py:107-118 and the apply of interp.py:206-228 for one rank as one kernel,
+ * ordered like cli.py:138-144 (owners' rows final before ghosts are read) without host or
+ * NCCL barriers.  Each rank owns a signal (2*nranks+4 uint64 words: ready[r], done[r], epoch,
+ * current, count, error) that its peers write through NVLink P2P / CUDA-IPC pointers.
+ *   sg_step_create: peer_* by plan peer slot (the owner's source field pointer + pitch, the
+ *     peer's signal words); targets whose stencil reads a ghost row wait for their owners'
+ *     ready word and read that row from the owner's field.
+ *   sg_step_launch: one signal kernel + one step kernel over n steps of ONE device.  n = 1 and
+ *     wait_done = 1 with one GPU per rank; n > 1 (every rank of a single-GPU emulation in one
+ *     launch) requires wait_done = 0.
+ *   sg_step_check: status 1 if a wait timed out (a peer never signalled); waits are bounded by
+ *     sg_step_set_timeout (default 10 s). */
+int32_t sg_signal_create(int32_t device, int32_t nranks, int32_t rank, uint64_t* out_signal);
+int32_t sg_signal_ptr(uint64_t signal, uint64_t* out_dev_ptr);
+int32_t sg_signal_ipc_handle(uint64_t signal, uint8_t* out_handle, size_t n);
+int32_t sg_signal_read(uint64_t signal, uint64_t* out_words, int64_t n);
+int32_t sg_step_create(uint64_t stencil, uint64_t plan, uint64_t src_field, uint64_t dst_field,
+                       uint64_t signal, const uint64_t* peer_ptrs, const int64_t* peer_pitch_elems,
+                       const uint64_t* peer_flag_ptrs, uint64_t* out_step);
+int32_t sg_step_info(uint64_t step, int64_t* out_m, int64_t* out_n_boundary);
+int32_t sg_step_launch(const uint64_t* steps, int32_t n, int32_t wait_done, uint64_t stream);
+int32_t sg_step_check(uint64_t step, uint64_t* out_error, uint64_t* out_epoch);
+int32_t sg_step_set_timeout(uint64_t step, uint64_t timeout_ns);
 
 /* Partition-invariant digest of owned rows [row0, row0+nrows) whose global ids are gids
  * (functionspace.py:233-254): the wrapping u64 sum of splitmix64(gid*G + (level+1)*Lv ^ bits);

@@ -52,6 +52,7 @@ _SIGS = {
     "sg_registry_count": [vp],
     "sg_release": [u64],
     "sg_device_count": [vp],
+    "sg_device_uuid": [i32, vp, sz],
     "sg_stream_synchronize": [i32, u64],
     "sg_field_alloc": [i32, i64, i32, i32, vp, vp, vp],
     "sg_field_h2d": [u64, vp, u64],
@@ -103,6 +104,15 @@ _SIGS = {
     "sg_ipc_handle": [u64, vp, sz],
     "sg_ipc_open": [i32, vp, sz, vp],
     "sg_ipc_close": [i32, u64],
+    "sg_signal_create": [i32, i32, i32, vp],
+    "sg_signal_ptr": [u64, vp],
+    "sg_signal_ipc_handle": [u64, vp, sz],
+    "sg_signal_read": [u64, vp, i64],
+    "sg_step_create": [u64, u64, u64, u64, u64, vp, vp, vp, vp],
+    "sg_step_info": [u64, vp, vp],
+    "sg_step_launch": [vp, i32, i32, u64],
+    "sg_step_check": [u64, vp, vp],
+    "sg_step_set_timeout": [u64, u64],
     "sg_meshgen_create": [i32, vp, i32, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp],
     "sg_meshgen_fetch": [u64, vp, vp, vp, vp, vp, vp, vp, vp, vp],
     "sg_matching_partition": [i32, vp, vp, vp, vp, i64, i32, vp],
@@ -196,6 +206,12 @@ def device_count() -> int:
     n = C.c_int32(0)
     call("sg_device_count", ref(n))
     return n.value
+
+
+def device_uuid(device: int) -> bytes:
+    buf = (C.c_uint8 * 16)()
+    call("sg_device_uuid", device, ref(buf), 16)
+    return bytes(buf)
 
 
 def registry_count() -> int:

@@ -2,6 +2,7 @@
 // pitch chosen by field_pitch_elems (dense today).  h2d/d2h move the unpadded host
 // (npts, levels) C-order array (field.py:161): one contiguous copy for dense rows, a
 // cudaMemcpy2DAsync otherwise.
+#include <cstring>
 #include <sys/mman.h>
 
 #include <algorithm>
@@ -49,6 +50,16 @@ void* mmap_pinned(size_t bytes) {
 }  // namespace
 
 extern "C" {
+
+// 16-byte UUID of a device: tells whether two ranks (processes) drive the same physical GPU.
+int32_t sg_device_uuid(int32_t device, uint8_t* out_uuid, size_t n) {
+  SG_API_BEGIN
+  SG_REQUIRE(out_uuid && n >= 16, "buffer must hold 16 bytes");
+  cudaDeviceProp prop;
+  SG_CUDA(cudaGetDeviceProperties(&prop, device));
+  memcpy(out_uuid, prop.uuid.bytes, 16);
+  SG_API_END
+}
 
 int32_t sg_device_count(int32_t* out_count) {
   SG_API_BEGIN

@@ -1,0 +1,495 @@
+// One distributed remap step as ONE kernel per rank: halo exchange over peer memory + apply,
+// fenced by device-side signals instead of host or NCCL barriers.
+//
+// The reference step of a partition is halo_exchange (functionspace.py:107-118: owners'
+// values land in the ghost rows) followed by apply_remap (interp.py:206-228), in that order
+// (cli.py:138-144).  Here the two fuse (as in fused.cu: boundary targets read their ghost
+// stencil rows straight from the owners' HBM through peer pointers, NVLink P2P or CUDA IPC),
+// and the two barriers around the peer reads become flag words in device memory:
+//
+//   signal kernel (one thread per rank, waits for nothing):
+//       e = epoch + 1;  for every rank that reads my rows: st.release.sys  its ready[me] = e
+//   step kernel (blocks [0, nIb) interior targets, [nIb, nIb + nBb) boundary targets):
+//       interior warps: apply from local rows only — no wait;
+//       boundary warps: ld.acquire.sys  ready[owner] >= e  for every owner, then apply with
+//         ghost rows read from the owners' fields;
+//       the last boundary block to finish (atomic count): st.release.sys  owner's done[me] = e
+//         for every owner, then (one GPU per rank) waits for done[reader] >= e from every
+//         reader of my rows — after that nobody reads my rows any more, so the caller may
+//         overwrite them; epoch = e.
+//
+// Both waits depend only on the OTHER ranks' signal kernel / boundary blocks, never on a
+// block of the same launch, so with one GPU per rank there is no cycle.  Several ranks on ONE
+// GPU must not run as separate launches that wait on each other (B200_PROFILING.md): for that
+// case sg_step_launch takes every rank's step in ONE launch (block ranges per rank); then the
+// ready flags were set by the preceding signal kernel, and the tail wait is left to the host
+// (wait_done = 0; sg_signal_read checks the words).  Waits are bounded (~10 s): on timeout the
+// error word is set and the kernel continues; sg_step_check reports it (no hang, no silent
+// result).
+//
+// Arithmetic identical to the apply kernels: bitwise equal to interp.py:219-223.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "plan.cuh"
+#include "stencil.cuh"
+
+namespace sg {
+
+// Signal words (uint64) of one rank, zeroed at creation.
+struct Signal : Object {
+  Signal() : Object(ObjKind::Signal) {}
+  int device = 0;
+  int32_t nranks = 0, rank = 0;
+  DevBuf words;
+  size_t nwords() const { return 2 * (size_t)nranks + 4; }
+};
+
+namespace {
+
+constexpr int kMaxGroup = 16;  // ranks in one launch (single-GPU emulation)
+constexpr int kRoleRecv = 1;   // I read this peer's rows (it owns some of my ghosts)
+constexpr int kRoleSend = 2;   // this peer reads my rows
+constexpr unsigned long long kTimeoutNs = 10ull * 1000 * 1000 * 1000;  // default wait bound
+
+// word offsets
+__host__ __device__ inline int w_ready(int r) { return r; }
+__host__ __device__ inline int w_done(int nr, int r) { return nr + r; }
+__host__ __device__ inline int w_epoch(int nr) { return 2 * nr; }
+__host__ __device__ inline int w_cur(int nr) { return 2 * nr + 1; }
+__host__ __device__ inline int w_count(int nr) { return 2 * nr + 2; }
+__host__ __device__ inline int w_error(int nr) { return 2 * nr + 3; }
+
+// Peers of one rank (device resident: only boundary warps and the finisher read it).
+struct PeerTable {
+  int32_t npeers;
+  int32_t rank[kMaxPeers];
+  int32_t role[kMaxPeers];
+  const double* base[kMaxPeers];
+  int64_t pitch[kMaxPeers];
+  unsigned long long* flags[kMaxPeers];
+};
+
+// Everything a target warp needs, passed BY VALUE in the kernel parameters (constant bank):
+// a warp reaches its stencil load with no dependent global load in front of it.
+struct StepArgs {
+  const int4* idx;
+  const double2* w;  // double4 as two double2
+  int64_t m;           // targets, processed in their natural (ascending) order
+  int64_t n_boundary;  // targets with a ghost stencil row
+  int32_t levels, k;
+  const double* src;
+  int64_t src_pitch;
+  double* dst;
+  int64_t dst_pitch;
+  int64_t ghost_lo;  // local rows >= ghost_lo are ghosts: read from their owners
+  const int32_t* ghost_slot;
+  const int32_t* ghost_row;
+  unsigned long long* flags;  // this rank's words
+  unsigned long long timeout_ns;
+  int32_t nranks, rank;
+  const PeerTable* peers;
+};
+
+struct Group {
+  StepArgs d[kMaxGroup];
+  int64_t start[kMaxGroup + 1];  // first block of each rank
+  int32_t n;
+  int32_t wait_done;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long now_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Spin until *p >= e; false (and the error word set) after timeout_ns.
+__device__ bool wait_geq(const unsigned long long* p, unsigned long long e, unsigned long long* err, int code,
+                         unsigned long long timeout_ns) {
+  if (ld_acquire_sys(p) >= e) return true;
+  const unsigned long long t0 = now_ns();
+  while (ld_acquire_sys(p) < e) {
+    __nanosleep(64);
+    if (now_ns() - t0 > timeout_ns) {
+      atomicExch(err, (unsigned long long)code);
+      return false;
+    }
+  }
+  return true;
+}
+
+__device__ __forceinline__ double ld_local(const double* p) {  // read-only for this launch
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_any(const double* p) {  // peer rows: written before the acquire
+  double v;
+  asm volatile("ld.global.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double combine(double w0, double w1, double w2, double x, double y, double z) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(w0, x), __dmul_rn(w1, y)), __dmul_rn(w2, z));
+}
+
+__device__ __forceinline__ const double* row_of(const StepArgs& d, int n) {
+  if (n < d.ghost_lo) return d.src + (int64_t)n * d.src_pitch;
+  const int g = n - (int)d.ghost_lo;
+  const int s = __ldg(d.ghost_slot + g);
+  return d.peers->base[s] + (int64_t)__ldg(d.ghost_row + g) * d.peers->pitch[s];
+}
+
+// One target per warp.  BOUNDARY: rows may live on peers (weak loads after the acquire).
+template <int ITERS, bool BOUNDARY>
+__device__ __forceinline__ void apply_target(const StepArgs& d, int64_t t, int4 id, int lane) {
+  const double2 wa = __ldg(d.w + 2 * t), wb = __ldg(d.w + 2 * t + 1);
+  const double *r0, *r1, *r2, *r3;
+  if (BOUNDARY) {
+    r0 = row_of(d, id.x);
+    r1 = row_of(d, id.y);
+    r2 = row_of(d, id.z);
+    r3 = d.k == 4 ? row_of(d, id.w) : r0;
+  } else {
+    r0 = d.src + (int64_t)id.x * d.src_pitch;
+    r1 = d.src + (int64_t)id.y * d.src_pitch;
+    r2 = d.src + (int64_t)id.z * d.src_pitch;
+    r3 = d.k == 4 ? d.src + (int64_t)id.w * d.src_pitch : r0;
+  }
+  double* out = d.dst + t * d.dst_pitch;
+  const int L = d.levels;
+  if (ITERS > 0) {
+    double v0[ITERS > 0 ? ITERS : 1], v1[ITERS > 0 ? ITERS : 1], v2[ITERS > 0 ? ITERS : 1],
+        v3[ITERS > 0 ? ITERS : 1];
+#pragma unroll
+    for (int i = 0; i < ITERS; ++i) {
+      const int l = lane + 32 * i;
+      if (l < L) {
+        v0[i] = BOUNDARY ? ld_any(r0 + l) : ld_local(r0 + l);
+        v1[i] = BOUNDARY ? ld_any(r1 + l) : ld_local(r1 + l);
+        v2[i] = BOUNDARY ? ld_any(r2 + l) : ld_local(r2 + l);
+        v3[i] = d.k == 4 ? (BOUNDARY ? ld_any(r3 + l) : ld_local(r3 + l)) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < ITERS; ++i) {
+      const int l = lane + 32 * i;
+      if (l < L) {
+        double o = combine(wa.x, wa.y, wb.x, v0[i], v1[i], v2[i]);
+        if (d.k == 4) o = __dadd_rn(o, __dmul_rn(wb.y, v3[i]));
+        __stcs(out + l, o);
+      }
+    }
+  } else {
+    for (int l = lane; l < L; l += 32) {
+      double o = BOUNDARY ? combine(wa.x, wa.y, wb.x, ld_any(r0 + l), ld_any(r1 + l), ld_any(r2 + l))
+                          : combine(wa.x, wa.y, wb.x, ld_local(r0 + l), ld_local(r1 + l), ld_local(r2 + l));
+      if (d.k == 4) o = __dadd_rn(o, __dmul_rn(wb.y, BOUNDARY ? ld_any(r3 + l) : ld_local(r3 + l)));
+      __stcs(out + l, o);
+    }
+  }
+}
+
+__global__ void signal_kernel(Group g) {
+  const int r = threadIdx.x;
+  if (r >= g.n) return;
+  const StepArgs& d = g.d[r];
+  unsigned long long* f = d.flags;
+  const unsigned long long e = f[w_epoch(d.nranks)] + 1;
+  f[w_cur(d.nranks)] = e;
+  __threadfence_system();  // the owned rows written by earlier work on this stream, then the flag
+  const PeerTable& P = *d.peers;
+  for (int s = 0; s < P.npeers; ++s)
+    if (P.role[s] & kRoleSend) st_release_sys(P.flags[s] + w_ready(d.rank), e);
+}
+
+// The rank's last act of a step (one thread): tell the owners I am done reading their rows,
+// then (one GPU per rank) wait until every reader of my rows is done; epoch = e.
+__device__ void finish_step(const StepArgs& d, unsigned long long e, int wait_done) {
+  unsigned long long* f = d.flags;
+  const int nr = d.nranks;
+  const PeerTable& P = *d.peers;
+  __threadfence_system();
+  for (int s = 0; s < P.npeers; ++s)
+    if (P.role[s] & kRoleRecv) st_release_sys(P.flags[s] + w_done(nr, d.rank), e);
+  if (wait_done)
+    for (int s = 0; s < P.npeers; ++s)
+      if (P.role[s] & kRoleSend) wait_geq(f + w_done(nr, P.rank[s]), e, f + w_error(nr), 2, d.timeout_ns);
+  f[w_count(nr)] = 0;
+  f[w_epoch(nr)] = e;
+}
+
+constexpr int kWarps = 2;  // targets per block: small blocks retire and refill (apply.cu)
+
+// Targets in natural order, one per warp.  A warp whose stencil touches a ghost row waits for
+// the owners' ready words, reads the ghost rows from the owners' fields, and counts itself;
+// the last such warp (or, with no boundary targets, warp 0 of block 0) finishes the step.
+template <int ITERS>
+__global__ void __launch_bounds__(kWarps * 32) step_kernel(Group g) {
+  int r = 0;
+  while (r + 1 < g.n && (int64_t)blockIdx.x >= g.start[r + 1]) ++r;
+  const StepArgs& d = g.d[r];
+  const int64_t b = (int64_t)blockIdx.x - g.start[r];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t t = b * kWarps + warp;
+  if (t >= d.m) return;
+  const int4 id = __ldg(d.idx + t);
+  const int hi = max(max(id.x, id.y), d.k == 4 ? max(id.z, id.w) : id.z);
+  if (hi < d.ghost_lo) {  // interior: local rows only, no wait
+    apply_target<ITERS, false>(d, t, id, lane);
+    if (d.n_boundary == 0 && t == 0 && lane == 0)
+      finish_step(d, *(volatile unsigned long long*)(d.flags + w_cur(d.nranks)), g.wait_done);
+    return;
+  }
+  unsigned long long* f = d.flags;
+  const int nr = d.nranks;
+  const unsigned long long e = *(volatile unsigned long long*)(f + w_cur(nr));
+  {  // every owner of my ghosts has published its rows for epoch e (each lane acquires)
+    const PeerTable& P = *d.peers;
+    for (int s = 0; s < P.npeers; ++s)
+      if (P.role[s] & kRoleRecv) wait_geq(f + w_ready(P.rank[s]), e, f + w_error(nr), 1, d.timeout_ns);
+  }
+  apply_target<ITERS, true>(d, t, id, lane);
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    const unsigned long long old = atomicAdd(f + w_count(nr), 1ull);
+    if ((int64_t)old == d.n_boundary - 1) finish_step(d, e, g.wait_done);  // all peer reads done
+  }
+}
+
+__global__ void count_boundary(const int4* idx, int64_t m, int k, int64_t ghost_lo, unsigned long long* out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool bnd = false;
+  if (t < m) {
+    const int4 id = idx[t];
+    const int hi = max(max(id.x, id.y), k == 4 ? max(id.z, id.w) : id.z);
+    bnd = hi >= ghost_lo;
+  }
+  const unsigned c = __popc(__ballot_sync(0xffffffffu, bnd));
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+
+struct Step : Object {
+  Step() : Object(ObjKind::Step) {}
+  int device = 0;
+  StepArgs args{};
+  DevBuf peers;  // PeerTable
+  int64_t nblocks = 0;
+  uint64_t signal = 0;
+};
+
+}  // namespace
+}  // namespace sg
+
+using namespace sg;
+
+extern "C" {
+
+int32_t sg_signal_create(int32_t device, int32_t nranks, int32_t rank, uint64_t* out_signal) {
+  SG_API_BEGIN
+  SG_REQUIRE(out_signal, "null out pointer");
+  SG_REQUIRE(nranks >= 1 && 0 <= rank && rank < nranks, "rank %d not in [0, %d)", rank, nranks);
+  auto s = std::make_unique<Signal>();
+  s->device = device;
+  s->nranks = nranks;
+  s->rank = rank;
+  DeviceScope ds(device);
+  s->words.alloc(device, s->nwords() * 8);
+  SG_CUDA(cudaMemset(s->words.ptr, 0, s->nwords() * 8));
+  SG_CUDA(cudaDeviceSynchronize());
+  *out_signal = registry_put(s.release());
+  SG_API_END
+}
+
+int32_t sg_signal_ptr(uint64_t signal, uint64_t* out_dev_ptr) {
+  SG_API_BEGIN
+  Signal* s = get<Signal>(signal, ObjKind::Signal);
+  SG_REQUIRE(out_dev_ptr, "null out pointer");
+  *out_dev_ptr = reinterpret_cast<uint64_t>(s->words.ptr);
+  SG_API_END
+}
+
+int32_t sg_signal_ipc_handle(uint64_t signal, uint8_t* out_handle, size_t n) {
+  SG_API_BEGIN
+  Signal* s = get<Signal>(signal, ObjKind::Signal);
+  SG_REQUIRE(out_handle && n >= sizeof(cudaIpcMemHandle_t), "buffer must hold %zu bytes", sizeof(cudaIpcMemHandle_t));
+  DeviceScope ds(s->device);
+  cudaIpcMemHandle_t h;
+  SG_CUDA(cudaIpcGetMemHandle(&h, s->words.ptr));
+  memcpy(out_handle, &h, sizeof(h));
+  SG_API_END
+}
+
+int32_t sg_signal_read(uint64_t signal, uint64_t* out_words, int64_t n) {
+  SG_API_BEGIN
+  Signal* s = get<Signal>(signal, ObjKind::Signal);
+  SG_REQUIRE(out_words && n >= (int64_t)s->nwords(), "need %zu words", s->nwords());
+  DeviceScope ds(s->device);
+  SG_CUDA(cudaMemcpy(out_words, s->words.ptr, s->nwords() * 8, cudaMemcpyDeviceToHost));
+  SG_API_END
+}
+
+int32_t sg_step_create(uint64_t stencil, uint64_t plan, uint64_t src_field, uint64_t dst_field, uint64_t signal,
+                       const uint64_t* peer_ptrs, const int64_t* peer_pitch_elems, const uint64_t* peer_flag_ptrs,
+                       uint64_t* out_step) {
+  SG_API_BEGIN
+  Stencil* s = get<Stencil>(stencil, ObjKind::Stencil);
+  Plan* p = get<Plan>(plan, ObjKind::Plan);
+  Field* src = get<Field>(src_field, ObjKind::Field);
+  Field* dst = get<Field>(dst_field, ObjKind::Field);
+  Signal* sig = get<Signal>(signal, ObjKind::Signal);
+  SG_REQUIRE(out_step, "null out pointer");
+  if (src->npts != s->source_nnodes)
+    throw_error(SG_DOMAIN_ERROR, "ShapeMismatch: source field has %lld points, weights expect %lld",
+                (long long)src->npts, (long long)s->source_nnodes);
+  if (dst->npts != s->m)
+    throw_error(SG_DOMAIN_ERROR, "ShapeMismatch: target field has %lld points, weights cover %lld",
+                (long long)dst->npts, (long long)s->m);
+  if (src->levels != dst->levels) throw_error(SG_DOMAIN_ERROR, "ShapeMismatch: level counts differ");
+  if (src->npts != p->nnodes)
+    throw_error(SG_DOMAIN_ERROR, "PlanMismatch: field has %lld points, plan covers %lld nodes", (long long)src->npts,
+                (long long)p->nnodes);
+  SG_REQUIRE(src->itemsize == 8 && dst->itemsize == 8, "real64 fields only");
+  SG_REQUIRE(src->device == s->device && dst->device == s->device && p->device == s->device &&
+                 sig->device == s->device,
+             "stencil, plan, fields and signal live on different devices");
+  SG_REQUIRE(s->m < INT32_MAX, "too many targets");
+  const size_t np = p->peers.size();
+  SG_REQUIRE(np == 0 || (peer_ptrs && peer_pitch_elems && peer_flag_ptrs), "null peer arrays");
+  SG_REQUIRE(p->recv_off.back() == 0 || p->has_remote,
+             "plan has ghosts without an owner row (recv_remote); the fused step needs them");
+  auto st = std::make_unique<Step>();
+  st->device = s->device;
+  st->signal = signal;
+  PeerTable pt{};
+  pt.npeers = (int32_t)np;
+  for (size_t i = 0; i < np; ++i) {
+    SG_REQUIRE(p->peers[i] >= 0 && p->peers[i] < sig->nranks && p->peers[i] != sig->rank,
+               "plan peer %d is not another rank of %d", p->peers[i], sig->nranks);
+    SG_REQUIRE(peer_flag_ptrs[i] != 0, "null signal words for peer %d", p->peers[i]);
+    pt.rank[i] = p->peers[i];
+    pt.role[i] = (p->recv_off[i + 1] > p->recv_off[i] ? kRoleRecv : 0) |
+                 (p->send_off[i + 1] > p->send_off[i] ? kRoleSend : 0);
+    SG_REQUIRE(!(pt.role[i] & kRoleRecv) || peer_ptrs[i] != 0, "null field pointer for peer %d", p->peers[i]);
+    pt.base[i] = reinterpret_cast<const double*>(peer_ptrs[i]);
+    pt.pitch[i] = peer_pitch_elems[i];
+    pt.flags[i] = reinterpret_cast<unsigned long long*>(peer_flag_ptrs[i]);
+  }
+  DeviceScope ds(s->device);
+  st->peers.alloc(s->device, sizeof(PeerTable));
+  SG_CUDA(cudaMemcpy(st->peers.ptr, &pt, sizeof(PeerTable), cudaMemcpyHostToDevice));
+  StepArgs& d = st->args;
+  d.idx = s->idx.as<int4>();
+  d.w = s->w.as<double2>();
+  d.m = s->m;
+  d.levels = src->levels;
+  d.k = s->k;
+  d.src = src->buf.as<double>();
+  d.src_pitch = src->pitch;
+  d.dst = dst->buf.as<double>();
+  d.dst_pitch = dst->pitch;
+  d.ghost_lo = p->ghost_lo;
+  d.ghost_slot = p->ghost_slot.as<int32_t>();
+  d.ghost_row = p->ghost_row.as<int32_t>();
+  d.flags = sig->words.as<unsigned long long>();
+  d.timeout_ns = kTimeoutNs;
+  d.nranks = sig->nranks;
+  d.rank = sig->rank;
+  d.peers = st->peers.as<PeerTable>();
+  // boundary targets (a stencil row >= ghost_lo): the count the last reader checks against
+  DevBuf cnt;
+  cnt.alloc(s->device, 8);
+  SG_CUDA(cudaMemset(cnt.ptr, 0, 8));
+  if (s->m) {
+    count_boundary<<<(unsigned)((s->m + 255) / 256), 256>>>(d.idx, d.m, d.k, d.ghost_lo,
+                                                          cnt.as<unsigned long long>());
+    SG_CUDA_LAUNCH();
+  }
+  unsigned long long nb = 0;
+  SG_CUDA(cudaMemcpy(&nb, cnt.ptr, 8, cudaMemcpyDeviceToHost));
+  d.n_boundary = (int64_t)nb;
+  SG_REQUIRE(nb == 0 || p->recv_off.back() > 0, "stencil reads ghost rows the plan does not receive");
+  st->nblocks = std::max<int64_t>(1, (s->m + kWarps - 1) / kWarps);
+  *out_step = registry_put(st.release());
+  SG_API_END
+}
+
+int32_t sg_step_info(uint64_t step, int64_t* out_m, int64_t* out_n_boundary) {
+  SG_API_BEGIN
+  Step* st = get<Step>(step, ObjKind::Step);
+  if (out_m) *out_m = st->args.m;
+  if (out_n_boundary) *out_n_boundary = st->args.n_boundary;
+  SG_API_END
+}
+
+int32_t sg_step_launch(const uint64_t* steps, int32_t n, int32_t wait_done, uint64_t stream) {
+  SG_API_BEGIN
+  SG_REQUIRE(steps && n >= 1 && n <= kMaxGroup, "1..%d steps per launch", kMaxGroup);
+  SG_REQUIRE(!(n > 1 && wait_done), "a multi-rank launch on one GPU cannot wait for its own ranks (wait_done=0)");
+  Group g{};
+  g.n = n;
+  g.wait_done = wait_done ? 1 : 0;
+  int device = -1, levels = -1;
+  g.start[0] = 0;
+  for (int i = 0; i < n; ++i) {
+    Step* st = get<Step>(steps[i], ObjKind::Step);
+    if (i == 0) device = st->device, levels = st->args.levels;
+    SG_REQUIRE(st->device == device, "steps of one launch must share a device");
+    SG_REQUIRE(st->args.levels == levels, "steps of one launch must share the level count");
+    g.d[i] = st->args;
+    g.start[i + 1] = g.start[i] + st->nblocks;
+  }
+  SG_REQUIRE(g.start[n] < INT32_MAX, "too many targets for one launch");
+  DeviceScope ds(device);
+  cudaStream_t s = as_stream(stream);
+  signal_kernel<<<1, 32, 0, s>>>(g);
+  SG_CUDA_LAUNCH();
+  const unsigned grid = (unsigned)g.start[n];
+  switch ((levels + 31) / 32) {
+    case 1: step_kernel<1><<<grid, kWarps * 32, 0, s>>>(g); break;
+    case 2: step_kernel<2><<<grid, kWarps * 32, 0, s>>>(g); break;
+    case 3: step_kernel<3><<<grid, kWarps * 32, 0, s>>>(g); break;
+    case 4: step_kernel<4><<<grid, kWarps * 32, 0, s>>>(g); break;
+    case 5: step_kernel<5><<<grid, kWarps * 32, 0, s>>>(g); break;
+    default: step_kernel<0><<<grid, kWarps * 32, 0, s>>>(g); break;
+  }
+  SG_CUDA_LAUNCH();
+  SG_API_END
+}
+
+// Bound on every wait of this step (default 10 s); tests shorten it to exercise the timeout.
+int32_t sg_step_set_timeout(uint64_t step, uint64_t timeout_ns) {
+  SG_API_BEGIN
+  Step* st = get<Step>(step, ObjKind::Step);
+  SG_REQUIRE(timeout_ns > 0, "timeout must be positive");
+  st->args.timeout_ns = timeout_ns;
+  SG_API_END
+}
+
+// Error word of the step's signal (0 = fine; 1 = an owner never published its rows, 2 = a
+// reader never finished) and the last completed epoch.  Synchronous (reads device memory).
+int32_t sg_step_check(uint64_t step, uint64_t* out_error, uint64_t* out_epoch) {
+  SG_API_BEGIN
+  Step* st = get<Step>(step, ObjKind::Step);
+  Signal* sig = get<Signal>(st->signal, ObjKind::Signal);
+  std::vector<uint64_t> w(sig->nwords());
+  DeviceScope ds(sig->device);
+  SG_CUDA(cudaMemcpy(w.data(), sig->words.ptr, w.size() * 8, cudaMemcpyDeviceToHost));
+  if (out_error) *out_error = w[w_error(sig->nranks)];
+  if (out_epoch) *out_epoch = w[w_epoch(sig->nranks)];
+  if (w[w_error(sig->nranks)])
+    throw_error(SG_DOMAIN_ERROR, "SpheregridError: fused step of rank %d timed out waiting for a peer (%s)", sig->rank,
+                w[w_error(sig->nranks)] == 1 ? "owner rows never published" : "reader never finished");
+  SG_API_END
+}
+
+}  // extern "C"

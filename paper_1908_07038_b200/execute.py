@@ -8,14 +8,19 @@ NCCL send/recv -> unpack) runs on a second stream; the boundary targets follow o
 exchange's event fires.  Both sets are device target lists, so any decomposition (bands or
 equal regions, whose boundary targets interleave with interior ones) overlaps fully.  With
 ``fused=True`` there is no ghost copy at all: boundary targets read ghost rows straight from
-their owners' fields inside the apply kernel (sg_remap_apply_fused_list), fenced by NCCL
-barriers (stream-ordered) or host barriers.  ``capture()`` records a stream-ordered step into
-one CUDA graph.
+their owners' fields inside the apply kernel.  With one GPU per rank the fused step is ONE
+kernel per rank (csrc/step.cu, ``FusedStep``): owners publish "rows final" and readers "done
+reading" through flag words in each other's HBM (NVLink P2P / CUDA IPC), so no host or NCCL
+barrier remains in the step.  Ranks sharing a GPU keep host barriers around the fused apply
+(kernels that wait on each other must not be separate launches on one GPU); a single-GPU
+emulation of P ranks runs every rank's step in one launch (``launch_fused_steps``).
+``capture()`` records a stream-ordered step into one CUDA graph.
 """
 
 from __future__ import annotations
 
-from typing import Optional
+import ctypes as C
+from typing import List, Optional, Sequence
 
 import numpy as np
 
@@ -44,6 +49,71 @@ def _device_list(rows: np.ndarray, device: int) -> Optional[DeviceArray]:
     return d
 
 
+class Signal(N.Handle):
+    """A rank's step signal words in HBM (csrc/step.cu): ready[r], done[r], epoch, ..."""
+
+    def __init__(self, device: int, nranks: int, rank: int):
+        h = C.c_uint64(0)
+        N.call("sg_signal_create", device, nranks, rank, N.ref(h))
+        super().__init__(h.value)
+        self.device, self.nranks, self.rank = device, nranks, rank
+        p = C.c_uint64(0)
+        N.call("sg_signal_ptr", self.handle, N.ref(p))
+        self.ptr = p.value
+
+    def read(self) -> dict:
+        w = np.zeros(2 * self.nranks + 4, np.uint64)
+        N.call("sg_signal_read", self.handle, N.ptr(w), len(w))
+        R = self.nranks
+        return {"ready": w[:R].tolist(), "done": w[R:2 * R].tolist(), "epoch": int(w[2 * R]),
+                "current": int(w[2 * R + 1]), "count": int(w[2 * R + 2]), "error": int(w[2 * R + 3])}
+
+
+class FusedStep(N.Handle):
+    """One rank's exchange + apply as one kernel with device-side signalling
+    (sg_step_create).  ``peer_info[r]`` = (ptr, pitch, device) of rank r's source field
+    (ctx.peer_fields); ``peer_sigs[r]`` = (pointer to rank r's signal words, device uuid)
+    (ctx.peer_signals).  Targets run in natural order; the ``n_boundary`` whose stencil reads
+    a ghost row wait for their owners' ready word and read that row from the owner's field."""
+
+    def __init__(self, weights: InterpolationWeights, plan, src: DeviceArray, dst: DeviceArray, signal: Signal,
+                 peer_info, peer_sigs):
+        dev = src.device
+        peers = plan.peers
+        ptrs = np.array([peer_info[p][0] for p in peers] or [0], np.uint64)
+        pitch = np.array([peer_info[p][1] for p in peers] or [0], np.int64)
+        flags = np.array([peer_sigs[p][0] for p in peers] or [0], np.uint64)
+        h = C.c_uint64(0)
+        N.call("sg_step_create", weights.device_stencil(dev), plan.native(dev), src.handle, dst.handle, signal.handle,
+               N.ptr(ptrs), N.ptr(pitch), N.ptr(flags), N.ref(h))
+        super().__init__(h.value)
+        self.signal, self.device = signal, dev
+        m, nb = C.c_int64(0), C.c_int64(0)
+        N.call("sg_step_info", self.handle, N.ref(m), N.ref(nb))
+        self.m, self.n_boundary = m.value, nb.value
+        self._keep = (weights, plan, src, dst)
+
+    def launch(self, stream: int = 0) -> None:
+        launch_fused_steps([self], stream, wait_done=True)
+
+    def set_timeout(self, seconds: float) -> None:
+        """Bound on every device-side wait of this step (default 10 s)."""
+        N.call("sg_step_set_timeout", self.handle, max(1, int(seconds * 1e9)))
+
+    def check(self) -> int:
+        """Raises if a wait timed out; returns the last completed epoch (synchronous)."""
+        err, ep = C.c_uint64(0), C.c_uint64(0)
+        N.call("sg_step_check", self.handle, N.ref(err), N.ref(ep))
+        return ep.value
+
+
+def launch_fused_steps(steps: Sequence[FusedStep], stream: int = 0, wait_done: bool = False) -> None:
+    """One signal kernel + one step kernel over the given ranks' steps (all on one device).
+    Several ranks on one GPU: wait_done must be False (the host checks the words after)."""
+    arr = np.array([s.handle for s in steps], np.uint64)
+    N.call("sg_step_launch", N.ptr(arr), len(arr), int(bool(wait_done)), stream)
+
+
 class DistributedRemap:
     def __init__(self, fs, weights: InterpolationWeights, ctx, src: DeviceArray, dst: DeviceArray,
                  variant: int = APPLY_DEFAULT, overlap: bool = True, fused: bool = False):
@@ -65,16 +135,29 @@ class DistributedRemap:
         self.multi = ctx is not None and getattr(ctx, "nranks", 1) > 1
         # NCCL: stream-ordered exchange, overlappable and graph-capturable.  Otherwise
         # (in-process ranks, CUDA-IPC pull) the exchange is host-synchronised: no overlap.
-        self.stream_ordered = self.multi and getattr(ctx, "transport", None) == "nccl"
         self.fused = bool(fused) and self.multi
+        self.stream_ordered = self.multi and not self.fused and getattr(ctx, "transport", None) == "nccl"
         self.comm = ctx.nccl_comm() if self.stream_ordered else None
         self.peer_info = ctx.peer_fields(src, self.plan) if self.fused else None
+        # fused with one GPU per rank: device-side signalling, one kernel per rank per step.
+        # The decision is collective (identical on every rank): every rank on its own GPU.
+        self.signalled = False
+        self.fused_step: Optional[FusedStep] = None
+        if self.fused and hasattr(ctx, "peer_signals"):
+            self.signal = Signal(dev, ctx.nranks, ctx.rank)
+            sigs = ctx.peer_signals(self.signal)
+            self.signalled = len({u for _, u in sigs}) == ctx.nranks
+            if self.signalled:
+                self.fused_step = FusedStep(weights, self.plan, src, dst, self.signal, self.peer_info, sigs)
+                self.stream_ordered = True
 
     @property
     def launches_per_step(self) -> int:
         applies = int(self.interior is not None) + int(self.boundary is not None)
         if not self.multi:
             return 1
+        if self.signalled:
+            return 2  # signal kernel + step kernel
         if self.fused:
             return applies
         if not self.stream_ordered:
@@ -92,22 +175,17 @@ class DistributedRemap:
         if not self.multi:
             apply_remap_range(self.w, [self.src], [self.dst], 0, self.m, self.variant, main)
             return
-        if self.fused:
-            def fence():
-                if self.stream_ordered:
-                    N.call("sg_comm_barrier", self.comm, main)
-                else:
-                    self.main.synchronize()
-                    self.ctx.barrier()
-
-            if self.stream_ordered:  # interior rows are local: no fence needed before them
-                self._apply(self.interior, main)
-            fence()  # every owner's rows are final
-            if not self.stream_ordered:
-                self._apply(self.interior, main)
+        if self.signalled:
+            self.fused_step.launch(main)
+            return
+        if self.fused:  # ranks share a GPU: host barriers around the peer reads
+            self.main.synchronize()
+            self.ctx.barrier()  # every owner's rows are final
+            self._apply(self.interior, main)
             if self.boundary is not None:
                 apply_remap_fused_list(self.w, self.plan, self.src, self.dst, self.boundary, self.peer_info, main)
-            fence()  # nobody overwrites owned rows while a peer still reads them
+            self.main.synchronize()
+            self.ctx.barrier()  # nobody overwrites owned rows while a peer still reads them
             return
         if not self.stream_ordered:
             self.main.synchronize()
@@ -137,3 +215,22 @@ class DistributedRemap:
 
     def synchronize(self) -> None:
         self.main.synchronize()
+        if self.fused_step is not None:
+            self.fused_step.check()
+
+
+def emulated_fused_steps(ranks: Sequence[tuple]) -> List[FusedStep]:
+    """Fused steps of P ranks that all live on ONE GPU, for ``launch_fused_steps(steps)`` (one
+    launch over every rank's data: the single-GPU stand-in for P GPUs).  ``ranks[r]`` =
+    (weights, plan, src DeviceArray, dst DeviceArray) of rank r; plans need owner rows
+    (build_exchange_plan sets them)."""
+    P = len(ranks)
+    dev = ranks[0][2].device
+    if any(r[2].device != dev or r[3].device != dev for r in ranks):
+        raise ValueError("an emulated launch needs every rank on one device")
+    sigs = [Signal(dev, P, r) for r in range(P)]
+    uuid = N.device_uuid(dev)
+    peer_info = [(r[2].ptr, r[2].pitch, dev) for r in ranks]
+    peer_sigs = [(s.ptr, uuid) for s in sigs]
+    return [FusedStep(w, plan, src, dst, sigs[r], peer_info, peer_sigs)
+            for r, (w, plan, src, dst) in enumerate(ranks)]

@@ -183,6 +183,14 @@ class RankContext:
                 enabled.add((dev_array.device, dev))
         return [g[:3] for g in got]
 
+    def peer_signals(self, signal) -> list:
+        """(signal words pointer, device uuid) of every rank's step signal (execute.Signal).
+        Collective.  One address space: raw device pointers (NVLink P2P between GPUs, enabled
+        by peer_fields)."""
+        from . import _native as N
+
+        return self.share((signal.ptr, N.device_uuid(signal.device)))
+
     def device_exchange(self, plan, dev_array, stream: int = 0) -> None:
         """Fused device halo exchange over peer memory: one pull kernel per rank on
         ``stream``, between two barriers (owners' rows final before, not overwritten while
@@ -262,6 +270,7 @@ class DistContext:
             raise ValueError(f"unknown transport {transport!r}")
         self.transport = transport
         self._ipc: Dict[int, tuple] = {}  # peer rank -> (ipc handle bytes, mapped ptr, device)
+        self._ipc_sig: Dict[int, tuple] = {}  # same, for the peers' step signals
         self._dist = dist
         self.rank = dist.get_rank()
         self.nranks = dist.get_world_size()
@@ -399,13 +408,41 @@ class DistContext:
             got.append((p.value, pitch, dev))
         return got
 
-    def close_ipc(self) -> None:
-        """Unmap every peer field opened through CUDA IPC."""
+    def peer_signals(self, signal) -> list:
+        """(pointer to rank r's step signal words, mapped here through CUDA IPC, device uuid)
+        for every rank.  Collective; mappings are cached per peer while its handle is
+        unchanged and closed by close_ipc."""
+        import ctypes as C
+
         from . import _native as N
 
-        for _, ptr, dev in self._ipc.values():
+        h = (C.c_uint8 * 64)()
+        N.call("sg_signal_ipc_handle", signal.handle, N.ref(h), 64)
+        everyone = self.share((bytes(h), N.device_uuid(signal.device)))
+        got = []
+        for r, (blob, uuid) in enumerate(everyone):
+            if r == self.rank:
+                got.append((signal.ptr, uuid))
+                continue
+            old = self._ipc_sig.get(r)
+            if old is None or old[0] != blob:
+                if old is not None:
+                    N.call("sg_ipc_close", old[2], old[1])
+                p = C.c_uint64(0)
+                hb = (C.c_uint8 * 64).from_buffer_copy(blob)
+                N.call("sg_ipc_open", signal.device, N.ref(hb), 64, N.ref(p))
+                old = self._ipc_sig[r] = (blob, p.value, signal.device)
+            got.append((old[1], uuid))
+        return got
+
+    def close_ipc(self) -> None:
+        """Unmap every peer field and step signal opened through CUDA IPC."""
+        from . import _native as N
+
+        for _, ptr, dev in list(self._ipc.values()) + list(self._ipc_sig.values()):
             N.call("sg_ipc_close", dev, ptr)
         self._ipc.clear()
+        self._ipc_sig.clear()
 
     def device_exchange(self, plan, dev_array, stream: int = 0) -> None:
         if self.transport == "nccl":

@@ -69,7 +69,7 @@ def test_ipc_pull_exchange_processes(gpu, world):
     assert all(o[1] and o[2] for o in out), out
 
 
-@pytest.mark.parametrize("extra", [[], ["--fused"]])
+@pytest.mark.parametrize("extra", [["--no-fused"], ["--fused"]])
 def test_bench_torchrun_two_processes(gpu, extra):
     """The driver's N>1 launch line (torch.distributed.run, one process per rank) end to end on
     the one GPU of the test box: bench.py --gpus 2 with the CUDA-IPC transport on cfg2 (equal
@@ -90,6 +90,7 @@ def test_bench_torchrun_two_processes(gpu, extra):
     assert line["halo"]["bytes_per_exchange"] > 0 and line["roofline"]["bound"] == "hbm"
     assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
     assert line["step"]["fused"] == ("--fused" in extra) and line["comm"]["transport_fallback"] is None
+    assert line["step"]["device_signalled"] is False  # two ranks on one GPU: host barriers
     p = line["parity"]
     assert p["source_rows_bitwise"] and p["target_rows_bitwise"] and p["e2e_target_rows_bitwise"], p
     assert [h["halo"] for h in line["halo_sweep"]] == [1, 2, 3]

@@ -29,7 +29,7 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("extra", [[], ["--fused"], ["--partitioner", "blocks"]])
+@pytest.mark.parametrize("extra", [["--no-fused"], ["--fused"], ["--partitioner", "blocks"]])
 def test_torchrun_nccl_two_gpus_bitwise(extra):
     if _ngpus() < 2:
         pytest.skip("needs >= 2 GPUs (one NCCL rank per device)")
@@ -41,6 +41,8 @@ def test_torchrun_nccl_two_gpus_bitwise(extra):
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["comm"]["transport"] == "nccl" and line["comm"]["nccl_nranks"] == 2
     assert line["comm"]["transport_fallback"] is None
+    # fused is the default: one kernel per rank with device-side signalling over NVLink
+    assert line["step"]["device_signalled"] == ("--no-fused" not in extra)
     p = line["parity"]
     assert p["source_rows_bitwise"] and p["target_rows_bitwise"] and p["e2e_target_rows_bitwise"], p
     assert line["step"]["cuda_graph"] is True

@@ -1,0 +1,121 @@
+"""The fused distributed step with device-side signalling (csrc/step.cu, execute.FusedStep):
+halo exchange over peer memory + apply as one kernel per rank, fenced by flag words that the
+ranks write into each other's HBM instead of host or NCCL barriers.
+
+One GPU cannot host ranks whose separate launches wait on each other (B200_PROFILING.md), so
+P ranks are emulated as ONE launch over every rank's data (``launch_fused_steps``): the
+protocol (epochs, ready/done words, the last-block count) and the peer reads run exactly as
+with one GPU per rank, minus the tail wait.  Reference behaviour: halo_exchange
+(functionspace.py:107-118) then apply_remap (interp.py:206-228), in the order of
+cli.py:138-144; results must be bitwise equal to the oracle apply on the exchanged field."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _ranks(sg, S, T, P, L, part, gvals, halo=2):
+    from paper_1908_07038_b200.device import DeviceArray
+    from paper_1908_07038_b200.partition import PARTITIONERS
+
+    dist = PARTITIONERS[part](S, P)
+    td = sg.matching_partition(T, S, dist)
+
+    def prog(ctx):
+        mesh = sg.generate_mesh(S, dist, ctx.rank, halo=halo, include_pole=True)
+        fs = sg.NodeColumns(mesh, ctx)
+        w = sg.build_remap(fs, T, td, ctx)
+        src = DeviceArray(mesh.nb_nodes, L, np.float64)
+        init = np.zeros((mesh.nb_nodes, L))
+        own = fs.owned_row_index()
+        init[own] = gvals[mesh.node_global[own]]
+        src.upload(init)
+        dst = DeviceArray(len(w), L, np.float64)
+        return w, fs.exchange_plan, src, dst, mesh.nb_owned_nodes, mesh
+
+    return sg.run_ranks(P, prog, devices=[0])
+
+
+@pytest.mark.parametrize("S,T,P,L,part", [("O64", "O32", 2, 20, "blocks"), ("O64", "O32", 4, 137, "equal_regions"),
+                                          ("O96", "O48", 8, 137, "equal_regions"), ("O64", "O32", 8, 3, "blocks"),
+                                          ("F32", "F16", 3, 33, "blocks"), ("O32", "O64", 4, 137, "blocks"),
+                                          ("O48", "O96", 8, 40, "equal_regions"), ("F16", "O32", 5, 200, "blocks")])
+def test_emulated_fused_step_bitwise(gpu, S, T, P, L, part):
+    sg = gpu
+    from oracle import oracle as O
+    from paper_1908_07038_b200.device import synchronize
+    from paper_1908_07038_b200.execute import emulated_fused_steps, launch_fused_steps
+
+    Sg, Tg = sg.grid_from_name(S), sg.grid_from_name(T)
+    gvals = np.random.default_rng(11).normal(size=(Sg.npts + 2, L))
+    ranks = _ranks(sg, Sg, Tg, P, L, part, gvals)
+    steps = emulated_fused_steps([r[:4] for r in ranks])
+    nsteps = 3
+    for _ in range(nsteps):
+        launch_fused_steps(steps)
+    synchronize(0)
+    if Sg.npts < Tg.npts:  # up-sampling: targets next to the partition boundary read peers' rows
+        assert sum(s.n_boundary for s in steps) > 0
+    for r, ((w, plan, src, dst, n_owned, mesh), st) in enumerate(zip(ranks, steps)):
+        exp = O.apply_remap(w.nodes, w.weights, gvals[mesh.node_global])
+        assert np.array_equal(dst.to_numpy().view(np.uint64), exp.view(np.uint64)), f"rank {r}"
+        assert not src.to_numpy()[n_owned:].any()  # ghosts never written: read from the owners
+        assert st.check() == nsteps
+        words = st.signal.read()
+        assert words["error"] == 0 and words["count"] == 0 and words["current"] == nsteps
+        for p in plan.recv:  # every owner published epoch nsteps to me
+            assert words["ready"][p] == nsteps
+        for p in plan.send:  # every reader of my rows finished epoch nsteps
+            assert words["done"][p] == nsteps
+
+
+def test_single_rank_step_equals_apply(gpu):
+    """P = 1 (no peers): the real-mode launch (n = 1, wait_done = 1) is the plain apply."""
+    sg = gpu
+    from oracle import oracle as O
+    from paper_1908_07038_b200.execute import FusedStep, Signal
+
+    Sg, Tg = sg.grid_from_name("O48"), sg.grid_from_name("O24")
+    L = 137
+    gvals = np.random.default_rng(5).normal(size=(Sg.npts + 2, L))
+    (w, plan, src, dst, n_owned, mesh), = _ranks(sg, Sg, Tg, 1, L, "blocks", gvals)
+    sig = Signal(0, 1, 0)
+    st = FusedStep(w, plan, src, dst, sig, [(src.ptr, src.pitch, 0)], [(sig.ptr, b"")])
+    for _ in range(2):
+        st.launch()
+    assert st.check() == 2 and st.n_boundary == 0 and st.m == len(w)
+    exp = O.apply_remap(w.nodes, w.weights, gvals[mesh.node_global])
+    assert np.array_equal(dst.to_numpy().view(np.uint64), exp.view(np.uint64))
+
+
+def test_missing_peer_times_out_instead_of_hanging(gpu):
+    """A rank whose owner never publishes its rows does not hang: the bounded wait (1 ms here)
+    sets the error word and sg_step_check raises."""
+    sg = gpu
+    from paper_1908_07038_b200.device import synchronize
+    from paper_1908_07038_b200.execute import emulated_fused_steps, launch_fused_steps
+
+    Sg, Tg = sg.grid_from_name("O32"), sg.grid_from_name("O16")
+    gvals = np.zeros((Sg.npts + 2, 4))
+    Tg = sg.grid_from_name("O48")  # finer targets: rank 0 has boundary targets
+    ranks = _ranks(sg, Sg, Tg, 2, 4, "blocks", gvals)
+    steps = emulated_fused_steps([r[:4] for r in ranks])
+    assert steps[0].n_boundary > 0
+    steps[0].set_timeout(1e-3)
+    launch_fused_steps(steps[:1])  # rank 1 never runs
+    synchronize(0)
+    with pytest.raises(sg.SpheregridError, match="timed out"):
+        steps[0].check()
+
+
+def test_step_refuses_bad_launches(gpu):
+    sg = gpu
+    from paper_1908_07038_b200 import _native as N
+    from paper_1908_07038_b200.execute import emulated_fused_steps
+
+    Sg, Tg = sg.grid_from_name("O32"), sg.grid_from_name("O16")
+    ranks = _ranks(sg, Sg, Tg, 2, 4, "blocks", np.zeros((Sg.npts + 2, 4)))
+    steps = emulated_fused_steps([r[:4] for r in ranks])
+    arr = np.array([s.handle for s in steps], np.uint64)
+    with pytest.raises(N.NativeError, match="wait_done"):  # ranks of one launch cannot wait for each other
+        N.call("sg_step_launch", N.ptr(arr), 2, 1, 0)
