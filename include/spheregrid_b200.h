@@ -96,15 +96,20 @@ int32_t sg_field_info(uint64_t field, int32_t* out_device, int64_t* out_npts,
  *   (mesh.py:395-403), and builds a latitude-band / longitude-bin search structure on the
  *   device (the B200 replacement for the cKDTree + incidence lists).
  * sg_locator_locate <- MeshLocator.locate (interp.py:102-117), batched: per point the
- *   element id, the local corner triple, or -1 (NotLocated).  Winner = max over containing
+ *   element id, the local corner triple, or -1 (NotLocated), -2 (DegenerateTriangle: a
+ *   degenerate triangle among the reference's kNN candidates, interp.py:34-43), -3 (more
+ *   overlapping candidates than the exact emulation holds).  Winner = max over containing
  *   triangles (score = min of the three signed tests >= -CONTAIN_EPS) of the score; exact
- *   ties -> lowest local element id, then triangle index.
+ *   ties -> lowest local element id, then triangle index.  Meshes with
+ *   degenerate triangles are decided per point as the k = 8 / min(32, n) nearest-node search
+ *   would (node ranks by brute force; exact distance ties at the k-th place unpinned).
  * sg_remap_build <- build_remap (interp.py:154-203): locate + gnomonic barycentric weights
  *   (interp.py:61-71) + scale (interp.py:194) + optional nearest-node fallback
  *   (interp.py:179-190).  Returns a device stencil handle for sg_remap_apply and copies the
  *   InterpolationWeights arrays (interp.py:120-133) to the caller's host buffers.
  *   out_status[k]: 0 located, 1 not located (fallback row if allow_fallback),
- *   2 degenerate candidate triangle, 3 singular vertex matrix, 4 zero weight sum.
+ *   2 degenerate candidate triangle, 3 singular vertex matrix, 4 zero weight sum,
+ *   5 undecidable (over 96 overlapping candidate triangles; SpheregridError).
  *   On status SG_DOMAIN_ERROR *out_first_bad is the first (ascending) offending row and
  *   the message carries the reference exception class (NotLocated / DegenerateTriangle).
  * sg_stencil_create: device stencil from host arrays (an InterpolationWeights built

@@ -52,6 +52,9 @@ struct Locator : Object {
   double dlat = 0;
   int nbands = 0;
   int64_t nbins = 0, nentries = 0;
+  // nodes incident to an element with a degenerate triangle (knn_rule_kernel); usually none
+  DevBuf flagged;  // int32[nflagged]
+  int64_t nflagged = 0;
 };
 
 struct LocView {
@@ -302,49 +305,10 @@ __device__ __forceinline__ bool lu_solve3(const double M_in[3][3], const double 
   return true;
 }
 
-__global__ void __launch_bounds__(128) locate_kernel(LocView v, const double* pts, int64_t m,
-                                                     bool want_weights, TargetOut out) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= m) return;
-  const V3 q = V3{pts[3 * t], pts[3 * t + 1], pts[3 * t + 2]};
-  const double phi = asin(fmax(-1.0, fmin(1.0, q.z)));
-  const int band = band_of(phi, v.dlat, v.nbands);
-  const int nlon = v.band_nlon[band];
-  int bin_lo, bin_hi;
-  if (hypot(q.x, q.y) <= 1e-10) {  // at a pole: every bin of the band
-    bin_lo = v.band_off[band];
-    bin_hi = v.band_off[band] + nlon - 1;
-  } else {
-    double lam = atan2(q.y, q.x);
-    if (lam < 0) lam += kTwoPi;
-    bin_lo = bin_hi = v.band_off[band] + lonbin_of(lam, nlon);
-  }
-  int best = -1;
-  double best_score = 0.0;
-  bool degenerate = false;
-  for (int bin = bin_lo; bin <= bin_hi; ++bin) {
-    const int e0 = v.bin_start[bin], e1 = v.bin_start[bin + 1];
-    for (int e = e0; e < e1; ++e) {
-      const int tri = __ldg(v.entries + e);
-      const int4 tc = __ldg(v.tris + tri);
-      const V3 a = load3(v.xyz, tc.x), b = load3(v.xyz, tc.y), c = load3(v.xyz, tc.z);
-      const V3 ab = cross_np(a, b);
-      if (fabs(dot_blas(ab, c)) <= kDegenerateVol) degenerate = true;  // interp.py:40-43
-      const double t1 = dot_blas(ab, q);
-      const double t2 = dot_blas(cross_np(b, c), q);
-      const double t3 = dot_blas(cross_np(c, a), q);
-      const double score = fmin(t1, fmin(t2, t3));
-      if (score >= -kContainEps &&
-          (best < 0 || score > best_score || (score == best_score && tri < best))) {
-        best = tri;
-        best_score = score;
-      }
-    }
-  }
+// Weights + scale of target t for its chosen triangle (status 0), or the [1,0,0] placeholder.
+__device__ void finish_target(const LocView& v, V3 q, int64_t t, int best, uint8_t st, bool want_weights,
+                              const TargetOut& out) {
   out.best_tri[t] = best;
-  uint8_t st = 0;
-  if (degenerate) st = 2;
-  else if (best < 0) st = 1;
   if (want_weights) {
     double w[3] = {1.0, 0.0, 0.0};
     double sc = 1.0;
@@ -376,6 +340,186 @@ __global__ void __launch_bounds__(128) locate_kernel(LocView v, const double* pt
     out.scale[t] = sc;
   }
   out.status[t] = st;
+}
+
+__device__ __forceinline__ void bins_of(const LocView& v, V3 q, int& bin_lo, int& bin_hi) {
+  const double phi = asin(fmax(-1.0, fmin(1.0, q.z)));
+  const int band = band_of(phi, v.dlat, v.nbands);
+  const int nlon = v.band_nlon[band];
+  if (hypot(q.x, q.y) <= 1e-10) {  // at a pole: every bin of the band
+    bin_lo = v.band_off[band];
+    bin_hi = v.band_off[band] + nlon - 1;
+  } else {
+    double lam = atan2(q.y, q.x);
+    if (lam < 0) lam += kTwoPi;
+    bin_lo = bin_hi = v.band_off[band] + lonbin_of(lam, nlon);
+  }
+}
+
+// min(t1, t2, t3) of interp.py:111-113 with the reference's rounding; *degen: |(a x b).c| <= 1e-15
+__device__ __forceinline__ double tri_score(const LocView& v, int tri, V3 q, bool* degen) {
+  const int4 tc = __ldg(v.tris + tri);
+  const V3 a = load3(v.xyz, tc.x), b = load3(v.xyz, tc.y), c = load3(v.xyz, tc.z);
+  const V3 ab = cross_np(a, b);
+  *degen = fabs(dot_blas(ab, c)) <= kDegenerateVol;  // interp.py:40-43
+  const double t1 = dot_blas(ab, q);
+  const double t2 = dot_blas(cross_np(b, c), q);
+  const double t3 = dot_blas(cross_np(c, a), q);
+  return fmin(t1, fmin(t2, t3));
+}
+
+// Meshes without degenerate triangles: best containing triangle among the target's bin (a
+// superset of the reference's kNN candidates), ties -> lowest triangle id.  Degenerate
+// triangles never win (the reference raises before it could pick one); meshes that have any
+// are re-decided per target by knn_rule_kernel.
+__global__ void __launch_bounds__(128) locate_kernel(LocView v, const double* pts, int64_t m,
+                                                     bool want_weights, TargetOut out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  const V3 q = V3{pts[3 * t], pts[3 * t + 1], pts[3 * t + 2]};
+  int bin_lo, bin_hi;
+  bins_of(v, q, bin_lo, bin_hi);
+  int best = -1;
+  double best_score = 0.0;
+  for (int bin = bin_lo; bin <= bin_hi; ++bin) {
+    const int e0 = v.bin_start[bin], e1 = v.bin_start[bin + 1];
+    for (int e = e0; e < e1; ++e) {
+      const int tri = __ldg(v.entries + e);
+      bool degen;
+      const double score = tri_score(v, tri, q, &degen);
+      if (!degen && score >= -kContainEps &&
+          (best < 0 || score > best_score || (score == best_score && tri < best))) {
+        best = tri;
+        best_score = score;
+      }
+    }
+  }
+  finish_target(v, q, t, best, best < 0 ? 1 : 0, want_weights, out);
+}
+
+// ---- exact kNN-candidate emulation (meshes with degenerate triangles) -------------------
+// The reference scores only the elements incident to the k = 8 (then k = min(32, n)) nearest
+// nodes (interp.py:90-117) and raises DegenerateTriangle as soon as one of them has a
+// degenerate triangle (interp.py:34-43, 109-110).  Node n is "flagged" when an element
+// incident to it has a degenerate triangle; rank(x) = #nodes strictly closer to p than x
+// (squared distance, unfused, as cKDTree) — x is among the k nearest iff rank(x) < k (exact
+// distance ties at the k-th place are cKDTree-order dependent: parity unpinned there).
+//   pass k: raise if rank(nearest flagged node) < k; else best over the containing
+//   triangles whose element has a corner of rank < k (max score, ties -> lowest id); none ->
+//   next pass; after the last pass NotLocated.
+constexpr int kRuleThreads = 128;
+constexpr int kRuleMaxCand = 96;
+
+__device__ __forceinline__ double dist2(const double* xyz, int64_t i, V3 p) {
+  const double dx = __dsub_rn(xyz[3 * i], p.x), dy = __dsub_rn(xyz[3 * i + 1], p.y),
+               dz = __dsub_rn(xyz[3 * i + 2], p.z);
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+// #nodes with dist2 < d (block-wide, all threads call), stops counting at cap.
+__device__ int count_closer(const double* xyz, int64_t n, V3 p, double d, int cap, int* sh) {
+  if (threadIdx.x == 0) *sh = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < n; base += (int64_t)kRuleThreads * 8) {
+    int local = 0;
+    for (int j = 0; j < 8; ++j) {
+      const int64_t i = base + (int64_t)j * kRuleThreads + threadIdx.x;
+      if (i < n && dist2(xyz, i, p) < d) ++local;
+    }
+    if (local) atomicAdd(sh, local);
+    __syncthreads();
+    const int c = *sh;
+    __syncthreads();
+    if (c >= cap) return c;
+  }
+  return *sh;
+}
+
+__global__ void __launch_bounds__(kRuleThreads) knn_rule_kernel(LocView v, int64_t n, const int32_t* flagged,
+                                                                 int64_t nflagged, const double* pts, int64_t m,
+                                                                 bool want_weights, TargetOut out) {
+  const int64_t t = blockIdx.x;
+  if (t >= m) return;
+  const V3 q = V3{pts[3 * t], pts[3 * t + 1], pts[3 * t + 2]};
+  __shared__ double red[kRuleThreads];
+  __shared__ int sh_count, ncand;
+  __shared__ double cscore[kRuleMaxCand];
+  __shared__ int ctri[kRuleMaxCand], crank[kRuleMaxCand];
+  const int kmax = (int)(n < 32 ? n : 32);
+  // 1. nearest flagged node and its rank
+  double dmin = INFINITY;
+  for (int64_t i = threadIdx.x; i < nflagged; i += kRuleThreads) dmin = fmin(dmin, dist2(v.xyz, flagged[i], q));
+  red[threadIdx.x] = dmin;
+  __syncthreads();
+  for (int o = kRuleThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = fmin(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  const double dflag = red[0];
+  const int rank_flag = count_closer(v.xyz, n, q, dflag, kmax, &sh_count);
+  // 2. containing, non-degenerate triangles of the bin
+  if (threadIdx.x == 0) ncand = 0;
+  __syncthreads();
+  int bin_lo, bin_hi;
+  bins_of(v, q, bin_lo, bin_hi);
+  for (int bin = bin_lo; bin <= bin_hi; ++bin) {
+    const int e0 = v.bin_start[bin], e1 = v.bin_start[bin + 1];
+    for (int e = e0 + threadIdx.x; e < e1; e += kRuleThreads) {
+      const int tri = __ldg(v.entries + e);
+      bool degen;
+      const double score = tri_score(v, tri, q, &degen);
+      if (!degen && score >= -kContainEps) {
+        const int k = atomicAdd(&ncand, 1);
+        if (k < kRuleMaxCand) {
+          cscore[k] = score;
+          ctri[k] = tri;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const int nc = min(ncand, kRuleMaxCand);
+  // 3. rank of each candidate's element = min rank of its corners (all triangles of the element)
+  for (int c = 0; c < nc; ++c) {
+    const int tri = ctri[c];
+    const int elem = __ldg(v.tris + tri).w;
+    int lo = tri, hi = tri;
+    while (lo > 0 && __ldg(v.tris + lo - 1).w == elem) --lo;
+    while (__ldg(v.tris + hi + 1).w == elem) ++hi;  // tris is padded by the sentinel below
+    int r = kmax;
+    for (int u = lo; u <= hi; ++u) {
+      const int4 tc = __ldg(v.tris + u);
+      const int cs[3] = {tc.x, tc.y, tc.z};
+      for (int j = 0; j < 3; ++j) r = min(r, count_closer(v.xyz, n, q, dist2(v.xyz, cs[j], q), r, &sh_count));
+    }
+    if (threadIdx.x == 0) crank[c] = r;
+    __syncthreads();
+  }
+  // 4. the reference's two passes
+  if (threadIdx.x == 0) {
+    uint8_t st = 1;
+    int best = -1;
+    if (ncand > kRuleMaxCand) {
+      st = 5;  // too many overlapping candidates to decide exactly
+    } else {
+      const int ks[2] = {min(8, kmax), kmax};
+      for (int pass = 0; pass < 2 && st == 1; ++pass) {
+        const int k = ks[pass];
+        if (rank_flag < k) {
+          st = 2;
+          break;
+        }
+        double bs = 0.0;
+        for (int c = 0; c < nc; ++c)
+          if (crank[c] < k && (best < 0 || cscore[c] > bs || (cscore[c] == bs && ctri[c] < best))) {
+            best = ctri[c];
+            bs = cscore[c];
+          }
+        if (best >= 0) st = 0;
+      }
+    }
+    finish_target(v, q, t, st == 0 ? best : -1, st, want_weights, out);
+  }
 }
 
 // Nearest local node for the fallback rows (interp.py:186; kd-tree tie order unspecified,
@@ -423,6 +567,50 @@ LocView view_of(const Locator* L) {
                  L->band_nlon.as<int32_t>(),   L->band_off.as<int32_t>(),
                  L->bin_start.as<int32_t>(),   L->entries.as<int32_t>(),
                  L->dlat,                      L->nbands};
+}
+
+__global__ void degenerate_elems_kernel(const double* xyz, const int4* tris, int64_t ntri, uint8_t* elem_flag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ntri) return;
+  const int4 tc = tris[i];
+  const V3 a = load3(xyz, tc.x), b = load3(xyz, tc.y), c = load3(xyz, tc.z);
+  if (fabs(dot_blas(cross_np(a, b), c)) <= kDegenerateVol) elem_flag[tc.w] = 1;  // interp.py:40-43
+}
+
+__global__ void flag_nodes_kernel(const int4* tris, int64_t ntri, const uint8_t* elem_flag, uint8_t* node_flag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ntri) return;
+  const int4 tc = tris[i];
+  if (elem_flag[tc.w]) node_flag[tc.x] = node_flag[tc.y] = node_flag[tc.z] = 1;
+}
+
+// Nodes that make the reference raise DegenerateTriangle when they are among a target's
+// nearest nodes (corners of an element that has a degenerate triangle).
+void find_flagged_nodes(Locator* L, cudaStream_t st) {
+  L->nflagged = 0;
+  if (L->ntri == 0) return;
+  DevBuf ef, nf;
+  ef.alloc(L->device, (size_t)std::max<int64_t>(L->n_elems, 1));
+  nf.alloc(L->device, (size_t)std::max<int64_t>(L->n_nodes, 1));
+  SG_CUDA(cudaMemsetAsync(ef.ptr, 0, ef.bytes, st));
+  SG_CUDA(cudaMemsetAsync(nf.ptr, 0, nf.bytes, st));
+  const unsigned g = (unsigned)((L->ntri + 255) / 256);
+  degenerate_elems_kernel<<<g, 256, 0, st>>>(L->xyz.as<double>(), L->tris.as<int4>(), L->ntri, ef.as<uint8_t>());
+  SG_CUDA_LAUNCH();
+  flag_nodes_kernel<<<g, 256, 0, st>>>(L->tris.as<int4>(), L->ntri, ef.as<uint8_t>(), nf.as<uint8_t>());
+  SG_CUDA_LAUNCH();
+  std::vector<uint8_t> h((size_t)L->n_nodes);
+  if (L->n_nodes) SG_CUDA(cudaMemcpyAsync(h.data(), nf.ptr, h.size(), cudaMemcpyDeviceToHost, st));
+  SG_CUDA(cudaStreamSynchronize(st));
+  std::vector<int32_t> list;
+  for (int64_t i = 0; i < L->n_nodes; ++i)
+    if (h[i]) list.push_back((int32_t)i);
+  L->nflagged = (int64_t)list.size();
+  if (!list.empty()) {
+    L->flagged.alloc(L->device, list.size() * 4);
+    SG_CUDA(cudaMemcpyAsync(L->flagged.ptr, list.data(), list.size() * 4, cudaMemcpyHostToDevice, st));
+    SG_CUDA(cudaStreamSynchronize(st));
+  }
 }
 
 void build_bins(Locator* L, cudaStream_t st) {
@@ -571,14 +759,15 @@ int32_t sg_locator_create(int32_t device, const double* node_xyz, int64_t n_node
   L->device = device;
   L->n_nodes = n_nodes;
   L->n_elems = n_elems;
-  L->ntri = (int64_t)tris.size();
+  L->ntri = (int64_t)tris.size();  // before the sentinel
   L->xyz.alloc(device, (size_t)std::max<int64_t>(n_nodes, 1) * 24);
-  L->tris.alloc(device, std::max<size_t>(tris.size(), 1) * sizeof(int4));
+  tris.push_back(make_int4(0, 0, 0, -1));  // sentinel: element -1 ends the last element's run
+  L->tris.alloc(device, tris.size() * sizeof(int4));
   cudaStream_t st = 0;
   if (n_nodes) SG_CUDA(cudaMemcpyAsync(L->xyz.ptr, node_xyz, (size_t)n_nodes * 24, cudaMemcpyHostToDevice, st));
-  if (!tris.empty())
-    SG_CUDA(cudaMemcpyAsync(L->tris.ptr, tris.data(), tris.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+  SG_CUDA(cudaMemcpyAsync(L->tris.ptr, tris.data(), tris.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
   build_bins(L.get(), st);
+  find_flagged_nodes(L.get(), st);
   *out_locator = registry_put(L.release());
   SG_API_END
 }
@@ -610,6 +799,11 @@ static void run_locate(Locator* L, const double* points, int64_t m, bool want_we
   locate_kernel<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(view_of(L), dpts.as<double>(), m, want_weights,
                                                              out);
   SG_CUDA_LAUNCH();
+  if (L->nflagged) {  // degenerate triangles present: decide every target as the kNN search would
+    knn_rule_kernel<<<(unsigned)m, kRuleThreads, 0, st>>>(view_of(L), L->n_nodes, L->flagged.as<int32_t>(),
+                                                          L->nflagged, dpts.as<double>(), m, want_weights, out);
+    SG_CUDA_LAUNCH();
+  }
 }
 
 int32_t sg_locator_locate(uint64_t locator, const double* points, int64_t m, int64_t* out_elem,
@@ -635,8 +829,9 @@ int32_t sg_locator_locate(uint64_t locator, const double* points, int64_t m, int
     SG_CUDA(cudaMemcpy(tris.data(), L->tris.ptr, tris.size() * sizeof(int4), cudaMemcpyDeviceToHost));
   }
   for (int64_t i = 0; i < m; ++i) {
-    if (hb[i] < 0) {
-      out_elem[i] = -1;
+    if (hs[i] != 0 || hb[i] < 0) {
+      // -1 NotLocated, -2 DegenerateTriangle (a kNN candidate is degenerate), -3 undecidable
+      out_elem[i] = hs[i] == 2 ? -2 : hs[i] == 5 ? -3 : -1;
       if (out_corners) out_corners[3 * i] = out_corners[3 * i + 1] = out_corners[3 * i + 2] = -1;
     } else {
       const int4 tc = tris[hb[i]];
@@ -693,6 +888,10 @@ int32_t sg_remap_build(uint64_t locator, const double* target_xyz, int64_t m, in
     if (bad_kind == 2)
       sg::throw_error(SG_DOMAIN_ERROR, "DegenerateTriangle: degenerate candidate triangle for target row %lld",
                       (long long)first_bad);
+    if (bad_kind == 5)
+      sg::throw_error(SG_DOMAIN_ERROR,
+                      "SpheregridError: more than %d overlapping candidate triangles at target row %lld",
+                      kRuleMaxCand, (long long)first_bad);
     if (bad_kind == 4)
       sg::throw_error(SG_DOMAIN_ERROR, "DegenerateTriangle: projection plane through the origin (target row %lld)",
                       (long long)first_bad);

@@ -32,7 +32,7 @@ import numpy as np
 
 from . import _native as N
 from .device import DeviceArray, current_device
-from .errors import DegenerateTriangle, NoDevice, NotLocated, ShapeMismatch, StaleDevice
+from .errors import DegenerateTriangle, NoDevice, NotLocated, ShapeMismatch, SpheregridError, StaleDevice
 from .field import Field, MemoryState
 from .functionspace import NodeColumns
 from .grid import Grid
@@ -109,7 +109,9 @@ class MeshLocator:
         return {"triangles": nt.value, "bins": nb.value, "entries": ne.value, "band_rad": band.value}
 
     def locate_many(self, points: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
-        """(m, 3) points -> (element ids (m,), corner triples (m, 3)); -1 where not located."""
+        """(m, 3) points -> (element ids (m,), corner triples (m, 3)); element -1 where not
+        located, -2 where the reference raises DegenerateTriangle (a degenerate triangle among
+        its kNN candidates, interp.py:34-43), -3 undecidable."""
         pts = np.ascontiguousarray(np.atleast_2d(points), dtype=np.float64)
         elem = np.empty(len(pts), np.int64)
         corners = np.empty((len(pts), 3), np.int64)
@@ -119,6 +121,10 @@ class MeshLocator:
     def locate(self, p: np.ndarray):
         """-> (element id, triangle, local corner indices) or NotLocated (interp.py:102-117)."""
         elem, corners = self.locate_many(np.asarray(p, dtype=float).reshape(1, 3))
+        if elem[0] == -2:
+            raise DegenerateTriangle("degenerate candidate triangle")  # interp.py:40-43
+        if elem[0] == -3:
+            raise SpheregridError("too many overlapping candidate triangles to decide")
         if elem[0] < 0:
             raise NotLocated("point not contained in any candidate element")
         xyz = self.mesh.node_xyz

@@ -316,8 +316,59 @@ def mesh_digests(ranks=(0, 3, 7)):
         dump()
 
 
+DEGENERATE_GRIDS = {
+    # a 2-point row puts its points at lon 0 and 180: every triangle it makes with the pole
+    # (and the quads between two such rows) lies in the plane y = 0 -> |triple| <= 1e-15
+    "polar2": ((60.0, 2), (30.0, 8), (0.0, 8), (-30.0, 8), (-60.0, 3)),
+    "mid2": ((70.0, 6), (40.0, 2), (10.0, 8), (-20.0, 12), (-50.0, 5)),
+    "two2": ((75.0, 4), (45.0, 2), (15.0, 2), (-15.0, 10), (-45.0, 7), (-75.0, 3)),
+}
+DEGENERATE_TARGETS = ("O8", "O16", "F12")
+
+
+def degenerate():
+    """MeshLocator.locate (interp.py:102-117) on custom grids whose meshes hold degenerate
+    triangles: per target the outcome (0 located, 1 NotLocated, 2 DegenerateTriangle raised
+    while constructing a kNN candidate, interp.py:34-43), the element and corners; and for the
+    located ones whether barycentric_weights raises (interp.py:61-71)."""
+    out = {}
+    for gname, rows in DEGENERATE_GRIDS.items():
+        S = R.build_grid(R.GridSpec(kind=R.GridKind.CUSTOM, rows=rows))
+        mesh = R.generate_mesh(S, R.blocks_partition(S, 1), 0, halo=0, include_pole=True)
+        loc = RI.MeshLocator(mesh)
+        out[f"{gname}__rows"] = np.array(rows, dtype=np.float64)
+        out[f"{gname}__node_xyz"] = mesh.node_xyz
+        for tname in DEGENERATE_TARGETS:
+            T = R.grid_from_name(tname)
+            xyz = T.xyz()
+            code = np.zeros(T.npts, np.int8)
+            elem = np.full(T.npts, -1, np.int64)
+            corners = np.full((T.npts, 3), -1, np.int64)
+            wcode = np.zeros(T.npts, np.int8)
+            for t in range(T.npts):
+                try:
+                    e, tri, c = loc.locate(xyz[t])
+                except R.errors.NotLocated:
+                    code[t] = 1
+                    continue
+                except R.errors.DegenerateTriangle:
+                    code[t] = 2
+                    continue
+                elem[t], corners[t] = e, c
+                try:
+                    RI.barycentric_weights(tri, xyz[t])
+                except R.errors.DegenerateTriangle:
+                    wcode[t] = 1
+            key = f"{gname}__{tname}"
+            out[key + "__code"], out[key + "__elem"] = code, elem
+            out[key + "__corners"], out[key + "__wcode"] = corners, wcode
+            print(gname, tname, np.bincount(code, minlength=3), int(wcode.sum()), flush=True)
+    save("degenerate", **out)
+
+
 JOBS = {
     "rotated": rotated,
+    "degenerate": degenerate,
     "checksum": checksums,
     "latitudes": latitudes,
     "cfg1": lambda: serial_remap("O32", "O16", 10, "cfg1_O32_O16"),

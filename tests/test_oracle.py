@@ -147,3 +147,23 @@ def test_oracle_rotated_target_equals_reference(golden):
     src = np.random.default_rng(2026).normal(size=(mesh.nb_nodes, 3))
     out = O.apply_remap(z["remap_nodes"].astype(np.int64), z["remap_weights"], src)
     assert np.array_equal(out.view(np.uint64), z["remap_out"].view(np.uint64))
+
+
+@pytest.mark.parametrize("gname", ["polar2", "mid2", "two2"])
+def test_oracle_degenerate_candidates_equal_reference(golden, gname):
+    """The oracle's brute-force kNN locate raises DegenerateTriangle (-2) exactly where the
+    reference does on meshes with degenerate triangles (interp.py:34-43, 90-117), except at
+    exact distance ties at the k-th nearest node (cKDTree order, unpinned)."""
+    z = golden("degenerate")
+    rows = tuple((float(a), int(b)) for a, b in z[f"{gname}__rows"].tolist())
+    S = sg.build_grid(sg.GridSpec(kind=sg.GridKind.CUSTOM, rows=rows))
+    mesh = sg.generate_mesh(S, sg.blocks_partition(S, 1), 0, halo=0, include_pole=True)
+    assert np.array_equal(mesh.node_xyz.view(np.uint64), z[f"{gname}__node_xyz"].view(np.uint64))
+    conn = mesh.element_connectivity
+    for tname in ("O8", "O16", "F12"):
+        xyz = sg.grid_from_name(tname).xyz()
+        elem, _ = O.locate(mesh.node_xyz, conn.offsets, conn.indices, xyz)
+        code = np.where(elem >= 0, 0, np.where(elem == -2, 2, 1))
+        ref = z[f"{gname}__{tname}__code"]
+        diff = np.flatnonzero((code != ref) | ((code == 0) & (elem != z[f"{gname}__{tname}__elem"])))
+        assert len(diff) <= 2, (tname, diff)
