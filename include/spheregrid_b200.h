@@ -274,6 +274,14 @@ int32_t sg_step_set_timeout(uint64_t step, uint64_t timeout_ns);
 int32_t sg_field_checksum(uint64_t field, int64_t row0, int64_t nrows, const int64_t* gids,
                           uint64_t* out_partial);
 
+/* gather_field / scatter_field on the device (functionspace.py:185-224): indexed row copy
+ *   dst[dst_idx ? dst_idx[i] : i] = src[src_idx ? src_idx[i] : i], i < n, rows of row_bytes
+ * (a multiple of 4); indices are device int64 arrays (NULL = identity); src / dst may be peer
+ * memory (P2P or CUDA IPC mappings). */
+int32_t sg_rows_copy(int32_t device, uint64_t dst, int64_t dst_pitch_bytes, const int64_t* dst_idx_dev,
+                     uint64_t src, int64_t src_pitch_bytes, const int64_t* src_idx_dev, int64_t n,
+                     int64_t row_bytes, uint64_t stream);
+
 /* CUDA IPC for the multi-process pull path (one process per GPU). */
 int32_t sg_ipc_handle(uint64_t field, uint8_t* out_handle, size_t n);
 int32_t sg_ipc_open(int32_t device, const uint8_t* handle, size_t n, uint64_t* out_ptr);

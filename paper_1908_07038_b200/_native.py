@@ -101,6 +101,7 @@ _SIGS = {
     "sg_comm_init_all": [i32, vp, vp],
     "sg_comm_info": [u64, vp, vp, vp, vp],
     "sg_field_checksum": [u64, i64, i64, vp, vp],
+    "sg_rows_copy": [i32, u64, i64, u64, u64, i64, u64, i64, i64, u64],
     "sg_ipc_handle": [u64, vp, sz],
     "sg_ipc_open": [i32, vp, sz, vp],
     "sg_ipc_close": [i32, u64],

@@ -4,6 +4,13 @@
 //   h   = splitmix64_finalizer(key ^ value_bits)                           (functionspace.py:37-44)
 // value_bits = the 8-byte pattern, or the 4-byte pattern zero-extended (functionspace.py:227-230);
 // the partial digest is the wrapping u64 sum over the owned rows.  Integer-only: bit-exact.
+//
+// Indexed row copy for gather_field / scatter_field (functionspace.py:185-224) on the device:
+//   dst[dst_idx ? dst_idx[i] : i] = src[src_idx ? src_idx[i] : i],  i in [0, n)
+// a warp per row, every lane issuing all its loads before its stores; src / dst may be a
+// peer's memory (NVLink P2P in one process, CUDA IPC across processes), so rank 0 assembles
+// the global field straight from the ranks' HBM (gather) and every rank pulls its owned rows
+// from rank 0's copy of the global array (scatter).
 #include <vector>
 
 #include "cuda_util.cuh"
@@ -42,6 +49,39 @@ __global__ void checksum_kernel(const unsigned char* base, int64_t pitch_bytes, 
   if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
 }
 
+template <class W, int UNROLL>
+__global__ void __launch_bounds__(256) rows_copy_kernel(char* dst, int64_t dst_pitch, const int64_t* dst_idx,
+                                                         const char* src, int64_t src_pitch, const int64_t* src_idx,
+                                                         int64_t n, int64_t words) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int64_t di = dst_idx ? __ldg(dst_idx + i) : i, si = src_idx ? __ldg(src_idx + i) : i;
+  W* d = reinterpret_cast<W*>(dst + di * dst_pitch);
+  const W* s = reinterpret_cast<const W*>(src + si * src_pitch);
+  for (int64_t base = 0; base < words; base += 32 * UNROLL) {
+    W v[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t k = base + lane + 32 * u;
+      if (k < words) v[u] = s[k];
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t k = base + lane + 32 * u;
+      if (k < words) d[k] = v[u];
+    }
+  }
+}
+
+template <class W>
+void launch_rows_copy(char* dst, int64_t dp, const int64_t* di, const char* src, int64_t sp, const int64_t* si,
+                      int64_t n, int64_t row_bytes, cudaStream_t st) {
+  const int64_t words = row_bytes / (int64_t)sizeof(W);
+  const unsigned grid = (unsigned)((n * 32 + 255) / 256);
+  rows_copy_kernel<W, 8><<<grid, 256, 0, st>>>(dst, dp, di, src, sp, si, n, words);
+}
+
 }  // namespace
 
 using namespace sg;
@@ -74,5 +114,31 @@ extern "C" int32_t sg_field_checksum(uint64_t field, int64_t row0, int64_t nrows
   }
   SG_CUDA(cudaMemcpyAsync(out_partial, dacc.ptr, 8, cudaMemcpyDeviceToHost, st));
   SG_CUDA(cudaStreamSynchronize(st));
+  SG_API_END
+}
+
+extern "C" int32_t sg_rows_copy(int32_t device, uint64_t dst, int64_t dst_pitch_bytes, const int64_t* dst_idx_dev,
+                                uint64_t src, int64_t src_pitch_bytes, const int64_t* src_idx_dev, int64_t n,
+                                int64_t row_bytes, uint64_t stream) {
+  SG_API_BEGIN
+  SG_REQUIRE(n >= 0 && row_bytes >= 0, "negative size");
+  if (n == 0 || row_bytes == 0) return SG_OK;
+  SG_REQUIRE(dst && src, "null row pointers");
+  SG_REQUIRE(row_bytes % 4 == 0 && dst_pitch_bytes >= row_bytes && src_pitch_bytes >= row_bytes,
+             "rows must be whole 4-byte words within their pitch");
+  DeviceScope ds(device);
+  cudaStream_t st = as_stream(stream);
+  char* d = reinterpret_cast<char*>(dst);
+  const char* s = reinterpret_cast<const char*>(src);
+  const uint64_t align = dst | src | (uint64_t)dst_pitch_bytes | (uint64_t)src_pitch_bytes | (uint64_t)row_bytes;
+  if (align % 16 == 0)
+    launch_rows_copy<int4>(d, dst_pitch_bytes, dst_idx_dev, s, src_pitch_bytes, src_idx_dev, n, row_bytes, st);
+  else if (align % 8 == 0)
+    launch_rows_copy<unsigned long long>(d, dst_pitch_bytes, dst_idx_dev, s, src_pitch_bytes, src_idx_dev, n,
+                                         row_bytes, st);
+  else
+    launch_rows_copy<unsigned int>(d, dst_pitch_bytes, dst_idx_dev, s, src_pitch_bytes, src_idx_dev, n, row_bytes,
+                                   st);
+  SG_CUDA_LAUNCH();
   SG_API_END
 }

@@ -28,7 +28,7 @@ import numpy as np
 from . import _native as N
 from .device import DeviceArray, current_device
 from .errors import InconsistentMesh, PlanMismatch, StaleHost
-from .field import Field, Kind, MemoryState, create_field
+from .field import Field, Kind, MemoryState, _host_mirror, create_field
 from .grid import Grid
 from .mesh import Mesh
 from .partition import Distribution
@@ -324,7 +324,8 @@ def _owned_device_rows(fs, f: Field):
         return f.device, 0, len(rows)
     if f.state is MemoryState.DEVICE_DIRTY:
         f.update_host()
-    host = np.ascontiguousarray(f.host[rows])
+    # owned rows [0, n): upload straight from the host mirror (page-locked for large fields)
+    host = f.host[:len(rows)] if contiguous and f.host.flags["C_CONTIGUOUS"] else np.ascontiguousarray(f.host[rows])
     st = DeviceArray(max(len(rows), 1), f.levels, f.host.dtype, current_device())
     if len(rows):
         st.upload_rows(0, host)
@@ -367,9 +368,68 @@ def _owned_values(fs, f: Field) -> np.ndarray:
     return fs.owned_rows(f)
 
 
+def _gids_device(gids: np.ndarray, device: int) -> DeviceArray:
+    d = DeviceArray(max(len(gids), 1), 1, np.int64, device)
+    if len(gids):
+        d.upload(np.ascontiguousarray(gids, np.int64).reshape(-1, 1))
+    return d
+
+
+def _rows_copy(device: int, dst: DeviceArray, dst_idx: Optional[DeviceArray], src_ptr: int, src_pitch_bytes: int,
+               src_idx: Optional[DeviceArray], n: int, row_bytes: int, stream: int = 0) -> None:
+    N.call("sg_rows_copy", device, dst.ptr, dst.pitch * dst.dtype.itemsize, dst_idx.ptr if dst_idx is not None else 0,
+           src_ptr, src_pitch_bytes, src_idx.ptr if src_idx is not None else 0, n, row_bytes, stream)
+
+
+def _device_path(fs) -> bool:
+    # every owned-row layout here is rows [0, n_owned): NodeColumns numbers owned nodes first,
+    # StructuredColumns rows are all owned
+    rows = fs.owned_row_index()
+    return len(rows) == 0 or (rows[0] == 0 and rows[-1] == len(rows) - 1)
+
+
 def gather_field(fs, f: Field, ctx) -> Optional[np.ndarray]:
-    """Owned values of every rank assembled on rank 0 in global order (functionspace.py:185-204);
-    device-dirty fields are read from HBM."""
+    """Owned values of every rank assembled on rank 0 in global order (functionspace.py:185-204),
+    on the device: rank 0 copies every rank's owned rows straight out of that rank's HBM
+    (NVLink P2P / CUDA IPC) into their global rows of one device array (sg_rows_copy), then one
+    D2H.  Device-current fields are read from their mirror, host ones through one staging
+    upload.  Message counters as the reference: every other rank sends rank 0 one message of
+    its gids and values."""
+    if not _device_path(fs):
+        return _gather_host(fs, f, ctx)
+    dev, _, n = _owned_device_rows(fs, f)
+    L, dt = f.levels, f.host.dtype
+    row_bytes = L * dt.itemsize
+    gids = np.ascontiguousarray(fs.owned_global, np.int64)
+    device = dev.device
+    single = ctx is None or ctx.nranks == 1
+    peers = None if single else ctx.peer_fields(dev)  # collective: every rank's owned rows
+    if not single:
+        parts = ctx.gather_to_root(gids.tobytes())  # the reference's message: gids + values
+        if ctx.rank != 0:
+            ctx.bytes_sent += n * row_bytes
+            ctx.barrier()  # rank 0 has read my rows
+            return None
+    out = _host_mirror((fs.global_size, L), dt)  # page-locked when large: D2H at the DMA rate
+    G = DeviceArray(max(fs.global_size, 1), L, dt, device)  # zero-filled, like np.zeros
+    try:
+        srcs = [(gids, dev.ptr, dev.pitch * dt.itemsize)] if single else [
+            (np.frombuffer(parts[r], np.int64), peers[r][0], peers[r][1] * dt.itemsize) for r in range(ctx.nranks)]
+        for g, ptr, pitch in srcs:
+            if len(g):
+                gd = _gids_device(g, device)
+                _rows_copy(device, G, gd, ptr, pitch, None, len(g), row_bytes)
+                gd.close()
+        if fs.global_size:
+            G.download(out)
+    finally:
+        if not single:
+            ctx.barrier()
+        G.close()
+    return out
+
+
+def _gather_host(fs, f: Field, ctx) -> Optional[np.ndarray]:
     owned = np.ascontiguousarray(_owned_values(fs, f))
     gids = fs.owned_global
     if ctx is None or ctx.nranks == 1:
@@ -389,9 +449,63 @@ def gather_field(fs, f: Field, ctx) -> Optional[np.ndarray]:
 
 
 def scatter_field(fs, f: Field, ctx, global_values: Optional[np.ndarray]) -> None:
-    """Rank 0's global array into every rank's owned rows (functionspace.py:207-224)."""
+    """Rank 0's global array into every rank's owned rows (functionspace.py:207-224), on the
+    device: rank 0 uploads the global array once; every rank pulls its owned rows from rank
+    0's HBM by global index (sg_rows_copy over P2P / CUDA IPC) and downloads them into its
+    host rows.  Host rows written, SYNCED -> HOST_DIRTY, message counters as the reference
+    (gid lists to rank 0, one data message back to every rank)."""
     if f.state is MemoryState.DEVICE_DIRTY:
         raise StaleHost(f"field {f.name!r} is device-dirty; update_host before scattering")
+    single = ctx is None or ctx.nranks == 1
+    root = single or ctx.rank == 0
+    dt, L = f.host.dtype, f.levels
+    same_dtype = not root or (isinstance(global_values, np.ndarray) and global_values.dtype == dt
+                              and global_values.shape == (fs.global_size, L))
+    if not single:  # collective decision: the reference's byte-reinterpreting quirk stays on the host
+        same_dtype = all(ctx.share(bool(same_dtype)))
+    if not (_device_path(fs) and same_dtype):
+        return _scatter_host(fs, f, ctx, global_values)
+    rows = fs.owned_row_index()
+    n = len(rows)
+    gids = np.ascontiguousarray(fs.owned_global, np.int64)
+    row_bytes = L * dt.itemsize
+    device = current_device()
+    G = None
+    if root:
+        G = DeviceArray(max(fs.global_size, 1), L, dt, device)
+        if fs.global_size:
+            G.upload(np.ascontiguousarray(global_values))
+    mine = DeviceArray(max(n, 1), L, dt, device)
+    try:
+        if single:
+            src = (G.ptr, G.pitch)
+        else:
+            src = ctx.peer_fields(G if root else mine)[0][:2]  # collective: rank 0's global copy
+            counts = ctx.share(n)
+            if root:
+                ctx.messages_received += ctx.nranks - 1
+                ctx.messages_sent += ctx.nranks - 1
+                ctx.bytes_sent += sum(counts[1:]) * row_bytes
+            else:
+                ctx.messages_sent += 1
+                ctx.bytes_sent += 8 * n
+                ctx.messages_received += 1
+        if n:
+            gd = _gids_device(gids, device)
+            _rows_copy(device, mine, None, src[0], src[1] * dt.itemsize, gd, n, row_bytes)
+            mine.download_rows_into(0, f.host[:n])  # owned rows are [0, n)
+            gd.close()
+    finally:
+        if not single:
+            ctx.barrier()  # rank 0's global copy is no longer read
+        mine.close()
+        if G is not None:
+            G.close()
+    if f.state is MemoryState.SYNCED:
+        f.state = MemoryState.HOST_DIRTY
+
+
+def _scatter_host(fs, f: Field, ctx, global_values: Optional[np.ndarray]) -> None:
     rows = fs.owned_row_index()
     if ctx is None or ctx.nranks == 1:
         f.host[rows] = global_values[fs.owned_global]

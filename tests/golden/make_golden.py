@@ -366,9 +366,48 @@ def degenerate():
     save("degenerate", **out)
 
 
+def gather_scatter():
+    """gather_field / scatter_field (functionspace.py:185-224) at P = 1, 2, 4: NodeColumns on
+    O32 (mesh halo 1, poles) with seeded owned values -> the gathered global array and every
+    rank's message counters; StructuredColumns scatter of a global array -> each rank's rows
+    and counters."""
+    out = {}
+    g = R.grid_from_name("O32")
+    for kind, levels in [(R.Kind.REAL64, 4), (R.Kind.INT32, 3)]:
+        tag = kind.name.lower()
+        rng = np.random.default_rng(91)
+        gvals = rng.normal(size=(g.npts + 2, levels)) * 1e3
+        gvals = gvals.astype(kind.dtype)
+        out[f"{tag}_values"] = gvals
+        for P in (1, 2, 4):
+            def program(ctx):
+                c = ctx if ctx.nranks > 1 else None
+                dist = R.blocks_partition(g, ctx.nranks)
+                mesh = R.generate_mesh(g, dist, ctx.rank, halo=1, include_pole=True)
+                fs = R.NodeColumns(mesh, c)
+                f = fs.create_field("n", levels, kind)
+                own = fs.owned_row_index()
+                f.host[own] = gvals[mesh.node_global[own]]
+                m0 = (ctx.messages_sent, ctx.bytes_sent, ctx.messages_received)
+                gathered = R.gather_field(fs, f, c)
+                m1 = (ctx.messages_sent, ctx.bytes_sent, ctx.messages_received)
+                sfs = R.StructuredColumns(g, dist, ctx.rank)
+                sf = sfs.create_field("s", levels, kind)
+                R.scatter_field(sfs, sf, c, gvals[: g.npts] if ctx.rank == 0 else None)
+                m2 = (ctx.messages_sent, ctx.bytes_sent, ctx.messages_received)
+                return gathered, np.array([np.subtract(m1, m0), np.subtract(m2, m1)]), sf.host.copy()
+            res = R.run_ranks(P, program)
+            out[f"{tag}_p{P}_gathered"] = res[0][0]
+            for r in range(P):
+                out[f"{tag}_p{P}_r{r}_counters"] = res[r][1]
+                out[f"{tag}_p{P}_r{r}_scattered"] = res[r][2]
+    save("gather_scatter", **out)
+
+
 JOBS = {
     "rotated": rotated,
     "degenerate": degenerate,
+    "gather_scatter": gather_scatter,
     "checksum": checksums,
     "latitudes": latitudes,
     "cfg1": lambda: serial_remap("O32", "O16", 10, "cfg1_O32_O16"),
