@@ -373,14 +373,33 @@ def emulated_halo(sg, S, L, flush, parts=8, halo=2, partitioner="equal_regions",
             t.append(Event.elapsed_ms(e0, e1))
         ms.append(statistics.median(t))
         nbytes.append(sum(len(v) for v in plans[r].recv.values()) * L * 8)
+    # all ranks' signalled pulls (the N>1 exchange kernel, csrc/step.cu) as ONE launch
+    from paper_1908_07038_b200.execute import emulated_exchanges, launch_exchanges
+
+    xs = emulated_exchanges(list(zip(plans, fields)))
+    launch_exchanges(xs)
+    t = []
+    for _ in range(reps):
+        flush()
+        e0, e1 = Event(0), Event(0)
+        e0.record()
+        launch_exchanges(xs)
+        e1.record()
+        t.append(Event.elapsed_ms(e0, e1))
+    one = statistics.median(t)
+    epochs = [x.check() for x in xs]
+    del xs
     for d in fields:
         d.close()
     worst = max(ms)
     return {"bytes_per_exchange": int(sum(nbytes)), "ms": worst, "GB_per_s": sum(nbytes) / (worst * 1e-3) / 1e9,
+            "signalled_one_launch_ms": one, "signalled_one_launch_GB_per_s": sum(nbytes) / (one * 1e-3) / 1e9,
+            "signalled_epochs": epochs,
             "worst_rank_bytes": int(nbytes[int(np.argmax(ms))]), "per_rank_ms": [round(x, 4) for x in ms],
             "scope": f"cfg4 point O1280, {L} lev, halo {halo}, {partitioner} P={parts}, EMULATED on one GPU: "
-                     "all ranks' fields in this GPU's HBM, each rank's fused pull kernel timed alone with L2 "
-                     "flushed; ms = max over ranks. Not NVLink (needs >1 GPU)"}
+                     "all ranks' fields in this GPU's HBM, each rank's pull kernel timed alone with L2 "
+                     "flushed (ms = max over ranks), and all ranks' signalled pulls as one launch "
+                     "(signalled_one_launch_ms). HBM, not NVLink (needs >1 GPU)"}
 
 
 def emulated_fused_step(sg, source, target, L, parts=8, partitioner="equal_regions", reps=10):
@@ -677,7 +696,7 @@ def run_multi(args):
         if not args.fused:
             raise SystemExit(f"rank {rank}: first step failed: {err}")
         # explicit, reported: the line carries transport_fallback and step.fused = false
-        fallback = f"fused step failed ({err or 'on another rank'}); pack -> {args.transport} -> unpack used"
+        fallback = f"fused step failed ({err or 'on another rank'}); exchange ({args.transport}) + apply used"
         log(f"rank {rank}: {fallback}")
         run = DistributedRemap(fs, w, ctx, f.device, tf.device, variant=args.variant, fused=False)
         run.step()
@@ -730,20 +749,38 @@ def run_multi(args):
     worst_kern_ms = allreduce([kern_ms], dist.ReduceOp.MAX)[0]
     worst_bytes = allreduce([my_bytes if kern_ms == worst_kern_ms else 0.0], dist.ReduceOp.MAX)[0]
     # halo exchange alone (bytes over NVLink)
-    ctx.barrier()
-    if args.transport == "nccl":
-        h0, h1 = Event(local), Event(local)
-        h0.record(run.halo.stream)
-        for _ in range(args.steps):
-            fs.exchange_plan.exchange_nccl(f.device, ctx.nccl_comm(), run.halo.stream)
-        h1.record(run.halo.stream)
-        run.halo.synchronize()
-        halo_ms = Event.elapsed_ms(h0, h1) / args.steps
-    else:  # host-synchronised pull: wall clock, barriers included
+    from paper_1908_07038_b200.parallel import _signalled_exchange
+
+    def exchanger(plan, d, stream, transport=args.transport):
+        """(run, device-timed?, label) of the halo exchange of ``plan`` on ``d`` (collective)."""
+        if transport == "nccl":
+            return (lambda: plan.exchange_nccl(d, ctx.nccl_comm(), stream)), True, "nccl pack/send/recv/unpack"
+        if transport == "nvlink":
+            x = _signalled_exchange(ctx, plan, d)
+            if x is not None:
+                return (lambda: x.launch(stream)), True, "signalled pull over NVLink, one kernel per rank"
+        return (lambda: ctx.device_exchange(plan, d, stream)), False, "pull kernel between host barriers"
+
+    def time_exchange(run_x, timed, stream, reps):
+        if timed:
+            a0, a1 = Event(local), Event(local)
+            a0.record(stream)
+            for _ in range(reps):
+                run_x()
+            a1.record(stream)
+            sg.synchronize(local, stream)
+            return Event.elapsed_ms(a0, a1) / reps
         tt = time.perf_counter()
-        for _ in range(args.steps):
-            ctx.device_exchange(fs.exchange_plan, f.device)
-        halo_ms = (time.perf_counter() - tt) * 1e3 / args.steps
+        for _ in range(reps):
+            run_x()
+        return (time.perf_counter() - tt) * 1e3 / reps
+
+    ctx.barrier()
+    hx, htimed, hlabel = exchanger(fs.exchange_plan, f.device, run.halo.stream)
+    hx()
+    sg.synchronize(local, run.halo.stream)
+    ctx.barrier()
+    halo_ms = time_exchange(hx, htimed, run.halo.stream, args.steps)
     send_bytes = float(sum(len(v) for v in fs.exchange_plan.send.values()) * L * 8)
     hmax = allreduce([halo_ms], dist.ReduceOp.MAX)[0]
     hsum = allreduce([send_bytes], dist.ReduceOp.SUM)[0]
@@ -790,8 +827,8 @@ def run_multi(args):
               "e2e_target_rows_bitwise": oks[2] == 1.0, "targets_checked": int(msum),
               "against": "per rank: analytic field on every local row (owned + ghost) and the oracle apply "
                          "(interp.py:219-223) on the rank's own stencils"}
-    comm = {"transport": args.transport, "transport_fallback": fallback}
-    if args.transport == "nccl":
+    comm = {"transport": args.transport, "transport_fallback": fallback, "exchange": hlabel}
+    if ndev >= world:
         info = ctx.comm_info()
         nr = allreduce([float(info["nranks"])], dist.ReduceOp.MIN)[0]
         comm.update({"nccl_nranks": int(nr), "nccl_version": info["nccl_version"],
@@ -814,41 +851,33 @@ def run_multi(args):
             init = np.where(mh.node_ghost[:, None], -1.0, vals)
             d.upload(init)
 
-            def exchange():
-                if args.transport == "nccl":
-                    plan.exchange_nccl(d, ctx.nccl_comm(), hs.stream)
-                else:
-                    ctx.device_exchange(plan, d, hs.stream)
-
-            exchange()
-            hs.synchronize()
-            ok = bool(np.array_equal(d.to_numpy(), vals))
-            for _ in range(3):
-                exchange()
-            hs.synchronize()
-            ctx.barrier()
-            if args.transport == "nccl":
-                a0, a1 = Event(local), Event(local)
-                a0.record(hs.stream)
-                for _ in range(args.steps):
-                    exchange()
-                a1.record(hs.stream)
-                hs.synchronize()
-                ms_h = Event.elapsed_ms(a0, a1) / args.steps
-            else:
-                tt = time.perf_counter()
-                for _ in range(args.steps):
-                    exchange()
-                ms_h = (time.perf_counter() - tt) * 1e3 / args.steps
             rb = float(sum(len(v) for v in plan.recv.values()) * L * 8)
-            r = allreduce([ms_h, rb, rb, float(ok), float(len(plan.peers))], dist.ReduceOp.MAX)
             tot = allreduce([rb], dist.ReduceOp.SUM)[0]
-            okmin = allreduce([float(ok)], dist.ReduceOp.MIN)[0]
-            sweep.append({"halo": h, "bytes_per_exchange": tot, "worst_rank_recv_bytes": r[2], "ms": r[0],
-                          "GB_per_s": tot / (r[0] * 1e-3) / 1e9, "max_peers": int(r[4]),
-                          "ghosts_bitwise": okmin == 1.0,
-                          "timing": "device events on the exchange stream" if args.transport == "nccl"
-                          else "wall clock incl. host barriers"})
+            entry = {"halo": h, "bytes_per_exchange": tot}
+            # the transport of the run, then NCCL (the library baseline) when each rank has a GPU
+            transports = [args.transport] + (["nccl"] if args.transport != "nccl" and ndev >= world else [])
+            for k, tr in enumerate(transports):
+                d.upload(init)
+                xrun, xtimed, xlabel = exchanger(plan, d, hs.stream, tr)
+                xrun()
+                sg.synchronize(local, hs.stream)
+                ok = bool(np.array_equal(d.to_numpy(), vals))
+                for _ in range(3):
+                    xrun()
+                sg.synchronize(local, hs.stream)
+                ctx.barrier()
+                ms_h = time_exchange(xrun, xtimed, hs.stream, args.steps)
+                r = allreduce([ms_h, rb, float(len(plan.peers))], dist.ReduceOp.MAX)
+                okmin = allreduce([float(ok)], dist.ReduceOp.MIN)[0]
+                res = {"ms": r[0], "GB_per_s": tot / (r[0] * 1e-3) / 1e9, "worst_rank_recv_bytes": r[1],
+                       "max_peers": int(r[2]), "ghosts_bitwise": okmin == 1.0, "exchange": xlabel,
+                       "timing": "device events on the exchange stream, max over ranks" if xtimed
+                       else "wall clock incl. host barriers, max over ranks"}
+                if k == 0:
+                    entry.update(res)
+                else:
+                    entry["nccl_baseline"] = res
+            sweep.append(entry)
             d.close()
 
     if rank == 0:
@@ -886,8 +915,7 @@ def run_multi(args):
         }
         print(json.dumps(line), flush=True)
     ctx.barrier()
-    if args.transport == "ipc":
-        ctx.close_ipc()
+    ctx.close_ipc()
     dist.destroy_process_group()
 
 
@@ -917,8 +945,11 @@ def main():
                          "transport -> unpack with the interior apply overlapped")
     ap.add_argument("--no-halo-sweep", action="store_true",
                     help="N>1: skip the cfg4 sweep (halo widths 1..3 exchanged on every rank)")
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
-                    help="N>1 halo exchange: NCCL send/recv (one GPU per rank) or CUDA-IPC pull")
+    ap.add_argument("--transport", default="nvlink", choices=["nvlink", "nccl", "ipc"],
+                    help="N>1 halo exchange (cfg4 sweep, --no-fused steps): nvlink = one signalled pull "
+                         "kernel per rank over CUDA-IPC mappings (ranks sharing a GPU: pull between host "
+                         "barriers); nccl = pack -> NCCL send/recv -> unpack; ipc = pull between host barriers. "
+                         "With nvlink the sweep also times NCCL as the library baseline")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rule)")

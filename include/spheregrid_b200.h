@@ -267,6 +267,17 @@ int32_t sg_step_info(uint64_t step, int64_t* out_m, int64_t* out_n_boundary);
 int32_t sg_step_launch(const uint64_t* steps, int32_t n, int32_t wait_done, uint64_t stream);
 int32_t sg_step_check(uint64_t step, uint64_t* out_error, uint64_t* out_epoch);
 int32_t sg_step_set_timeout(uint64_t step, uint64_t timeout_ns);
+/* The halo exchange alone, signalled (functionspace.py:107-118; cfg4): one signal kernel + one
+ * pull kernel per rank — a warp per ghost row waits for its owner's ready word and copies the
+ * owner's row (recv_remote) through the peer pointer; the last row publishes done.  Same
+ * signal words, launch rules (n > 1 on one GPU => wait_done = 0) and timeout as the step;
+ * sg_exchange_signal returns the signal handle (check its error word with sg_signal_read). */
+int32_t sg_exchange_create(uint64_t plan, uint64_t field, uint64_t signal, const uint64_t* peer_ptrs,
+                           const int64_t* peer_pitch_elems, const uint64_t* peer_flag_ptrs,
+                           uint64_t* out_exchange);
+int32_t sg_exchange_launch(const uint64_t* exchanges, int32_t n, int32_t wait_done, uint64_t stream);
+int32_t sg_exchange_set_timeout(uint64_t exchange, uint64_t timeout_ns);
+int32_t sg_exchange_signal(uint64_t exchange, uint64_t* out_signal);
 
 /* Partition-invariant digest of owned rows [row0, row0+nrows) whose global ids are gids
  * (functionspace.py:233-254): the wrapping u64 sum of splitmix64(gid*G + (level+1)*Lv ^ bits);

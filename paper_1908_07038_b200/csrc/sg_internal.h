@@ -13,7 +13,7 @@
 
 namespace sg {
 
-enum class ObjKind : int { Field = 1, Locator, Stencil, Plan, Comm, MeshGen, Event, Stream, Graph, Signal, Step };
+enum class ObjKind : int { Field = 1, Locator, Stencil, Plan, Comm, MeshGen, Event, Stream, Graph, Signal, Step, Exchange };
 
 struct Object {
   explicit Object(ObjKind k) : kind(k) {}

@@ -29,6 +29,7 @@
 //
 // Arithmetic identical to the apply kernels: bitwise equal to interp.py:219-223.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -66,9 +67,13 @@ struct PeerTable {
   int32_t npeers;
   int32_t rank[kMaxPeers];
   int32_t role[kMaxPeers];
-  const double* base[kMaxPeers];
-  int64_t pitch[kMaxPeers];
+  union {
+    const double* base[kMaxPeers];
+    const void* base_any[kMaxPeers];
+  };
+  int64_t pitch[kMaxPeers];  // elements
   unsigned long long* flags[kMaxPeers];
+  bool sys[kMaxPeers];  // the peer is another GPU: flag accesses at system scope
 };
 
 // Everything a target warp needs, passed BY VALUE in the kernel parameters (constant bank):
@@ -99,13 +104,22 @@ struct Group {
   int32_t wait_done;
 };
 
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+// Scope of a flag access: .sys when the other side of the flag is another GPU (NVLink / IPC),
+// .gpu when it is this GPU (ranks of a single-GPU emulation) — a .sys release under load costs
+// tens of µs more than a .gpu one (tools/xchg_sweep.py, profiles/r02_fused_step.md).
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p, bool sys) {
   unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  if (sys)
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v, bool sys) {
+  if (sys)
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long now_ns() {
   unsigned long long t;
@@ -114,10 +128,10 @@ __device__ __forceinline__ unsigned long long now_ns() {
 }
 // Spin until *p >= e; false (and the error word set) after timeout_ns.
 __device__ bool wait_geq(const unsigned long long* p, unsigned long long e, unsigned long long* err, int code,
-                         unsigned long long timeout_ns) {
-  if (ld_acquire_sys(p) >= e) return true;
+                         unsigned long long timeout_ns, bool sys) {
+  if (ld_acquire(p, sys) >= e) return true;
   const unsigned long long t0 = now_ns();
-  while (ld_acquire_sys(p) < e) {
+  while (ld_acquire(p, sys) < e) {
     __nanosleep(64);
     if (now_ns() - t0 > timeout_ns) {
       atomicExch(err, (unsigned long long)code);
@@ -135,6 +149,16 @@ __device__ __forceinline__ double ld_local(const double* p) {  // read-only for 
 __device__ __forceinline__ double ld_any(const double* p) {  // peer rows: written before the acquire
   double v;
   asm volatile("ld.global.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_weak(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.global.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned int ld_weak(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.global.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ double combine(double w0, double w1, double w2, double x, double y, double z) {
@@ -198,33 +222,37 @@ __device__ __forceinline__ void apply_target(const StepArgs& d, int64_t t, int4 
   }
 }
 
-__global__ void signal_kernel(Group g) {
-  const int r = threadIdx.x;
-  if (r >= g.n) return;
-  const StepArgs& d = g.d[r];
-  unsigned long long* f = d.flags;
-  const unsigned long long e = f[w_epoch(d.nranks)] + 1;
-  f[w_cur(d.nranks)] = e;
-  __threadfence_system();  // the owned rows written by earlier work on this stream, then the flag
-  const PeerTable& P = *d.peers;
-  for (int s = 0; s < P.npeers; ++s)
-    if (P.role[s] & kRoleSend) st_release_sys(P.flags[s] + w_ready(d.rank), e);
-}
 
 // The rank's last act of a step (one thread): tell the owners I am done reading their rows,
 // then (one GPU per rank) wait until every reader of my rows is done; epoch = e.
-__device__ void finish_step(const StepArgs& d, unsigned long long e, int wait_done) {
-  unsigned long long* f = d.flags;
-  const int nr = d.nranks;
-  const PeerTable& P = *d.peers;
-  __threadfence_system();
+__device__ void finish_epoch(unsigned long long* f, int nr, int rank, const PeerTable& P, unsigned long long e,
+                             int wait_done, unsigned long long timeout_ns) {
+  // each st.release.sys orders this thread's (and, through the acq_rel count, every counted
+  // block's) earlier reads of the peers' rows before the done word
   for (int s = 0; s < P.npeers; ++s)
-    if (P.role[s] & kRoleRecv) st_release_sys(P.flags[s] + w_done(nr, d.rank), e);
+    if (P.role[s] & kRoleRecv) st_release(P.flags[s] + w_done(nr, rank), e, P.sys[s]);
   if (wait_done)
     for (int s = 0; s < P.npeers; ++s)
-      if (P.role[s] & kRoleSend) wait_geq(f + w_done(nr, P.rank[s]), e, f + w_error(nr), 2, d.timeout_ns);
+      if (P.role[s] & kRoleSend) wait_geq(f + w_done(nr, P.rank[s]), e, f + w_error(nr), 2, timeout_ns, P.sys[s]);
   f[w_count(nr)] = 0;
   f[w_epoch(nr)] = e;
+}
+__device__ void finish_step(const StepArgs& d, unsigned long long e, int wait_done) {
+  finish_epoch(d.flags, d.nranks, d.rank, *d.peers, e, wait_done, d.timeout_ns);
+}
+// ready[me] = epoch + 1 into every reader's words (one thread per rank)
+__device__ void publish_ready(unsigned long long* f, int nr, int rank, const PeerTable& P) {
+  const unsigned long long e = f[w_epoch(nr)] + 1;
+  f[w_cur(nr)] = e;
+  // the owned rows were written by earlier kernels of this stream (complete); the release store
+  // orders them before the ready word at system scope — no separate fence.sc.sys (18 µs here)
+  for (int s = 0; s < P.npeers; ++s)
+    if (P.role[s] & kRoleSend) st_release(P.flags[s] + w_ready(rank), e, P.sys[s]);
+}
+
+__global__ void signal_kernel(Group g) {
+  const int r = threadIdx.x;
+  if (r < g.n) publish_ready(g.d[r].flags, g.d[r].nranks, g.d[r].rank, *g.d[r].peers);
 }
 
 constexpr int kWarps = 2;  // targets per block: small blocks retire and refill (apply.cu)
@@ -255,7 +283,7 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(Group g) {
   {  // every owner of my ghosts has published its rows for epoch e (each lane acquires)
     const PeerTable& P = *d.peers;
     for (int s = 0; s < P.npeers; ++s)
-      if (P.role[s] & kRoleRecv) wait_geq(f + w_ready(P.rank[s]), e, f + w_error(nr), 1, d.timeout_ns);
+      if (P.role[s] & kRoleRecv) wait_geq(f + w_ready(P.rank[s]), e, f + w_error(nr), 1, d.timeout_ns, P.sys[s]);
   }
   apply_target<ITERS, true>(d, t, id, lane);
   __syncwarp();
@@ -278,6 +306,118 @@ __global__ void count_boundary(const int4* idx, int64_t m, int k, int64_t ghost_
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
 }
 
+// ---- the halo exchange alone, signalled (cfg4): ghost rows pulled from their owners ----
+// functionspace.py:107-118 as one kernel per rank: warp per ghost row, waits for the owner's
+// ready word, copies the owner's row (recv_remote) through the peer pointer into the ghost
+// row; the last row's warp publishes done to the owners and waits for its own readers.
+struct XchgArgs {
+  void* base;
+  int64_t pitch;  // elements (= words of the item size)
+  int32_t W;      // words per row (levels)
+  const int32_t* rows;    // ghost rows (local)
+  const int32_t* remote;  // owner row of each ghost
+  const int32_t* slot;    // owner's plan peer slot of each ghost
+  int64_t n;
+  unsigned long long* flags;
+  unsigned long long timeout_ns;
+  int32_t nranks, rank;
+  const PeerTable* peers;
+};
+
+struct XGroup {
+  XchgArgs d[kMaxGroup];
+  int64_t start[kMaxGroup + 1];
+  int32_t n;
+  int32_t wait_done;
+};
+
+constexpr int kXWarps = 8;
+
+__global__ void xsignal_kernel(XGroup g) {
+  const int r = threadIdx.x;
+  if (r < g.n) publish_ready(g.d[r].flags, g.d[r].nranks, g.d[r].rank, *g.d[r].peers);
+}
+
+// acq_rel RMW at gpu scope: orders this block's peer reads (made visible to thread 0 by the
+// preceding __syncthreads) before the count the finisher acquires.
+__device__ __forceinline__ unsigned long long atom_add_acq_rel(unsigned long long* p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+
+// A block moves kXRows ghost rows per warp (kXWarps warps): thread 0 first acquires the
+// owners' ready words (one L1 invalidation per block), then every warp issues the loads of all
+// its rows before its stores (4 rows x IT words in flight per lane: the copy is latency-bound
+// otherwise); the last block to finish (acq_rel count) finishes the epoch.
+constexpr int kXRows = 4;
+constexpr int kXBlocksPerSM = 4;  // 256 threads x 64 registers: 4 resident blocks per SM
+
+template <typename Wd, int IT>
+__global__ void __launch_bounds__(kXWarps * 32) xchg_kernel(XGroup g) {
+  int r = 0;
+  while (r + 1 < g.n && (int64_t)blockIdx.x >= g.start[r + 1]) ++r;
+  const XchgArgs& d = g.d[r];
+  const int64_t b = (int64_t)blockIdx.x - g.start[r], nb = g.start[r + 1] - g.start[r];
+  const int lane = threadIdx.x & 31;
+  unsigned long long* f = d.flags;
+  const int nr = d.nranks;
+  const PeerTable& P = *d.peers;
+  __shared__ unsigned long long e_sh;
+  if (threadIdx.x == 0) {
+    const unsigned long long e = *(volatile unsigned long long*)(f + w_cur(nr));
+    e_sh = e;
+    if (d.n > 0)
+      for (int s = 0; s < P.npeers; ++s)
+        if (P.role[s] & kRoleRecv) wait_geq(f + w_ready(P.rank[s]), e, f + w_error(nr), 1, d.timeout_ns, P.sys[s]);
+  }
+  __syncthreads();
+  // resident grid: each warp moves kXRows rows per iteration, blocks stride over the rank's rows
+  for (int64_t i0 = (b * kXWarps + (threadIdx.x >> 5)) * kXRows; i0 < d.n; i0 += nb * kXWarps * kXRows) {
+    if (IT > 0) {
+      const Wd* src[kXRows];
+      Wd* dst[kXRows];
+#pragma unroll
+      for (int q = 0; q < kXRows; ++q) {
+        const int64_t i = min(i0 + q, d.n - 1);  // a short tail repeats the last row (idempotent)
+        const int s = __ldg(d.slot + i);
+        src[q] = static_cast<const Wd*>(P.base_any[s]) + (int64_t)__ldg(d.remote + i) * P.pitch[s];
+        dst[q] = static_cast<Wd*>(d.base) + (int64_t)__ldg(d.rows + i) * d.pitch;
+      }
+      Wd v[kXRows][IT > 0 ? IT : 1];
+#pragma unroll
+      for (int q = 0; q < kXRows; ++q)
+#pragma unroll
+        for (int k = 0; k < IT; ++k)
+          if (lane + 32 * k < d.W) v[q][k] = ld_weak(src[q] + lane + 32 * k);
+#pragma unroll
+      for (int q = 0; q < kXRows; ++q)
+#pragma unroll
+        for (int k = 0; k < IT; ++k)
+          if (lane + 32 * k < d.W) dst[q][lane + 32 * k] = v[q][k];
+    } else {
+      for (int64_t i = i0; i < min(i0 + kXRows, d.n); ++i) {
+        const int s = __ldg(d.slot + i);
+        const Wd* src = static_cast<const Wd*>(P.base_any[s]) + (int64_t)__ldg(d.remote + i) * P.pitch[s];
+        Wd* dst = static_cast<Wd*>(d.base) + (int64_t)__ldg(d.rows + i) * d.pitch;
+        for (int k = lane; k < d.W; k += 32) dst[k] = ld_weak(src + k);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && atom_add_acq_rel(f + w_count(nr), 1ull) == (unsigned long long)(nb - 1))
+    finish_epoch(f, nr, d.rank, P, e_sh, g.wait_done, d.timeout_ns);  // all reads of peers' rows done
+}
+
+struct Exchange : Object {
+  Exchange() : Object(ObjKind::Exchange) {}
+  int device = 0;
+  int itemsize = 8;
+  XchgArgs args{};
+  DevBuf peers;  // PeerTable
+  uint64_t signal = 0;
+};
+
 struct Step : Object {
   Step() : Object(ObjKind::Step) {}
   int device = 0;
@@ -286,6 +426,36 @@ struct Step : Object {
   int64_t nblocks = 0;
   uint64_t signal = 0;
 };
+
+// Peers of a plan for a signalled launch: role bits from the plan's send / recv lists, the
+// owners' field pointers (needed where this rank receives) and every peer's signal words.
+PeerTable peer_table(const Plan* p, const Signal* sig, const uint64_t* peer_ptrs, const int64_t* peer_pitch_elems,
+                     const uint64_t* peer_flag_ptrs) {
+  const size_t np = p->peers.size();
+  SG_REQUIRE(np == 0 || (peer_ptrs && peer_pitch_elems && peer_flag_ptrs), "null peer arrays");
+  SG_REQUIRE(p->recv_off.back() == 0 || p->has_remote,
+             "plan has ghosts without an owner row (recv_remote); signalled peer reads need them");
+  PeerTable pt{};
+  pt.npeers = (int32_t)np;
+  for (size_t i = 0; i < np; ++i) {
+    SG_REQUIRE(p->peers[i] >= 0 && p->peers[i] < sig->nranks && p->peers[i] != sig->rank,
+               "plan peer %d is not another rank of %d", p->peers[i], sig->nranks);
+    SG_REQUIRE(peer_flag_ptrs[i] != 0, "null signal words for peer %d", p->peers[i]);
+    pt.rank[i] = p->peers[i];
+    pt.role[i] = (p->recv_off[i + 1] > p->recv_off[i] ? kRoleRecv : 0) |
+                 (p->send_off[i + 1] > p->send_off[i] ? kRoleSend : 0);
+    SG_REQUIRE(!(pt.role[i] & kRoleRecv) || peer_ptrs[i] != 0, "null field pointer for peer %d", p->peers[i]);
+    pt.base_any[i] = reinterpret_cast<const void*>(peer_ptrs[i]);
+    pt.pitch[i] = peer_pitch_elems[i];
+    pt.flags[i] = reinterpret_cast<unsigned long long*>(peer_flag_ptrs[i]);
+    // the peer's signal words live on this GPU (same-device ranks) or another one
+    cudaPointerAttributes at{};
+    const bool known = cudaPointerGetAttributes(&at, pt.flags[i]) == cudaSuccess && at.type == cudaMemoryTypeDevice;
+    if (!known) cudaGetLastError();
+    pt.sys[i] = !(known && at.device == sig->device);
+  }
+  return pt;
+}
 
 }  // namespace
 }  // namespace sg
@@ -363,27 +533,10 @@ int32_t sg_step_create(uint64_t stencil, uint64_t plan, uint64_t src_field, uint
                  sig->device == s->device,
              "stencil, plan, fields and signal live on different devices");
   SG_REQUIRE(s->m < INT32_MAX, "too many targets");
-  const size_t np = p->peers.size();
-  SG_REQUIRE(np == 0 || (peer_ptrs && peer_pitch_elems && peer_flag_ptrs), "null peer arrays");
-  SG_REQUIRE(p->recv_off.back() == 0 || p->has_remote,
-             "plan has ghosts without an owner row (recv_remote); the fused step needs them");
   auto st = std::make_unique<Step>();
   st->device = s->device;
   st->signal = signal;
-  PeerTable pt{};
-  pt.npeers = (int32_t)np;
-  for (size_t i = 0; i < np; ++i) {
-    SG_REQUIRE(p->peers[i] >= 0 && p->peers[i] < sig->nranks && p->peers[i] != sig->rank,
-               "plan peer %d is not another rank of %d", p->peers[i], sig->nranks);
-    SG_REQUIRE(peer_flag_ptrs[i] != 0, "null signal words for peer %d", p->peers[i]);
-    pt.rank[i] = p->peers[i];
-    pt.role[i] = (p->recv_off[i + 1] > p->recv_off[i] ? kRoleRecv : 0) |
-                 (p->send_off[i + 1] > p->send_off[i] ? kRoleSend : 0);
-    SG_REQUIRE(!(pt.role[i] & kRoleRecv) || peer_ptrs[i] != 0, "null field pointer for peer %d", p->peers[i]);
-    pt.base[i] = reinterpret_cast<const double*>(peer_ptrs[i]);
-    pt.pitch[i] = peer_pitch_elems[i];
-    pt.flags[i] = reinterpret_cast<unsigned long long*>(peer_flag_ptrs[i]);
-  }
+  const PeerTable pt = peer_table(p, sig, peer_ptrs, peer_pitch_elems, peer_flag_ptrs);
   DeviceScope ds(s->device);
   st->peers.alloc(s->device, sizeof(PeerTable));
   SG_CUDA(cudaMemcpy(st->peers.ptr, &pt, sizeof(PeerTable), cudaMemcpyHostToDevice));
@@ -489,6 +642,113 @@ int32_t sg_step_check(uint64_t step, uint64_t* out_error, uint64_t* out_epoch) {
   if (w[w_error(sig->nranks)])
     throw_error(SG_DOMAIN_ERROR, "SpheregridError: fused step of rank %d timed out waiting for a peer (%s)", sig->rank,
                 w[w_error(sig->nranks)] == 1 ? "owner rows never published" : "reader never finished");
+  SG_API_END
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int32_t sg_exchange_create(uint64_t plan, uint64_t field, uint64_t signal, const uint64_t* peer_ptrs,
+                           const int64_t* peer_pitch_elems, const uint64_t* peer_flag_ptrs, uint64_t* out_exchange) {
+  SG_API_BEGIN
+  Plan* p = get<Plan>(plan, ObjKind::Plan);
+  Field* f = get<Field>(field, ObjKind::Field);
+  Signal* sig = get<Signal>(signal, ObjKind::Signal);
+  SG_REQUIRE(out_exchange, "null out pointer");
+  if (f->npts != p->nnodes)
+    throw_error(SG_DOMAIN_ERROR, "PlanMismatch: field has %lld points, plan covers %lld nodes", (long long)f->npts,
+                (long long)p->nnodes);
+  SG_REQUIRE(f->device == p->device && sig->device == p->device, "plan, field and signal live on different devices");
+  SG_REQUIRE(f->itemsize == 4 || f->itemsize == 8, "item size %d", f->itemsize);
+  auto x = std::make_unique<Exchange>();
+  x->device = p->device;
+  x->signal = signal;
+  x->itemsize = f->itemsize;
+  const PeerTable pt = peer_table(p, sig, peer_ptrs, peer_pitch_elems, peer_flag_ptrs);
+  DeviceScope ds(p->device);
+  x->peers.alloc(p->device, sizeof(PeerTable));
+  SG_CUDA(cudaMemcpy(x->peers.ptr, &pt, sizeof(PeerTable), cudaMemcpyHostToDevice));
+  XchgArgs& d = x->args;
+  d.base = f->buf.ptr;
+  d.pitch = f->pitch;
+  d.W = f->levels;
+  d.rows = p->recv_rows.as<int32_t>();
+  d.remote = p->recv_remote.as<int32_t>();
+  d.slot = p->recv_peer.as<int32_t>();
+  d.n = p->recv_off.back();
+  d.flags = sig->words.as<unsigned long long>();
+  d.timeout_ns = kTimeoutNs;
+  d.nranks = sig->nranks;
+  d.rank = sig->rank;
+  d.peers = x->peers.as<PeerTable>();
+  *out_exchange = registry_put(x.release());
+  SG_API_END
+}
+
+int32_t sg_exchange_launch(const uint64_t* exchanges, int32_t n, int32_t wait_done, uint64_t stream) {
+  SG_API_BEGIN
+  SG_REQUIRE(exchanges && n >= 1 && n <= kMaxGroup, "1..%d exchanges per launch", kMaxGroup);
+  SG_REQUIRE(!(n > 1 && wait_done), "a multi-rank launch on one GPU cannot wait for its own ranks (wait_done=0)");
+  XGroup g{};
+  g.n = n;
+  g.wait_done = wait_done ? 1 : 0;
+
+  int device = -1, item = 0, W = 0;
+  for (int i = 0; i < n; ++i) {
+    Exchange* x = get<Exchange>(exchanges[i], ObjKind::Exchange);
+    if (i == 0) device = x->device, item = x->itemsize, W = x->args.W;
+    SG_REQUIRE(x->device == device && x->itemsize == item && x->args.W == W,
+               "exchanges of one launch must share device, item size and levels");
+    g.d[i] = x->args;
+  }
+  // grid: one block per kXWarps * kXRows ghost rows, at most a resident grid (kXBlocksPerSM
+  // blocks per SM) per launch shared among its ranks — each block acquires and counts once;
+  // at least one block per rank (it publishes the epoch even without ghosts)
+  int nsm = 148;
+  SG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+  const int64_t cap = std::max<int64_t>(1, (int64_t)nsm * kXBlocksPerSM / n);
+  for (int i = 0; i < n; ++i)
+    g.start[i + 1] = g.start[i] + std::min<int64_t>(cap, std::max<int64_t>(1, (g.d[i].n + kXWarps * kXRows - 1) /
+                                                                                  (kXWarps * kXRows)));
+  DeviceScope ds(device);
+  cudaStream_t s = as_stream(stream);
+  xsignal_kernel<<<1, 32, 0, s>>>(g);
+  SG_CUDA_LAUNCH();
+  const unsigned grid = (unsigned)g.start[n];
+  const int it = (W + 31) / 32;
+#define SG_XLAUNCH(Wd)                                                            \
+  switch (it) {                                                                   \
+    case 1: xchg_kernel<Wd, 1><<<grid, kXWarps * 32, 0, s>>>(g); break;           \
+    case 2: xchg_kernel<Wd, 2><<<grid, kXWarps * 32, 0, s>>>(g); break;           \
+    case 3: xchg_kernel<Wd, 3><<<grid, kXWarps * 32, 0, s>>>(g); break;           \
+    case 4: xchg_kernel<Wd, 4><<<grid, kXWarps * 32, 0, s>>>(g); break;           \
+    case 5: xchg_kernel<Wd, 5><<<grid, kXWarps * 32, 0, s>>>(g); break;           \
+    default: xchg_kernel<Wd, 0><<<grid, kXWarps * 32, 0, s>>>(g); break;          \
+  }
+  if (item == 8) {
+    SG_XLAUNCH(unsigned long long)
+  } else {
+    SG_XLAUNCH(unsigned int)
+  }
+#undef SG_XLAUNCH
+  SG_CUDA_LAUNCH();
+  SG_API_END
+}
+
+int32_t sg_exchange_set_timeout(uint64_t exchange, uint64_t timeout_ns) {
+  SG_API_BEGIN
+  Exchange* x = get<Exchange>(exchange, ObjKind::Exchange);
+  SG_REQUIRE(timeout_ns > 0, "timeout must be positive");
+  x->args.timeout_ns = timeout_ns;
+  SG_API_END
+}
+
+int32_t sg_exchange_signal(uint64_t exchange, uint64_t* out_signal) {
+  SG_API_BEGIN
+  Exchange* x = get<Exchange>(exchange, ObjKind::Exchange);
+  SG_REQUIRE(out_signal, "null out pointer");
+  *out_signal = x->signal;
   SG_API_END
 }
 

@@ -61,6 +61,17 @@ class Signal(N.Handle):
         N.call("sg_signal_ptr", self.handle, N.ref(p))
         self.ptr = p.value
 
+    def check(self) -> int:
+        """Raises if a device-side wait timed out; returns the last completed epoch."""
+        w = self.read()
+        if w["error"]:
+            from .errors import SpheregridError
+
+            raise SpheregridError(f"signalled launch of rank {self.rank} timed out waiting for a peer ("
+                                  + ("owner rows never published" if w["error"] == 1 else "reader never finished")
+                                  + ")")
+        return w["epoch"]
+
     def read(self) -> dict:
         w = np.zeros(2 * self.nranks + 4, np.uint64)
         N.call("sg_signal_read", self.handle, N.ptr(w), len(w))
@@ -136,8 +147,16 @@ class DistributedRemap:
         # NCCL: stream-ordered exchange, overlappable and graph-capturable.  Otherwise
         # (in-process ranks, CUDA-IPC pull) the exchange is host-synchronised: no overlap.
         self.fused = bool(fused) and self.multi
-        self.stream_ordered = self.multi and not self.fused and getattr(ctx, "transport", None) == "nccl"
-        self.comm = ctx.nccl_comm() if self.stream_ordered else None
+        transport = getattr(ctx, "transport", None)
+        # not fused: the exchange is stream-ordered (and overlaps the interior targets) with NCCL
+        # or, every rank on its own GPU, the signalled pull kernel (transport "nvlink")
+        self.xchg = None
+        if self.multi and not self.fused and transport == "nvlink":
+            from .parallel import _signalled_exchange
+
+            self.xchg = _signalled_exchange(ctx, self.plan, src)
+        self.stream_ordered = self.multi and not self.fused and (transport == "nccl" or self.xchg is not None)
+        self.comm = ctx.nccl_comm() if self.stream_ordered and self.xchg is None else None
         self.peer_info = ctx.peer_fields(src, self.plan) if self.fused else None
         # fused with one GPU per rank: device-side signalling, one kernel per rank per step.
         # The decision is collective (identical on every rank): every rank on its own GPU.
@@ -162,6 +181,8 @@ class DistributedRemap:
             return applies
         if not self.stream_ordered:
             return 1 + int(sum(len(v) for v in self.plan.recv.values()) > 0)  # pull + apply
+        if self.xchg is not None:
+            return 2 + applies  # signal + pull
         n = int(sum(len(v) for v in self.plan.send.values()) > 0)  # pack
         n += int(sum(len(v) for v in self.plan.recv.values()) > 0)  # unpack
         return n + applies
@@ -194,7 +215,10 @@ class DistributedRemap:
             return
         self.ev_fork.record(main)
         self.halo.wait(self.ev_fork)
-        self.plan.exchange_nccl(self.src, self.comm, self.halo.stream)
+        if self.xchg is not None:
+            self.xchg.launch(self.halo.stream)
+        else:
+            self.plan.exchange_nccl(self.src, self.comm, self.halo.stream)
         self.ev_halo.record(self.halo.stream)
         self._apply(self.interior, main)  # overlaps the exchange
         self.main.wait(self.ev_halo)
@@ -217,6 +241,8 @@ class DistributedRemap:
         self.main.synchronize()
         if self.fused_step is not None:
             self.fused_step.check()
+        if self.xchg is not None:
+            self.xchg.check()
 
 
 def emulated_fused_steps(ranks: Sequence[tuple]) -> List[FusedStep]:
@@ -234,3 +260,59 @@ def emulated_fused_steps(ranks: Sequence[tuple]) -> List[FusedStep]:
     peer_sigs = [(s.ptr, uuid) for s in sigs]
     return [FusedStep(w, plan, src, dst, sigs[r], peer_info, peer_sigs)
             for r, (w, plan, src, dst) in enumerate(ranks)]
+
+
+class SignalledExchange(N.Handle):
+    """The halo exchange of ``plan`` on ``field`` (a DeviceArray) as one pull kernel per rank
+    with device-side signalling (sg_exchange_create): every ghost row is copied from its
+    owner's field once the owner published its epoch.  ``peer_info`` / ``peer_sigs`` as for
+    FusedStep."""
+
+    def __init__(self, plan, field: DeviceArray, signal: Signal, peer_info, peer_sigs):
+        dev = field.device
+        peers = plan.peers
+        ptrs = np.array([peer_info[p][0] for p in peers] or [0], np.uint64)
+        pitch = np.array([peer_info[p][1] for p in peers] or [0], np.int64)
+        flags = np.array([peer_sigs[p][0] for p in peers] or [0], np.uint64)
+        h = C.c_uint64(0)
+        N.call("sg_exchange_create", plan.native(dev), field.handle, signal.handle, N.ptr(ptrs), N.ptr(pitch),
+               N.ptr(flags), N.ref(h))
+        super().__init__(h.value)
+        self.signal, self.device = signal, dev
+        self.nghosts = sum(len(v) for v in plan.recv.values())
+        self._keep = (plan, field)
+
+    def launch(self, stream: int = 0) -> None:
+        launch_exchanges([self], stream, wait_done=True)
+
+    def set_timeout(self, seconds: float) -> None:
+        N.call("sg_exchange_set_timeout", self.handle, max(1, int(seconds * 1e9)))
+
+    def check(self) -> int:
+        return self.signal.check()
+
+    @classmethod
+    def for_rank(cls, ctx, plan, field: DeviceArray) -> "SignalledExchange":
+        """Collective: every rank of ``ctx`` (all on distinct GPUs) builds its exchange."""
+        info = ctx.peer_fields(field, plan)
+        sig = Signal(field.device, ctx.nranks, ctx.rank)
+        return cls(plan, field, sig, info, ctx.peer_signals(sig))
+
+
+def launch_exchanges(xs: Sequence[SignalledExchange], stream: int = 0, wait_done: bool = False) -> None:
+    arr = np.array([x.handle for x in xs], np.uint64)
+    N.call("sg_exchange_launch", N.ptr(arr), len(arr), int(bool(wait_done)), stream)
+
+
+def emulated_exchanges(ranks: Sequence[tuple]) -> List[SignalledExchange]:
+    """Signalled exchanges of P ranks on ONE GPU, for one ``launch_exchanges(xs)``:
+    ``ranks[r]`` = (plan, DeviceArray) of rank r."""
+    P = len(ranks)
+    dev = ranks[0][1].device
+    if any(f.device != dev for _, f in ranks):
+        raise ValueError("an emulated launch needs every rank on one device")
+    sigs = [Signal(dev, P, r) for r in range(P)]
+    uuid = N.device_uuid(dev)
+    info = [(f.ptr, f.pitch, dev) for _, f in ranks]
+    psig = [(s.ptr, uuid) for s in sigs]
+    return [SignalledExchange(plan, f, sigs[r], info, psig) for r, (plan, f) in enumerate(ranks)]

@@ -192,15 +192,45 @@ class RankContext:
         return self.share((signal.ptr, N.device_uuid(signal.device)))
 
     def device_exchange(self, plan, dev_array, stream: int = 0) -> None:
-        """Fused device halo exchange over peer memory: one pull kernel per rank on
-        ``stream``, between two barriers (owners' rows final before, not overwritten while
-        peers read)."""
+        """Device halo exchange over peer memory.  Every rank on its own GPU: one signalled
+        pull kernel per rank (owners' ready words, no host barrier).  Ranks sharing a GPU: one
+        pull kernel per rank between two host barriers (owners' rows final before, not
+        overwritten while peers read)."""
+        x = _signalled_exchange(self, plan, dev_array)
+        if x is not None:
+            x.launch(stream)
+            D.synchronize(dev_array.device, stream)
+            x.check()
+            return
         ptrs = self.peer_fields(dev_array, plan)
         D.synchronize(dev_array.device, stream)
         self.barrier()
         plan.pull(dev_array, ptrs, stream)
         D.synchronize(dev_array.device, stream)
         self.barrier()
+
+
+def _signalled_exchange(ctx, plan, dev_array):
+    """The signalled pull exchange (execute.SignalledExchange) of ``plan`` on ``dev_array`` when
+    every rank drives its own GPU, else None.  Collective on every call (ranks decide together
+    whether to reuse their cached objects, so a rank whose field buffer changed never leaves
+    the others in a different collective); at most 4 cached objects per rank, FIFO."""
+    from . import _native as N
+    from .execute import SignalledExchange
+
+    cache = ctx.__dict__.setdefault("_xcache", [])
+    key = (id(plan), dev_array.ptr, dev_array.handle)
+    hit = next((x for k, x in cache if k == key), None)
+    everyone = ctx.share((hit is not None, N.device_uuid(dev_array.device)))
+    if len({u for _, u in everyone}) != ctx.nranks:
+        return None  # ranks share a GPU: spinning launches must not wait on each other there
+    if all(h for h, _ in everyone):
+        return hit
+    x = SignalledExchange.for_rank(ctx, plan, dev_array)
+    cache.append((key, x))
+    if len(cache) > 4:
+        cache.pop(0)
+    return x
 
 
 def _default_devices() -> List[int]:
@@ -260,13 +290,15 @@ class DistContext:
     Host messages (plan build, gather) travel on a gloo group as uint8 tensors; counters
     mirror the reference.  ``device_exchange`` uses the library's NCCL communicator."""
 
-    def __init__(self, group=None, device: Optional[int] = None, transport: str = "nccl"):
-        """transport: "nccl" (pack -> grouped ncclSend/ncclRecv -> unpack, stream-ordered) or
-        "ipc" (fused pull kernel over CUDA-IPC mappings of the owners' fields, host barriers
-        around it; works for several processes on one GPU too)."""
+    def __init__(self, group=None, device: Optional[int] = None, transport: str = "nvlink"):
+        """transport: "nvlink" (default: one signalled pull kernel per rank over CUDA-IPC
+        mappings of the owners' fields, owners' ready words instead of barriers; ranks that
+        share a GPU fall back to "ipc"), "nccl" (pack -> grouped ncclSend/ncclRecv -> unpack,
+        stream-ordered) or "ipc" (pull kernel over CUDA-IPC mappings between two host
+        barriers; works for several processes on one GPU too)."""
         import torch.distributed as dist
 
-        if transport not in ("nccl", "ipc"):
+        if transport not in ("nvlink", "nccl", "ipc"):
             raise ValueError(f"unknown transport {transport!r}")
         self.transport = transport
         self._ipc: Dict[int, tuple] = {}  # peer rank -> (ipc handle bytes, mapped ptr, device)
@@ -449,6 +481,13 @@ class DistContext:
             plan.exchange_nccl(dev_array, self.nccl_comm(), stream)
             D.synchronize(dev_array.device, stream)
             return
+        if self.transport == "nvlink":
+            x = _signalled_exchange(self, plan, dev_array)
+            if x is not None:
+                x.launch(stream)
+                D.synchronize(dev_array.device, stream)
+                x.check()
+                return
         peers = self.peer_fields(dev_array)
         D.synchronize(dev_array.device, stream)
         self.barrier()  # every owner's rows are final

@@ -69,7 +69,7 @@ def test_ipc_pull_exchange_processes(gpu, world):
     assert all(o[1] and o[2] for o in out), out
 
 
-@pytest.mark.parametrize("extra", [["--no-fused"], ["--fused"]])
+@pytest.mark.parametrize("extra", [["--no-fused"], ["--fused"], ["--no-fused", "--transport", "nvlink"]])
 def test_bench_torchrun_two_processes(gpu, extra):
     """The driver's N>1 launch line (torch.distributed.run, one process per rank) end to end on
     the one GPU of the test box: bench.py --gpus 2 with the CUDA-IPC transport on cfg2 (equal
@@ -82,7 +82,8 @@ def test_bench_torchrun_two_processes(gpu, extra):
 
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
-           "--steps", "3", "--warmup", "3", "--transport", "ipc", "--config", "cfg2"] + extra
+           "--steps", "3", "--warmup", "3", "--config", "cfg2"] + (extra if "--transport" in extra
+                                                                     else ["--transport", "ipc"] + extra)
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
@@ -91,6 +92,8 @@ def test_bench_torchrun_two_processes(gpu, extra):
     assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
     assert line["step"]["fused"] == ("--fused" in extra) and line["comm"]["transport_fallback"] is None
     assert line["step"]["device_signalled"] is False  # two ranks on one GPU: host barriers
+    if "nvlink" in extra:  # signalled pulls need one GPU per rank: explicit host-barrier pull here
+        assert line["comm"]["exchange"] == "pull kernel between host barriers"
     p = line["parity"]
     assert p["source_rows_bitwise"] and p["target_rows_bitwise"] and p["e2e_target_rows_bitwise"], p
     assert [h["halo"] for h in line["halo_sweep"]] == [1, 2, 3]

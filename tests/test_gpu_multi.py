@@ -29,17 +29,21 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("extra", [["--no-fused"], ["--fused"], ["--partitioner", "blocks"]])
+@pytest.mark.parametrize("extra", [["--no-fused", "--transport", "nccl"], ["--fused", "--transport", "nccl"],
+                                   ["--partitioner", "blocks", "--transport", "nccl"], ["--no-fused"], []])
 def test_torchrun_nccl_two_gpus_bitwise(extra):
     if _ngpus() < 2:
         pytest.skip("needs >= 2 GPUs (one NCCL rank per device)")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
-           "--steps", "5", "--warmup", "3", "--config", "cfg2", "--transport", "nccl"] + extra
+           "--steps", "5", "--warmup", "3", "--config", "cfg2"] + extra
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
-    assert line["n_gpus"] == 2 and line["comm"]["transport"] == "nccl" and line["comm"]["nccl_nranks"] == 2
+    assert line["n_gpus"] == 2 and line["comm"]["nccl_nranks"] == 2
+    if "nccl" not in extra:  # default transport: the signalled NVLink pull, NCCL timed beside it
+        assert line["comm"]["exchange"].startswith("signalled pull")
+        assert all("nccl_baseline" in h and h["nccl_baseline"]["ghosts_bitwise"] for h in line["halo_sweep"])
     assert line["comm"]["transport_fallback"] is None
     # fused is the default: one kernel per rank with device-side signalling over NVLink
     assert line["step"]["device_signalled"] == ("--no-fused" not in extra)

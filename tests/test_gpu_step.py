@@ -119,3 +119,61 @@ def test_step_refuses_bad_launches(gpu):
     arr = np.array([s.handle for s in steps], np.uint64)
     with pytest.raises(N.NativeError, match="wait_done"):  # ranks of one launch cannot wait for each other
         N.call("sg_step_launch", N.ptr(arr), 2, 1, 0)
+
+
+@pytest.mark.parametrize("grid,P,halo,part,kind,levels", [("O32", 2, 1, "blocks", "REAL64", 137),
+                                                         ("O48", 4, 2, "equal_regions", "INT32", 3),
+                                                         ("F16", 8, 3, "equal_regions", "REAL32", 33),
+                                                         ("O24", 3, 2, "blocks", "INT64", 1),
+                                                         ("O32", 5, 2, "blocks", "REAL64", 300)])
+def test_emulated_signalled_exchange(gpu, grid, P, halo, part, kind, levels):
+    """The halo exchange alone as one signalled pull kernel per rank (sg_exchange_*), P ranks in
+    one launch on one GPU: every ghost row equals its owner's values (functionspace.py:107-118),
+    owned rows untouched, signal words = epochs, for every field kind and level count."""
+    sg = gpu
+    from paper_1908_07038_b200.device import DeviceArray, synchronize
+    from paper_1908_07038_b200.execute import emulated_exchanges, launch_exchanges
+    from paper_1908_07038_b200.partition import PARTITIONERS
+
+    S = sg.grid_from_name(grid)
+    dist = PARTITIONERS[part](S, P)
+    K = getattr(sg.Kind, kind)
+
+    def prog(ctx):
+        mesh = sg.generate_mesh(S, dist, ctx.rank, halo=halo, include_pole=True)
+        plan = sg.NodeColumns(mesh, ctx).exchange_plan
+        expect = (mesh.node_global[:, None] * 7 + np.arange(levels)[None, :] % 5).astype(K.dtype)
+        d = DeviceArray(mesh.nb_nodes, levels, K.dtype)
+        d.upload(np.where(mesh.node_ghost[:, None], 0, expect).astype(K.dtype))
+        return plan, d, expect
+
+    ranks = sg.run_ranks(P, prog, devices=[0])
+    xs = emulated_exchanges([(plan, d) for plan, d, _ in ranks])
+    for _ in range(2):
+        launch_exchanges(xs)
+    synchronize(0)
+    for (plan, d, expect), x in zip(ranks, xs):
+        assert np.array_equal(d.to_numpy(), expect)
+        w = x.signal.read()
+        assert w["epoch"] == 2 and w["error"] == 0 and w["count"] == 0
+        assert all(w["ready"][p] == 2 for p in plan.recv) and all(w["done"][p] == 2 for p in plan.send)
+
+
+def test_signalled_exchange_times_out_without_owner(gpu):
+    sg = gpu
+    from paper_1908_07038_b200.device import DeviceArray, synchronize
+    from paper_1908_07038_b200.execute import emulated_exchanges, launch_exchanges
+
+    S = sg.grid_from_name("O16")
+    dist = sg.blocks_partition(S, 2)
+
+    def prog(ctx):
+        mesh = sg.generate_mesh(S, dist, ctx.rank, halo=1, include_pole=True)
+        return sg.NodeColumns(mesh, ctx).exchange_plan, DeviceArray(mesh.nb_nodes, 2, np.float64)
+
+    xs = emulated_exchanges(sg.run_ranks(2, prog, devices=[0]))
+    xs[0].set_timeout(1e-3)
+    launch_exchanges(xs[:1])  # rank 1 never publishes its rows
+    synchronize(0)
+    with pytest.raises(sg.SpheregridError, match="timed out"):
+        xs[0].check()
