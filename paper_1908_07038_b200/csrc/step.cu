@@ -268,7 +268,11 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(Group g) {
   const int64_t b = (int64_t)blockIdx.x - g.start[r];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t t = b * kWarps + warp;
-  if (t >= d.m) return;
+  if (t >= d.m) {
+    if (d.m == 0 && t == 0 && lane == 0)  // no targets: still tell the owners, wait for readers
+      finish_step(d, *(volatile unsigned long long*)(d.flags + w_cur(d.nranks)), g.wait_done);
+    return;
+  }
   const int4 id = __ldg(d.idx + t);
   const int hi = max(max(id.x, id.y), d.k == 4 ? max(id.z, id.w) : id.z);
   if (hi < d.ghost_lo) {  // interior: local rows only, no wait

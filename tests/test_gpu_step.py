@@ -39,7 +39,8 @@ def _ranks(sg, S, T, P, L, part, gvals, halo=2):
 @pytest.mark.parametrize("S,T,P,L,part", [("O64", "O32", 2, 20, "blocks"), ("O64", "O32", 4, 137, "equal_regions"),
                                           ("O96", "O48", 8, 137, "equal_regions"), ("O64", "O32", 8, 3, "blocks"),
                                           ("F32", "F16", 3, 33, "blocks"), ("O32", "O64", 4, 137, "blocks"),
-                                          ("O48", "O96", 8, 40, "equal_regions"), ("F16", "O32", 5, 200, "blocks")])
+                                          ("O48", "O96", 8, 40, "equal_regions"), ("F16", "O32", 5, 200, "blocks"),
+                                          ("O48", "O4", 8, 5, "blocks")])  # ranks without targets
 def test_emulated_fused_step_bitwise(gpu, S, T, P, L, part):
     sg = gpu
     from oracle import oracle as O

@@ -176,3 +176,68 @@ def test_create_field_without_gpu_is_plain_numpy():
         pytest.skip("a GPU is present")
     f = sg.create_field("x", (F.PIN_HOST_BYTES // 8 + 1, 1))
     assert isinstance(f.host, np.ndarray) and f.host.base is None and not f.host.any()
+
+
+class _FakeArray:
+    def __init__(self, ptr, handle):
+        self.ptr, self.handle, self.device = ptr, handle, 0
+
+
+def _gloo_signal_worker(rank, world, port, q, same_gpu):
+    """The collective decisions behind the signalled exchange (parallel._signalled_exchange):
+    ranks agree on signalled vs host-barrier mode from the device UUIDs, and on cache reuse,
+    even when one rank's field buffer changes between calls (the ADVICE r1 hazard)."""
+    import torch.distributed as dist
+
+    import paper_1908_07038_b200._native as N
+    import paper_1908_07038_b200.execute as E
+    import paper_1908_07038_b200.parallel as PAR
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ.setdefault("GLOO_SOCKET_IFNAME", "lo")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        N.device_uuid = lambda dev: b"one-gpu" if same_gpu else bytes([rank]) * 16
+        built = []
+
+        class FakeExchange:
+            @classmethod
+            def for_rank(cls, ctx, plan, field):
+                ctx.share(("build", field.ptr))  # collective, like peer_fields / peer_signals
+                built.append(field.ptr)
+                return cls()
+
+        E.SignalledExchange = FakeExchange
+        ctx = sg.DistContext(device=0)
+        plan = object()
+        a, b = _FakeArray(1000 + rank, 1), _FakeArray(2000 + rank, 2)
+        seq = [a, a, b if rank == 1 else a, a, a]
+        got = [PAR._signalled_exchange(ctx, plan, x) for x in seq]
+        q.put((rank, [g is None for g in got], built))
+        ctx.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("same_gpu", [False, True])
+def test_signalled_exchange_decisions_are_collective(same_gpu):
+    import torch.multiprocessing as mp
+
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_signal_worker, args=(r, world, port, q, same_gpu)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    if same_gpu:  # spinning launches must not wait on each other on one GPU: never signalled
+        assert all(o[1] == [True] * 5 and o[2] == [] for o in out)
+    else:
+        assert all(o[1] == [False] * 5 for o in out)
+        # call 1 builds; call 3 rebuilds on BOTH ranks because rank 1's buffer changed
+        assert [len(o[2]) for o in out] == [2, 2]
+        assert out[1][2] == [1001, 2001] and out[0][2] == [1000, 1000]
