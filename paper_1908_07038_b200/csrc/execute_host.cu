@@ -6,6 +6,7 @@
 // stencil), gather (the same compact device copy, filled by a GPU kernel that reads only the
 // referenced rows straight out of the pinned, mapped user array: no host CPU work, no DMA of
 // unreferenced rows) and zero-copy (the apply kernel reads/writes pinned host memory directly).
+#include <cub/cub.cuh>
 #include <emmintrin.h>
 
 #include <algorithm>
@@ -28,6 +29,8 @@ struct CompactRun {
 
 struct HostPlan {
   int nchunks = 0;
+  bool host_tables = false;  // idx_host / mark_host / runs / t_end built on the host
+  bool device_gather = false;  // gather-mode tables (t_end, cb, cidx, pieces) built on the device
   std::vector<int64_t> t_end;                                  // chunk c: targets [t_end[c-1], t_end[c])
   std::vector<std::vector<std::pair<int64_t, int64_t>>> runs;  // chunk c: referenced source rows
   int64_t rows_copied = 0;
@@ -205,32 +208,6 @@ void launch_gather_tma(const double* host, int64_t host_rows, const int2* pieces
 
 namespace {
 
-// Pieces of the referenced runs for `levels` (rebuilt when the level count changes).
-void build_pieces(int device, HostPlan* hp, int levels) {
-  const int prows = gather_piece_rows(levels);
-  if (hp->piece_levels == levels && hp->piece_rows == prows) return;
-  std::vector<int2> pcs;
-  std::vector<int64_t> dst;
-  hp->pb.assign(hp->nchunks + 1, 0);
-  for (int c = 0; c < hp->nchunks; ++c) {
-    hp->pb[c] = (int64_t)pcs.size();
-    for (const auto& r : hp->cruns[c])
-      for (int64_t q = 0; q < r.len; q += prows) {
-        pcs.push_back(make_int2((int)(r.src + q), (int)std::min<int64_t>(prows, r.len - q)));
-        dst.push_back(r.dst + q);
-      }
-  }
-  hp->pb[hp->nchunks] = (int64_t)pcs.size();
-  hp->pieces.alloc(device, std::max<size_t>(pcs.size(), 1) * sizeof(int2));
-  hp->pdst.alloc(device, std::max<size_t>(dst.size(), 1) * sizeof(int64_t));
-  if (!pcs.empty()) {
-    SG_CUDA(cudaMemcpy(hp->pieces.ptr, pcs.data(), pcs.size() * sizeof(int2), cudaMemcpyHostToDevice));
-    SG_CUDA(cudaMemcpy(hp->pdst.ptr, dst.data(), dst.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
-  }
-  hp->piece_levels = levels;
-  hp->piece_rows = prows;
-}
-
 HostPool& host_pool() {
   static HostPool pool(std::max(1u, std::min(32u, std::thread::hardware_concurrency())) - 1);
   return pool;
@@ -304,6 +281,24 @@ HostPlan* host_plan(Stencil* s, int nchunks) {
   auto owned = std::make_unique<HostPlan>();
   hp = owned.get();
   hp->nchunks = nchunks;
+  SG_CUDA(cudaStreamCreateWithFlags(&hp->s_in, cudaStreamNonBlocking));
+  SG_CUDA(cudaStreamCreateWithFlags(&hp->s_cmp, cudaStreamNonBlocking));
+  SG_CUDA(cudaStreamCreateWithFlags(&hp->s_out, cudaStreamNonBlocking));
+  hp->ev_in.resize(nchunks);
+  hp->ev_cmp.resize(nchunks);
+  for (int c = 0; c < nchunks; ++c) {
+    SG_CUDA(cudaEventCreateWithFlags(&hp->ev_in[c], cudaEventDisableTiming));
+    SG_CUDA(cudaEventCreateWithFlags(&hp->ev_cmp[c], cudaEventDisableTiming));
+  }
+  s->host_plan = owned.release();
+  return hp;
+}
+
+// Host-side tables of the dma / compact modes: the stencil copied down, referenced rows,
+// the target ranges each chunk of source rows completes, referenced runs per chunk.
+void host_tables(Stencil* s, HostPlan* hp) {
+  if (hp->host_tables) return;
+  const int nchunks = hp->nchunks;
   const int64_t m = s->m, n = s->source_nnodes;
   std::vector<int4> idx((size_t)m);
   if (m) SG_CUDA(cudaMemcpy(idx.data(), s->idx.ptr, (size_t)m * sizeof(int4), cudaMemcpyDeviceToHost));
@@ -321,8 +316,9 @@ HostPlan* host_plan(Stencil* s, int nchunks) {
     pmax[t] = run_max;  // monotone: targets [0, t] need source rows <= pmax[t]
   }
   int64_t tprev = 0, rprev = 0;
-  hp->t_end.resize(nchunks);
-  hp->runs.resize(nchunks);
+  hp->t_end.assign(nchunks, 0);
+  hp->runs.assign(nchunks, {});
+  hp->rows_copied = 0;
   for (int c = 0; c < nchunks; ++c) {
     const int64_t rb = (c + 1 == nchunks) ? n : n * (c + 1) / nchunks;  // source rows [rprev, rb)
     int64_t te = (c + 1 == nchunks) ? m : (int64_t)(std::lower_bound(pmax.begin(), pmax.end(), rb) - pmax.begin());
@@ -350,19 +346,206 @@ HostPlan* host_plan(Stencil* s, int nchunks) {
   }
   hp->idx_host = std::move(idx);
   hp->mark_host = std::move(mark);
-  SG_CUDA(cudaStreamCreateWithFlags(&hp->s_in, cudaStreamNonBlocking));
-  SG_CUDA(cudaStreamCreateWithFlags(&hp->s_cmp, cudaStreamNonBlocking));
-  SG_CUDA(cudaStreamCreateWithFlags(&hp->s_out, cudaStreamNonBlocking));
-  hp->ev_in.resize(nchunks);
-  hp->ev_cmp.resize(nchunks);
-  for (int c = 0; c < nchunks; ++c) {
-    SG_CUDA(cudaEventCreateWithFlags(&hp->ev_in[c], cudaEventDisableTiming));
-    SG_CUDA(cudaEventCreateWithFlags(&hp->ev_cmp[c], cudaEventDisableTiming));
-  }
-  s->host_plan = owned.release();
-  return hp;
+  hp->host_tables = true;
 }
 
+// ---- gather-mode tables built on the device (the default host-field path) ---------------------
+// Same layout as host_tables + build_compact(period 0) on the host: compact row of a
+// referenced source row = exclusive scan of the referenced flags; pieces = maximal runs of
+// referenced rows inside a chunk of source rows, cut every piece_rows rows; t_end[c] = first
+// target whose prefix-max stencil row reaches the next chunk.  ~10 ms instead of ~180 ms of
+// host loops and pageable uploads at cfg3 (first call of apply_remap on host fields).
+__global__ void plan_mark(const int4* idx, int64_t m, int k, int32_t* mark, int32_t* tmax) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  const int4 id = idx[t];
+  mark[id.x] = 1;
+  mark[id.y] = 1;
+  mark[id.z] = 1;
+  int hi = max(id.x, max(id.y, id.z));
+  if (k == 4) {
+    mark[id.w] = 1;
+    hi = max(hi, id.w);
+  }
+  tmax[t] = hi;
+}
+
+struct MaxOp {
+  __device__ __forceinline__ int32_t operator()(int32_t a, int32_t b) const { return a > b ? a : b; }
+};
+
+__device__ __forceinline__ int64_t chunk_lo(int64_t n, int nchunks, int c) { return n * c / nchunks; }
+
+// candidate segment start of row i (a referenced row that starts a run or a chunk), else -1
+__global__ void plan_starts(const int32_t* mark, int64_t n, int nchunks, int32_t* cand) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool start = false;
+  if (mark[i]) {
+    // chunk c holds rows [n*c/nchunks, n*(c+1)/nchunks); i starts a chunk iff i == chunk_lo(c(i))
+    int c = (int)((i * nchunks) / n);
+    while (c + 1 < nchunks && chunk_lo(n, nchunks, c + 1) <= i) ++c;
+    while (c > 0 && chunk_lo(n, nchunks, c) > i) --c;
+    start = i == 0 || !mark[i - 1] || i == chunk_lo(n, nchunks, c);
+  }
+  cand[i] = start ? (int32_t)i : -1;
+}
+
+__global__ void plan_piece_flags(const int32_t* mark, const int32_t* seg, int64_t n, int prows,
+                                 unsigned char* flag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  flag[i] = mark[i] && ((i - seg[i]) % prows == 0);
+}
+
+__global__ void plan_pieces(const int32_t* starts, int64_t np, const int32_t* seg, const int32_t* cpos,
+                            const int32_t* mark, int64_t n, int nchunks, int prows, int2* pieces,
+                            int64_t* pdst) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= np) return;
+  const int32_t st = starts[k];
+  int len = 1;
+  while (len < prows && st + len < n && mark[st + len] && seg[st + len] == seg[st]) ++len;
+  pieces[k] = make_int2(st, len);
+  pdst[k] = cpos[st];
+}
+
+__global__ void plan_cidx(const int4* idx, int64_t m, int k, const int32_t* cpos, int4* cidx) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  const int4 id = idx[t];
+  cidx[t] = make_int4(cpos[id.x], cpos[id.y], cpos[id.z], k == 4 ? cpos[id.w] : 0);
+}
+
+// per chunk c: t_end (first target t with pmax[t] >= rb_c), cb = cpos[rlo_c], pb = first piece
+// starting at or after rlo_c
+__global__ void plan_chunks(const int32_t* pmax, int64_t m, const int32_t* cpos, const int32_t* starts, int64_t np,
+                            int64_t n, int nchunks, int64_t* t_end, int64_t* cb, int64_t* pb) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > nchunks) return;
+  const int64_t lo = c == nchunks ? n : chunk_lo(n, nchunks, c);
+  cb[c] = cpos[lo];
+  int64_t a = 0, b = np;  // first piece with start >= lo
+  while (a < b) {
+    const int64_t mid = (a + b) / 2;
+    if (starts[mid] < lo) a = mid + 1; else b = mid;
+  }
+  pb[c] = a;
+  if (c < nchunks) {
+    const int64_t rb = c + 1 == nchunks ? n : chunk_lo(n, nchunks, c + 1);
+    int64_t x = 0, y = m;  // lower_bound(pmax, rb)
+    while (x < y) {
+      const int64_t mid = (x + y) / 2;
+      if (pmax[mid] < rb) x = mid + 1; else y = mid;
+    }
+    t_end[c] = c + 1 == nchunks ? m : x;
+  }
+}
+
+struct PlanBuf {  // a slice of the plan's temporary arena
+  void* ptr;
+  size_t bytes;
+  template <class T>
+  T* as() const { return static_cast<T*>(ptr); }
+};
+
+void device_gather_tables(Stencil* s, HostPlan* hp, int levels, cudaStream_t st) {
+  const int prows = gather_piece_rows(levels);
+  if (hp->device_gather && hp->piece_rows == prows) return;
+  const int nchunks = hp->nchunks;
+  const int64_t m = s->m, n = s->source_nnodes;
+  SG_REQUIRE(n < INT32_MAX && m < INT32_MAX, "too large for the device plan");
+  const int dev = s->device;
+  // one arena for every temporary (a cudaMalloc per buffer cost ~10 ms each here)
+  struct Part {
+    size_t off, bytes;
+  };
+  size_t arena_bytes = 0;
+  auto part = [&](size_t bytes) {
+    Part p{arena_bytes, bytes};
+    arena_bytes += (bytes + 255) / 256 * 256;
+    return p;
+  };
+  const size_t nn = (size_t)std::max<int64_t>(n, 1), mm = (size_t)std::max<int64_t>(m, 1);
+  const Part p_mark = part((nn + 1) * 4), p_tmax = part(mm * 4), p_pmax = part(mm * 4), p_cpos = part((nn + 1) * 4),
+             p_cand = part(nn * 4), p_seg = part(nn * 4), p_flag = part(nn), p_starts = part(nn * 4), p_nsel = part(8),
+             p_tend = part((size_t)nchunks * 8), p_cb = part((size_t)(nchunks + 1) * 8),
+             p_pb = part((size_t)(nchunks + 1) * 8);
+  // CUB temp storage: sized with null pointers first
+  size_t b1 = 0, b2 = 0, b3 = 0, b4 = 0;
+  SG_CUDA(cub::DeviceScan::InclusiveScan(nullptr, b1, (int32_t*)nullptr, (int32_t*)nullptr, MaxOp(), (int)mm, st));
+  SG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b2, (int32_t*)nullptr, (int32_t*)nullptr, (int)(nn + 1), st));
+  SG_CUDA(cub::DeviceScan::InclusiveScan(nullptr, b3, (int32_t*)nullptr, (int32_t*)nullptr, MaxOp(), (int)nn, st));
+  SG_CUDA(cub::DeviceSelect::Flagged(nullptr, b4, cub::CountingInputIterator<int32_t>(0), (unsigned char*)nullptr,
+                                     (int32_t*)nullptr, (int64_t*)nullptr, (int)nn, st));
+  const Part p_tmp = part(std::max(std::max(b1, b2), std::max(b3, b4)) + 16);
+  DevBuf arena;
+  arena.alloc(dev, arena_bytes);
+  auto buf = [&](Part p) { return PlanBuf{arena.as<char>() + p.off, p.bytes}; };
+  const PlanBuf mark = buf(p_mark), tmax = buf(p_tmax), pmax = buf(p_pmax), cpos = buf(p_cpos), cand = buf(p_cand),
+            seg = buf(p_seg), flag = buf(p_flag), starts = buf(p_starts), nsel = buf(p_nsel), t_end = buf(p_tend),
+            cb = buf(p_cb), pb = buf(p_pb), tmp = buf(p_tmp);
+  SG_CUDA(cudaMemsetAsync(mark.ptr, 0, mark.bytes, st));
+  const unsigned gm = (unsigned)((m + 255) / 256), gn = (unsigned)((n + 255) / 256);
+  if (m) plan_mark<<<gm, 256, 0, st>>>(s->idx.as<int4>(), m, s->k, mark.as<int32_t>(), tmax.as<int32_t>());
+  SG_CUDA_LAUNCH();
+  size_t tb = tmp.bytes;
+  if (m) SG_CUDA(cub::DeviceScan::InclusiveScan(tmp.ptr, tb, tmax.as<int32_t>(), pmax.as<int32_t>(), MaxOp(), (int)m, st));
+  tb = tmp.bytes;  // mark[n] is the zero pad: cpos[n] = U
+  SG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, tb, mark.as<int32_t>(), cpos.as<int32_t>(), (int)(n + 1), st));
+  if (n) {
+    plan_starts<<<gn, 256, 0, st>>>(mark.as<int32_t>(), n, nchunks, cand.as<int32_t>());
+    SG_CUDA_LAUNCH();
+    tb = tmp.bytes;
+    SG_CUDA(cub::DeviceScan::InclusiveScan(tmp.ptr, tb, cand.as<int32_t>(), seg.as<int32_t>(), MaxOp(), (int)n, st));
+    plan_piece_flags<<<gn, 256, 0, st>>>(mark.as<int32_t>(), seg.as<int32_t>(), n, prows, flag.as<unsigned char>());
+    SG_CUDA_LAUNCH();
+    tb = tmp.bytes;
+    SG_CUDA(cub::DeviceSelect::Flagged(tmp.ptr, tb, cub::CountingInputIterator<int32_t>(0), flag.as<unsigned char>(),
+                                       starts.as<int32_t>(), nsel.as<int64_t>(), (int)n, st));
+  } else {
+    SG_CUDA(cudaMemsetAsync(nsel.ptr, 0, 8, st));
+  }
+  int64_t np = 0;
+  int32_t U = 0;
+  SG_CUDA(cudaMemcpyAsync(&np, nsel.ptr, 8, cudaMemcpyDeviceToHost, st));
+  SG_CUDA(cudaMemcpyAsync(&U, cpos.as<int32_t>() + n, 4, cudaMemcpyDeviceToHost, st));
+  SG_CUDA(cudaStreamSynchronize(st));
+  hp->pieces.alloc(dev, (size_t)std::max<int64_t>(np, 1) * sizeof(int2));
+  hp->pdst.alloc(dev, (size_t)std::max<int64_t>(np, 1) * sizeof(int64_t));
+  hp->cidx.alloc(dev, (size_t)std::max<int64_t>(m, 1) * sizeof(int4));
+  if (np) {
+    plan_pieces<<<(unsigned)((np + 255) / 256), 256, 0, st>>>(starts.as<int32_t>(), np, seg.as<int32_t>(),
+                                                             cpos.as<int32_t>(), mark.as<int32_t>(), n, nchunks,
+                                                             prows, hp->pieces.as<int2>(), hp->pdst.as<int64_t>());
+    SG_CUDA_LAUNCH();
+  }
+  if (m) {
+    plan_cidx<<<gm, 256, 0, st>>>(s->idx.as<int4>(), m, s->k, cpos.as<int32_t>(), hp->cidx.as<int4>());
+    SG_CUDA_LAUNCH();
+  }
+  plan_chunks<<<(nchunks + 1 + 127) / 128, 128, 0, st>>>(pmax.as<int32_t>(), m, cpos.as<int32_t>(),
+                                                        starts.as<int32_t>(), np, n, nchunks, t_end.as<int64_t>(),
+                                                        cb.as<int64_t>(), pb.as<int64_t>());
+  SG_CUDA_LAUNCH();
+  std::vector<int64_t> te(nchunks);
+  hp->cb.assign(nchunks + 1, 0);
+  hp->pb.assign(nchunks + 1, 0);
+  SG_CUDA(cudaMemcpyAsync(te.data(), t_end.ptr, (size_t)nchunks * 8, cudaMemcpyDeviceToHost, st));
+  SG_CUDA(cudaMemcpyAsync(hp->cb.data(), cb.ptr, (size_t)(nchunks + 1) * 8, cudaMemcpyDeviceToHost, st));
+  SG_CUDA(cudaMemcpyAsync(hp->pb.data(), pb.ptr, (size_t)(nchunks + 1) * 8, cudaMemcpyDeviceToHost, st));
+  SG_CUDA(cudaStreamSynchronize(st));
+  int64_t tprev = 0;
+  hp->t_end.assign(nchunks, 0);
+  for (int c = 0; c < nchunks; ++c) hp->t_end[c] = tprev = std::max(te[c], tprev);
+  hp->ncompact = U;
+  hp->direct.assign(nchunks, 0);
+  hp->piece_levels = levels;
+  hp->piece_rows = prows;
+  hp->period = 0;
+  hp->compact_ready = false;  // the host compact tables (cruns, gsrc) are not built
+  hp->device_gather = true;
+}
 
 }  // namespace
 
@@ -444,24 +627,33 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
   std::vector<const double*> gsrc_host(gather ? nfields : 0);
   for (int f = 0; f < (int)gsrc_host.size(); ++f)
     gsrc_host[f] = static_cast<const double*>(mapped(host_src[f], "gather"));
-  if (compact) {
-    const int period = gather ? 0 : (flags >> 8) & 0xff;
-    if (!hp->compact_ready || hp->period != period) build_compact(s, hp, hp->idx_host, hp->mark_host, period);
-    // device compact sources and the pinned staging ring (sized for the largest chunk)
-    size_t maxc = 0;
-    for (int c = 0; c < nchunks; ++c)
-      if (!hp->direct[c]) maxc = std::max<size_t>(maxc, (size_t)(hp->cb[c + 1] - hp->cb[c]));
-    const size_t need = std::max<size_t>(maxc * row, 16);
-    if (!gather && (hp->ring_bytes < need || hp->ring_fields < nfields)) {
-      for (void* q : hp->ring)
-        if (q) cudaFreeHost(q);
-      hp->ring.assign((size_t)nfields * HostPlan::kRing, nullptr);
-      for (auto& q : hp->ring) SG_CUDA(cudaHostAlloc(&q, need, cudaHostAllocPortable));
-      hp->ring_bytes = need;
-      hp->ring_fields = nfields;
+  if (tma_gather) {
+    device_gather_tables(s, hp, p.levels, hp->s_in);  // the default path: tables built on the GPU
+  } else {
+    host_tables(s, hp);
+    if (compact) {
+      const int period = gather ? 0 : (flags >> 8) & 0xff;
+      if (!hp->compact_ready || hp->period != period) {
+        build_compact(s, hp, hp->idx_host, hp->mark_host, period);
+        hp->device_gather = false;
+      }
+      // the pinned staging ring (sized for the largest chunk)
+      size_t maxc = 0;
+      for (int c = 0; c < nchunks; ++c)
+        if (!hp->direct[c]) maxc = std::max<size_t>(maxc, (size_t)(hp->cb[c + 1] - hp->cb[c]));
+      const size_t need = std::max<size_t>(maxc * row, 16);
+      if (!gather && (hp->ring_bytes < need || hp->ring_fields < nfields)) {
+        for (void* q : hp->ring)
+          if (q) cudaFreeHost(q);
+        hp->ring.assign((size_t)nfields * HostPlan::kRing, nullptr);
+        for (auto& q : hp->ring) SG_CUDA(cudaHostAlloc(&q, need, cudaHostAllocPortable));
+        hp->ring_bytes = need;
+        hp->ring_fields = nfields;
+      }
     }
+  }
+  if (compact) {  // device compact sources
     while ((int)hp->csrc.size() < nfields) hp->csrc.emplace_back(new DevBuf());
-    if (tma_gather) build_pieces(s->device, hp, p.levels);
     for (int f = 0; f < nfields; ++f)
       if (hp->csrc[f]->bytes < std::max<size_t>(hp->ncompact * row, 16))
         hp->csrc[f]->alloc(s->device, std::max<size_t>(hp->ncompact * row, 16));
