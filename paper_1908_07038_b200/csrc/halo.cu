@@ -81,15 +81,45 @@ struct PeerPtrs {
 
 // Fused exchange: ghost row k (peer slot s) <- the owner's row recv_remote[k], read through a
 // peer pointer (same device, NVLink P2P or CUDA IPC): pack, transfer and unpack in one pass.
+// A warp moves kPullRows rows, issuing the loads of all of them before any store (the copy is
+// latency-bound with one row per warp: 4 x IT loads in flight per lane instead of IT).
+constexpr int kPullRows = 4;
+
 template <typename Wd, int IT>
 __global__ void __launch_bounds__(256) pull_rows(Wd* __restrict__ f, int64_t pitch_w, int W,
                                                  const int32_t* __restrict__ rows, const int32_t* __restrict__ remote,
                                                  const int32_t* __restrict__ slot, int64_t n, PeerPtrs peers) {
-  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (r >= n) return;
-  const int s = slot[r];
-  const Wd* src = static_cast<const Wd*>(peers.base[s]) + (int64_t)remote[r] * peers.pitch_w[s];
-  copy_row<Wd, IT>(f + (int64_t)rows[r] * pitch_w, src, W, threadIdx.x & 31);
+  const int64_t r0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kPullRows;
+  if (r0 >= n) return;
+  const int lane = threadIdx.x & 31;
+  if (IT == 0) {
+    for (int64_t r = r0; r < min(r0 + kPullRows, n); ++r) {
+      const int s = slot[r];
+      const Wd* src = static_cast<const Wd*>(peers.base[s]) + (int64_t)remote[r] * peers.pitch_w[s];
+      copy_row<Wd, 0>(f + (int64_t)rows[r] * pitch_w, src, W, lane);
+    }
+    return;
+  }
+  const Wd* src[kPullRows];
+  Wd* dst[kPullRows];
+#pragma unroll
+  for (int q = 0; q < kPullRows; ++q) {
+    const int64_t r = min(r0 + q, n - 1);  // a short tail repeats the last row (idempotent)
+    const int s = slot[r];
+    src[q] = static_cast<const Wd*>(peers.base[s]) + (int64_t)remote[r] * peers.pitch_w[s];
+    dst[q] = f + (int64_t)rows[r] * pitch_w;
+  }
+  Wd v[kPullRows][IT > 0 ? IT : 1];
+#pragma unroll
+  for (int q = 0; q < kPullRows; ++q)
+#pragma unroll
+    for (int i = 0; i < IT; ++i)
+      if (lane + 32 * i < W) v[q][i] = src[q][lane + 32 * i];
+#pragma unroll
+  for (int q = 0; q < kPullRows; ++q)
+#pragma unroll
+    for (int i = 0; i < IT; ++i)
+      if (lane + 32 * i < W) dst[q][lane + 32 * i] = v[q][i];
 }
 
 // Launches KERNEL<Wd, IT> with IT = ceil(W / 32) (0 = chunked loop beyond 8 slices).
@@ -335,7 +365,8 @@ int32_t sg_halo_pull(uint64_t plan, uint64_t field, const uint64_t* peer_ptrs, c
   DeviceScope ds(p->device);
   by_word(f, [&](auto* tag) {
     using Wd = std::remove_pointer_t<decltype(tag)>;
-    SG_ROW_KERNEL(pull_rows, Wd, f->levels, warps_grid(n), as_stream(stream), f->buf.as<Wd>(), f->pitch, f->levels,
+    SG_ROW_KERNEL(pull_rows, Wd, f->levels, warps_grid((n + kPullRows - 1) / kPullRows), as_stream(stream),
+                  f->buf.as<Wd>(), f->pitch, f->levels,
                   p->recv_rows.as<int32_t>(), p->recv_remote.as<int32_t>(), p->recv_peer.as<int32_t>(), n, pp);
   });
   SG_CUDA_LAUNCH();
