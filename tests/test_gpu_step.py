@@ -178,3 +178,57 @@ def test_signalled_exchange_times_out_without_owner(gpu):
     synchronize(0)
     with pytest.raises(sg.SpheregridError, match="timed out"):
         xs[0].check()
+
+
+def _random_step_cases(n, seed=9117):
+    rng = np.random.default_rng(seed)
+    grids = ["O16", "O24", "O32", "O48", "F8", "F16", "F24"]
+    out = []
+    for _ in range(n):
+        s, t = rng.choice(grids, 2, replace=False)
+        out.append((str(s), str(t), int(rng.integers(2, 9)), int(rng.integers(1, 4)),
+                    str(rng.choice(["blocks", "equal_regions"])), int(rng.choice([1, 7, 64, 137, 161]))))
+    return out
+
+
+@pytest.mark.parametrize("S,T,P,halo,part,L", _random_step_cases(14))
+def test_random_fused_steps_and_exchanges(gpu, S, T, P, halo, part, L):
+    """Seeded random sweep (grid pairs up and down, 2-8 ranks, halo 1-3, both decompositions,
+    1-161 levels): per rank the fused step equals the oracle apply on the exchanged field and
+    the signalled exchange leaves every ghost equal to its owner, three epochs in a row.
+    Thin halos can leave targets without a containing element: those runs use the reference's
+    nearest-node fallback rows (allow_fallback), which the step applies like any stencil."""
+    sg = gpu
+    from oracle import oracle as O
+    from paper_1908_07038_b200.device import DeviceArray, synchronize
+    from paper_1908_07038_b200.execute import (emulated_exchanges, emulated_fused_steps, launch_exchanges,
+                                               launch_fused_steps)
+    from paper_1908_07038_b200.partition import PARTITIONERS
+
+    Sg, Tg = sg.grid_from_name(S), sg.grid_from_name(T)
+    dist = PARTITIONERS[part](Sg, P)
+    td = sg.matching_partition(Tg, Sg, dist)
+    gvals = np.random.default_rng(P * 100 + halo).normal(size=(Sg.npts + 2, L))
+
+    def prog(ctx):
+        mesh = sg.generate_mesh(Sg, dist, ctx.rank, halo=halo, include_pole=True)
+        fs = sg.NodeColumns(mesh, ctx)
+        w = sg.build_remap(fs, Tg, td, ctx, allow_fallback=True)
+        init = np.where(mesh.node_ghost[:, None], 0.0, gvals[mesh.node_global])
+        a, b = DeviceArray(mesh.nb_nodes, L, np.float64), DeviceArray(mesh.nb_nodes, L, np.float64)
+        a.upload(init)
+        b.upload(init)
+        return mesh, fs.exchange_plan, w, a, b, DeviceArray(len(w), L, np.float64)
+
+    ranks = sg.run_ranks(P, prog, devices=[0])
+    xs = emulated_exchanges([(r[1], r[3]) for r in ranks])
+    steps = emulated_fused_steps([(r[2], r[1], r[4], r[5]) for r in ranks])
+    for _ in range(3):
+        launch_exchanges(xs)
+        launch_fused_steps(steps)
+    synchronize(0)
+    for mesh, plan, w, a, b, out in ranks:
+        assert np.array_equal(a.to_numpy(), gvals[mesh.node_global])
+        exp = O.apply_remap(w.nodes, w.weights, gvals[mesh.node_global])
+        assert np.array_equal(out.to_numpy().view(np.uint64), exp.view(np.uint64))
+    assert all(x.check() == 3 for x in xs) and all(st.check() == 3 for st in steps)
