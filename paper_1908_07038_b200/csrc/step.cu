@@ -1,5 +1,6 @@
 // One distributed remap step as ONE kernel per rank: halo exchange over peer memory + apply,
-// fenced by device-side signals instead of host or NCCL barriers.
+// fenced by device-side signals instead of host or NCCL barriers; and the halo exchange alone
+// as one signalled pull kernel per rank (cfg4).
 //
 // The reference step of a partition is halo_exchange (functionspace.py:107-118: owners'
 // values land in the ghost rows) followed by apply_remap (interp.py:206-228), in that order
@@ -8,24 +9,25 @@
 // and the two barriers around the peer reads become flag words in device memory:
 //
 //   signal kernel (one thread per rank, waits for nothing):
-//       e = epoch + 1;  for every rank that reads my rows: st.release.sys  its ready[me] = e
-//   step kernel (blocks [0, nIb) interior targets, [nIb, nIb + nBb) boundary targets):
-//       interior warps: apply from local rows only — no wait;
-//       boundary warps: ld.acquire.sys  ready[owner] >= e  for every owner, then apply with
-//         ghost rows read from the owners' fields;
-//       the last boundary block to finish (atomic count): st.release.sys  owner's done[me] = e
-//         for every owner, then (one GPU per rank) waits for done[reader] >= e from every
-//         reader of my rows — after that nobody reads my rows any more, so the caller may
-//         overwrite them; epoch = e.
+//       e = epoch + 1;  for every rank that reads my rows: st.release  its ready[me] = e
+//   step kernel (targets in natural order, one warp each):
+//       interior targets (every stencil row owned): apply from local rows — no wait;
+//       boundary targets: ld.acquire  ready[owner] >= e  for every owner, then apply with the
+//         ghost rows read from the owners' fields; each counts itself (acq_rel atomic) and the
+//         last one st.release-es done[me] = e to every owner and, with one GPU per rank, waits
+//         for done[reader] >= e from every reader of my rows — after that nobody reads my
+//         rows any more, so the caller may overwrite them; epoch = e.
+// Flag accesses use the peer's scope: .sys for a peer on another GPU, .gpu for a rank on the
+// same GPU (a .sys release under load costs tens of µs, profiles/r02_exchange_signalled.md).
 //
-// Both waits depend only on the OTHER ranks' signal kernel / boundary blocks, never on a
-// block of the same launch, so with one GPU per rank there is no cycle.  Several ranks on ONE
-// GPU must not run as separate launches that wait on each other (B200_PROFILING.md): for that
-// case sg_step_launch takes every rank's step in ONE launch (block ranges per rank); then the
-// ready flags were set by the preceding signal kernel, and the tail wait is left to the host
-// (wait_done = 0; sg_signal_read checks the words).  Waits are bounded (~10 s): on timeout the
-// error word is set and the kernel continues; sg_step_check reports it (no hang, no silent
-// result).
+// Both waits depend only on the OTHER ranks' signal kernel / boundary warps, never on a block
+// of the same launch, so with one GPU per rank there is no cycle.  Several ranks on ONE GPU
+// must not run as separate launches that wait on each other (B200_PROFILING.md): for that case
+// sg_step_launch takes every rank's step in ONE launch (block ranges per rank); the ready flags
+// were then set by the preceding signal kernel, and the tail wait is left to the host
+// (wait_done = 0; sg_signal_read checks the words).  Waits are bounded (10 s by default): on
+// timeout the error word is set and the kernel continues; sg_step_check reports it (no hang,
+// no silent result).
 //
 // Arithmetic identical to the apply kernels: bitwise equal to interp.py:219-223.
 #include <algorithm>
@@ -121,11 +123,25 @@ __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long 
   else
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// Programmatic dependent launch: the signal kernel lets the step / pull kernel start at once
+// (interior targets need nothing from it); code that reads the current epoch the signal kernel
+// wrote first waits for the signal grid (griddepcontrol.wait = full completion + visibility).
+__device__ __forceinline__ void pdl_release_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_wait_primary() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned long long now_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// acq_rel RMW at gpu scope: orders this block's peer reads (made visible to thread 0 by the
+// preceding __syncthreads) before the count the finisher acquires.
+__device__ __forceinline__ unsigned long long atom_add_acq_rel(unsigned long long* p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+
 // Spin until *p >= e; false (and the error word set) after timeout_ns.
 __device__ bool wait_geq(const unsigned long long* p, unsigned long long e, unsigned long long* err, int code,
                          unsigned long long timeout_ns, bool sys) {
@@ -251,6 +267,7 @@ __device__ void publish_ready(unsigned long long* f, int nr, int rank, const Pee
 }
 
 __global__ void signal_kernel(Group g) {
+  pdl_release_dependents();
   const int r = threadIdx.x;
   if (r < g.n) publish_ready(g.d[r].flags, g.d[r].nranks, g.d[r].rank, *g.d[r].peers);
 }
@@ -269,20 +286,25 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(Group g) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t t = b * kWarps + warp;
   if (t >= d.m) {
-    if (d.m == 0 && t == 0 && lane == 0)  // no targets: still tell the owners, wait for readers
+    if (d.m == 0 && t == 0 && lane == 0) {  // no targets: still tell the owners, wait for readers
+      pdl_wait_primary();
       finish_step(d, *(volatile unsigned long long*)(d.flags + w_cur(d.nranks)), g.wait_done);
+    }
     return;
   }
   const int4 id = __ldg(d.idx + t);
   const int hi = max(max(id.x, id.y), d.k == 4 ? max(id.z, id.w) : id.z);
   if (hi < d.ghost_lo) {  // interior: local rows only, no wait
     apply_target<ITERS, false>(d, t, id, lane);
-    if (d.n_boundary == 0 && t == 0 && lane == 0)
+    if (d.n_boundary == 0 && t == 0 && lane == 0) {
+      pdl_wait_primary();
       finish_step(d, *(volatile unsigned long long*)(d.flags + w_cur(d.nranks)), g.wait_done);
+    }
     return;
   }
   unsigned long long* f = d.flags;
   const int nr = d.nranks;
+  pdl_wait_primary();
   const unsigned long long e = *(volatile unsigned long long*)(f + w_cur(nr));
   {  // every owner of my ghosts has published its rows for epoch e (each lane acquires)
     const PeerTable& P = *d.peers;
@@ -291,11 +313,8 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(Group g) {
   }
   apply_target<ITERS, true>(d, t, id, lane);
   __syncwarp();
-  if (lane == 0) {
-    __threadfence();
-    const unsigned long long old = atomicAdd(f + w_count(nr), 1ull);
-    if ((int64_t)old == d.n_boundary - 1) finish_step(d, e, g.wait_done);  // all peer reads done
-  }
+  if (lane == 0 && (int64_t)atom_add_acq_rel(f + w_count(nr), 1ull) == d.n_boundary - 1)
+    finish_step(d, e, g.wait_done);  // all peer reads done
 }
 
 __global__ void count_boundary(const int4* idx, int64_t m, int k, int64_t ghost_lo, unsigned long long* out) {
@@ -338,16 +357,9 @@ struct XGroup {
 constexpr int kXWarps = 8;
 
 __global__ void xsignal_kernel(XGroup g) {
+  pdl_release_dependents();
   const int r = threadIdx.x;
   if (r < g.n) publish_ready(g.d[r].flags, g.d[r].nranks, g.d[r].rank, *g.d[r].peers);
-}
-
-// acq_rel RMW at gpu scope: orders this block's peer reads (made visible to thread 0 by the
-// preceding __syncthreads) before the count the finisher acquires.
-__device__ __forceinline__ unsigned long long atom_add_acq_rel(unsigned long long* p, unsigned long long v) {
-  unsigned long long old;
-  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
-  return old;
 }
 
 // A block moves kXRows ghost rows per warp (kXWarps warps): thread 0 first acquires the
@@ -369,6 +381,7 @@ __global__ void __launch_bounds__(kXWarps * 32) xchg_kernel(XGroup g) {
   const PeerTable& P = *d.peers;
   __shared__ unsigned long long e_sh;
   if (threadIdx.x == 0) {
+    pdl_wait_primary();
     const unsigned long long e = *(volatile unsigned long long*)(f + w_cur(nr));
     e_sh = e;
     if (d.n > 0)
@@ -411,6 +424,23 @@ __global__ void __launch_bounds__(kXWarps * 32) xchg_kernel(XGroup g) {
   __syncthreads();
   if (threadIdx.x == 0 && atom_add_acq_rel(f + w_count(nr), 1ull) == (unsigned long long)(nb - 1))
     finish_epoch(f, nr, d.rank, P, e_sh, g.wait_done, d.timeout_ns);  // all reads of peers' rows done
+}
+
+// Launch with programmatic stream serialization: may start while the preceding kernel of the
+// stream (the signal kernel) is still running; the kernel calls pdl_wait_primary() where needed.
+template <class G>
+void launch_pdl(void (*kernel)(G), unsigned grid, unsigned block, cudaStream_t s, const G& g) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SG_CUDA(cudaLaunchKernelEx(&cfg, kernel, g));
 }
 
 struct Exchange : Object {
@@ -612,12 +642,12 @@ int32_t sg_step_launch(const uint64_t* steps, int32_t n, int32_t wait_done, uint
   SG_CUDA_LAUNCH();
   const unsigned grid = (unsigned)g.start[n];
   switch ((levels + 31) / 32) {
-    case 1: step_kernel<1><<<grid, kWarps * 32, 0, s>>>(g); break;
-    case 2: step_kernel<2><<<grid, kWarps * 32, 0, s>>>(g); break;
-    case 3: step_kernel<3><<<grid, kWarps * 32, 0, s>>>(g); break;
-    case 4: step_kernel<4><<<grid, kWarps * 32, 0, s>>>(g); break;
-    case 5: step_kernel<5><<<grid, kWarps * 32, 0, s>>>(g); break;
-    default: step_kernel<0><<<grid, kWarps * 32, 0, s>>>(g); break;
+    case 1: launch_pdl(step_kernel<1>, grid, kWarps * 32, s, g); break;
+    case 2: launch_pdl(step_kernel<2>, grid, kWarps * 32, s, g); break;
+    case 3: launch_pdl(step_kernel<3>, grid, kWarps * 32, s, g); break;
+    case 4: launch_pdl(step_kernel<4>, grid, kWarps * 32, s, g); break;
+    case 5: launch_pdl(step_kernel<5>, grid, kWarps * 32, s, g); break;
+    default: launch_pdl(step_kernel<0>, grid, kWarps * 32, s, g); break;
   }
   SG_CUDA_LAUNCH();
   SG_API_END
@@ -723,12 +753,12 @@ int32_t sg_exchange_launch(const uint64_t* exchanges, int32_t n, int32_t wait_do
   const int it = (W + 31) / 32;
 #define SG_XLAUNCH(Wd)                                                            \
   switch (it) {                                                                   \
-    case 1: xchg_kernel<Wd, 1><<<grid, kXWarps * 32, 0, s>>>(g); break;           \
-    case 2: xchg_kernel<Wd, 2><<<grid, kXWarps * 32, 0, s>>>(g); break;           \
-    case 3: xchg_kernel<Wd, 3><<<grid, kXWarps * 32, 0, s>>>(g); break;           \
-    case 4: xchg_kernel<Wd, 4><<<grid, kXWarps * 32, 0, s>>>(g); break;           \
-    case 5: xchg_kernel<Wd, 5><<<grid, kXWarps * 32, 0, s>>>(g); break;           \
-    default: xchg_kernel<Wd, 0><<<grid, kXWarps * 32, 0, s>>>(g); break;          \
+    case 1: launch_pdl(xchg_kernel<Wd, 1>, grid, kXWarps * 32, s, g); break;           \
+    case 2: launch_pdl(xchg_kernel<Wd, 2>, grid, kXWarps * 32, s, g); break;           \
+    case 3: launch_pdl(xchg_kernel<Wd, 3>, grid, kXWarps * 32, s, g); break;           \
+    case 4: launch_pdl(xchg_kernel<Wd, 4>, grid, kXWarps * 32, s, g); break;           \
+    case 5: launch_pdl(xchg_kernel<Wd, 5>, grid, kXWarps * 32, s, g); break;           \
+    default: launch_pdl(xchg_kernel<Wd, 0>, grid, kXWarps * 32, s, g); break;          \
   }
   if (item == 8) {
     SG_XLAUNCH(unsigned long long)

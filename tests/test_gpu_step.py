@@ -232,3 +232,39 @@ def test_random_fused_steps_and_exchanges(gpu, S, T, P, halo, part, L):
         exp = O.apply_remap(w.nodes, w.weights, gvals[mesh.node_global])
         assert np.array_equal(out.to_numpy().view(np.uint64), exp.view(np.uint64))
     assert all(x.check() == 3 for x in xs) and all(st.check() == 3 for st in steps)
+
+
+def test_signalled_launches_replay_from_a_cuda_graph(gpu):
+    """The N>1 step is captured once into a CUDA graph and replayed (bench.py run_multi): the
+    signal kernels and the programmatically dependent step / pull kernels (PDL) captured on a
+    stream replay bitwise, with the epochs advancing once per replay."""
+    sg = gpu
+    from oracle import oracle as O
+    from paper_1908_07038_b200.device import DeviceArray, Graph, Stream
+    from paper_1908_07038_b200.execute import (emulated_exchanges, emulated_fused_steps, launch_exchanges,
+                                               launch_fused_steps)
+
+    Sg, Tg = sg.grid_from_name("O32"), sg.grid_from_name("O64")
+    L = 9
+    gvals = np.random.default_rng(3).normal(size=(Sg.npts + 2, L))
+    ranks = _ranks(sg, Sg, Tg, 3, L, "equal_regions", gvals)
+    xfields = [DeviceArray(r[2].shape[0], L, np.float64) for r in ranks]
+    for xf, r in zip(xfields, ranks):
+        xf.upload(np.where(r[5].node_ghost[:, None], 0.0, gvals[r[5].node_global]))
+    xs = emulated_exchanges([(r[1], xf) for r, xf in zip(ranks, xfields)])
+    steps = emulated_fused_steps([r[:4] for r in ranks])
+    st = Stream(0)
+
+    def body():
+        launch_exchanges(xs, st.stream)
+        launch_fused_steps(steps, st.stream)
+
+    g = Graph(0, st.stream, body)
+    for _ in range(4):
+        g.launch(st.stream)
+    st.synchronize()
+    for (w, plan, src, dst, n_owned, mesh), xf in zip(ranks, xfields):
+        assert np.array_equal(xf.to_numpy(), gvals[mesh.node_global])
+        exp = O.apply_remap(w.nodes, w.weights, gvals[mesh.node_global])
+        assert np.array_equal(dst.to_numpy().view(np.uint64), exp.view(np.uint64))
+    assert all(x.check() == 4 for x in xs) and all(s.check() == 4 for s in steps)
