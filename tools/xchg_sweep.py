@@ -17,7 +17,7 @@ from paper_1908_07038_b200.device import DeviceArray, Event  # noqa: E402
 from paper_1908_07038_b200.execute import emulated_exchanges, launch_exchanges  # noqa: E402
 from paper_1908_07038_b200.partition import PARTITIONERS  # noqa: E402
 
-P, H, L = int(os.environ.get("PARTS", 8)), int(os.environ.get("HALO", 2)), 137
+P, H, L = int(os.environ.get("PARTS", 8)), int(os.environ.get("HALO", 2)), int(os.environ.get("LEVELS", 137))
 S = sg.grid_from_name(os.environ.get("GRID", "O1280"))
 dist = PARTITIONERS[os.environ.get("PART", "equal_regions")](S, P)
 meshes = [sg.generate_mesh(S, dist, r, halo=H, include_pole=True) for r in range(P)]
@@ -48,7 +48,7 @@ for _ in range(10):
     t.append(Event.elapsed_ms(e0, e1))
 nb = sum(sum(len(v) for v in p.recv.values()) for p in plans) * L * 8
 ms = statistics.median(t)
-print(json.dumps({"P": P, "halo": H, "flush": os.environ.get("FLUSH", "copy"),
+print(json.dumps({"P": P, "halo": H, "levels": L, "flush": os.environ.get("FLUSH", "copy"),
 
                   "bytes": nb, "ms": ms, "GB_per_s": nb / (ms * 1e-3) / 1e9, "ghosts_bitwise": ok,
                   "epochs": [x.check() for x in xs]}))
