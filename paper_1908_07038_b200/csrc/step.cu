@@ -8,20 +8,24 @@
 // stencil rows straight from the owners' HBM through peer pointers, NVLink P2P or CUDA IPC),
 // and the two barriers around the peer reads become flag words in device memory:
 //
-//   signal kernel (one thread per rank, waits for nothing):
-//       e = epoch + 1;  for every rank that reads my rows: st.release  its ready[me] = e
-//   step kernel (targets in natural order, one warp each):
+//   signal kernel (one thread per rank):
+//       e = epoch + 1;  for every rank that reads my rows: st.release  its ready[me] = e;
+//       then (all ranks of the launch published) ld.acquire  ready[owner] >= e  for every owner
+//   step kernel (targets in natural order, one warp each; launched with PDL, so it starts
+//   while the signal kernel still waits):
 //       interior targets (every stencil row owned): apply from local rows — no wait;
-//       boundary targets: ld.acquire  ready[owner] >= e  for every owner, then apply with the
-//         ghost rows read from the owners' fields; each counts itself (acq_rel atomic) and the
-//         last one st.release-es done[me] = e to every owner and, with one GPU per rank, waits
-//         for done[reader] >= e from every reader of my rows — after that nobody reads my
-//         rows any more, so the caller may overwrite them; epoch = e.
+//       boundary targets: griddepcontrol.wait (the signal kernel saw every owner's ready
+//         word), then apply with the ghost rows read from the owners' fields; each counts
+//         itself (acq_rel atomic) and the last one st.release-es done[me] = e to every owner
+//         and, with one GPU per rank, waits for done[reader] >= e from every reader of my
+//         rows — after that nobody reads my rows any more, so the caller may overwrite them;
+//         epoch = e.
 // Flag accesses use the peer's scope: .sys for a peer on another GPU, .gpu for a rank on the
 // same GPU (a .sys release under load costs tens of µs, profiles/r02_exchange_signalled.md).
 //
-// Both waits depend only on the OTHER ranks' signal kernel / boundary warps, never on a block
-// of the same launch, so with one GPU per rank there is no cycle.  Several ranks on ONE GPU
+// Both waits depend only on the OTHER ranks' signal kernels (which publish before they wait)
+// and boundary warps, never on a block of the same launch, so with one GPU per rank there is no
+// cycle.  Several ranks on ONE GPU
 // must not run as separate launches that wait on each other (B200_PROFILING.md): for that case
 // sg_step_launch takes every rank's step in ONE launch (block ranges per rank); the ready flags
 // were then set by the preceding signal kernel, and the tail wait is left to the host
@@ -266,10 +270,22 @@ __device__ void publish_ready(unsigned long long* f, int nr, int rank, const Pee
     if (P.role[s] & kRoleSend) st_release(P.flags[s] + w_ready(rank), e, P.sys[s]);
 }
 
+// Every owner of this rank's ghosts has published epoch e (one thread; acquire at the owner's
+// scope).  Runs in the signal kernel after ALL ranks of the launch published theirs, so the
+// step / pull kernel that depends on it (griddepcontrol.wait) reads the owners' rows without
+// an acquire of its own.
+__device__ void wait_owners(unsigned long long* f, int nr, const PeerTable& P, unsigned long long timeout_ns) {
+  const unsigned long long e = f[w_cur(nr)];
+  for (int s = 0; s < P.npeers; ++s)
+    if (P.role[s] & kRoleRecv) wait_geq(f + w_ready(P.rank[s]), e, f + w_error(nr), 1, timeout_ns, P.sys[s]);
+}
+
 __global__ void signal_kernel(Group g) {
   pdl_release_dependents();
   const int r = threadIdx.x;
   if (r < g.n) publish_ready(g.d[r].flags, g.d[r].nranks, g.d[r].rank, *g.d[r].peers);
+  __syncthreads();  // every rank of this launch has published (single-GPU emulation)
+  if (r < g.n && g.d[r].n_boundary > 0) wait_owners(g.d[r].flags, g.d[r].nranks, *g.d[r].peers, g.d[r].timeout_ns);
 }
 
 constexpr int kWarps = 2;  // targets per block: small blocks retire and refill (apply.cu)
@@ -304,13 +320,8 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(Group g) {
   }
   unsigned long long* f = d.flags;
   const int nr = d.nranks;
-  pdl_wait_primary();
+  pdl_wait_primary();  // the signal kernel has seen every owner's ready word for this epoch
   const unsigned long long e = *(volatile unsigned long long*)(f + w_cur(nr));
-  {  // every owner of my ghosts has published its rows for epoch e (each lane acquires)
-    const PeerTable& P = *d.peers;
-    for (int s = 0; s < P.npeers; ++s)
-      if (P.role[s] & kRoleRecv) wait_geq(f + w_ready(P.rank[s]), e, f + w_error(nr), 1, d.timeout_ns, P.sys[s]);
-  }
   apply_target<ITERS, true>(d, t, id, lane);
   __syncwarp();
   if (lane == 0 && (int64_t)atom_add_acq_rel(f + w_count(nr), 1ull) == d.n_boundary - 1)
@@ -360,11 +371,13 @@ __global__ void xsignal_kernel(XGroup g) {
   pdl_release_dependents();
   const int r = threadIdx.x;
   if (r < g.n) publish_ready(g.d[r].flags, g.d[r].nranks, g.d[r].rank, *g.d[r].peers);
+  __syncthreads();  // every rank of this launch has published (single-GPU emulation)
+  if (r < g.n && g.d[r].n > 0) wait_owners(g.d[r].flags, g.d[r].nranks, *g.d[r].peers, g.d[r].timeout_ns);
 }
 
-// A block moves kXRows ghost rows per warp (kXWarps warps): thread 0 first acquires the
-// owners' ready words (one L1 invalidation per block), then every warp issues the loads of all
-// its rows before its stores (4 rows x IT words in flight per lane: the copy is latency-bound
+// A block moves kXRows ghost rows per warp (kXWarps warps): after griddepcontrol.wait (the
+// signal kernel saw every owner's ready word) every warp issues the loads of all its rows
+// before its stores (4 rows x IT words in flight per lane: the copy is latency-bound
 // otherwise); the last block to finish (acq_rel count) finishes the epoch.
 constexpr int kXRows = 4;
 constexpr int kXBlocksPerSM = 4;  // 256 threads x 64 registers: 4 resident blocks per SM
@@ -379,16 +392,8 @@ __global__ void __launch_bounds__(kXWarps * 32) xchg_kernel(XGroup g) {
   unsigned long long* f = d.flags;
   const int nr = d.nranks;
   const PeerTable& P = *d.peers;
-  __shared__ unsigned long long e_sh;
-  if (threadIdx.x == 0) {
-    pdl_wait_primary();
-    const unsigned long long e = *(volatile unsigned long long*)(f + w_cur(nr));
-    e_sh = e;
-    if (d.n > 0)
-      for (int s = 0; s < P.npeers; ++s)
-        if (P.role[s] & kRoleRecv) wait_geq(f + w_ready(P.rank[s]), e, f + w_error(nr), 1, d.timeout_ns, P.sys[s]);
-  }
-  __syncthreads();
+  pdl_wait_primary();  // the signal kernel has seen every owner's ready word for this epoch
+  const unsigned long long e_sh = *(volatile unsigned long long*)(f + w_cur(nr));
   // resident grid: each warp moves kXRows rows per iteration, blocks stride over the rank's rows
   for (int64_t i0 = (b * kXWarps + (threadIdx.x >> 5)) * kXRows; i0 < d.n; i0 += nb * kXWarps * kXRows) {
     if (IT > 0) {
