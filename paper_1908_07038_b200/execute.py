@@ -85,7 +85,8 @@ class FusedStep(N.Handle):
     (sg_step_create).  ``peer_info[r]`` = (ptr, pitch, device) of rank r's source field
     (ctx.peer_fields); ``peer_sigs[r]`` = (pointer to rank r's signal words, device uuid)
     (ctx.peer_signals).  Targets run in natural order; the ``n_boundary`` whose stencil reads
-    a ghost row wait for their owners' ready word and read that row from the owner's field."""
+    a ghost row read it from the owner's field once the step's signal kernel has seen every
+    owner's ready word."""
 
     def __init__(self, weights: InterpolationWeights, plan, src: DeviceArray, dst: DeviceArray, signal: Signal,
                  peer_info, peer_sigs):

@@ -1,6 +1,8 @@
 """The C-ABI from plain C on the GPU (tests/c_abi/remap_c.c): sg_remap_apply and the gather
-host-buffer execute bitwise equal to the reference expression evaluated in C, ShapeMismatch as
-a class-prefixed domain error, invalid/double-released handles, no leaked handles."""
+host-buffer execute bitwise equal to the reference expression evaluated in C; the N>1 entry
+points (halo plans, signal words, the signalled exchange and the fused exchange + apply step)
+on a 2-rank toy decomposition emulated on one GPU, bitwise against C; ShapeMismatch as a
+class-prefixed domain error, invalid/double-released handles, no leaked handles."""
 import subprocess
 
 import pytest
