@@ -643,6 +643,7 @@ def run_single(args):
         "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)
+    log(f"total {time.time() - t0:.1f}s")
 
 
 # ------------------------------------------------------------------------------------------
