@@ -268,3 +268,40 @@ def test_signalled_launches_replay_from_a_cuda_graph(gpu):
         exp = O.apply_remap(w.nodes, w.weights, gvals[mesh.node_global])
         assert np.array_equal(dst.to_numpy().view(np.uint64), exp.view(np.uint64))
     assert all(x.check() == 4 for x in xs) and all(s.check() == 4 for s in steps)
+
+
+def test_many_epochs_share_one_signal(gpu):
+    """200 rounds of exchange + step per rank sharing ONE signal per rank (epochs advance by two
+    per round): counters reset every epoch, no drift, results stay bitwise."""
+    sg = gpu
+    from oracle import oracle as O
+    from paper_1908_07038_b200.device import DeviceArray, synchronize
+    from paper_1908_07038_b200.execute import (FusedStep, Signal, SignalledExchange, launch_exchanges,
+                                               launch_fused_steps)
+
+    Sg, Tg = sg.grid_from_name("O24"), sg.grid_from_name("O48")
+    L, P = 5, 4
+    gvals = np.random.default_rng(1).normal(size=(Sg.npts + 2, L))
+    ranks = _ranks(sg, Sg, Tg, P, L, "equal_regions", gvals)
+    sigs = [Signal(0, P, r) for r in range(P)]
+    uuid = sg._native.device_uuid(0)
+    psig = [(s.ptr, uuid) for s in sigs]
+    xf = []
+    for r in ranks:
+        d = DeviceArray(r[2].shape[0], L, np.float64)
+        d.upload(np.where(r[5].node_ghost[:, None], 0.0, gvals[r[5].node_global]))
+        xf.append(d)
+    xinfo = [(d.ptr, d.pitch, 0) for d in xf]
+    sinfo = [(r[2].ptr, r[2].pitch, 0) for r in ranks]
+    xs = [SignalledExchange(r[1], xf[i], sigs[i], xinfo, psig) for i, r in enumerate(ranks)]
+    steps = [FusedStep(r[0], r[1], r[2], r[3], sigs[i], sinfo, psig) for i, r in enumerate(ranks)]
+    for _ in range(200):
+        launch_exchanges(xs)
+        launch_fused_steps(steps)
+    synchronize(0)
+    for i, (w, plan, src, dst, n_owned, mesh) in enumerate(ranks):
+        assert np.array_equal(xf[i].to_numpy(), gvals[mesh.node_global])
+        exp = O.apply_remap(w.nodes, w.weights, gvals[mesh.node_global])
+        assert np.array_equal(dst.to_numpy().view(np.uint64), exp.view(np.uint64))
+        words = sigs[i].read()
+        assert words["epoch"] == 400 and words["count"] == 0 and words["error"] == 0
