@@ -260,6 +260,7 @@ int32_t sg_signal_create(int32_t device, int32_t nranks, int32_t rank, uint64_t*
 int32_t sg_signal_ptr(uint64_t signal, uint64_t* out_dev_ptr);
 int32_t sg_signal_ipc_handle(uint64_t signal, uint8_t* out_handle, size_t n);
 int32_t sg_signal_read(uint64_t signal, uint64_t* out_words, int64_t n);
+int32_t sg_signal_write(uint64_t signal, const uint64_t* words, int64_t n);  /* tests / measurement */
 int32_t sg_step_create(uint64_t stencil, uint64_t plan, uint64_t src_field, uint64_t dst_field,
                        uint64_t signal, const uint64_t* peer_ptrs, const int64_t* peer_pitch_elems,
                        const uint64_t* peer_flag_ptrs, uint64_t* out_step);

@@ -109,6 +109,7 @@ _SIGS = {
     "sg_signal_ptr": [u64, vp],
     "sg_signal_ipc_handle": [u64, vp, sz],
     "sg_signal_read": [u64, vp, i64],
+    "sg_signal_write": [u64, vp, i64],
     "sg_step_create": [u64, u64, u64, u64, u64, vp, vp, vp, vp],
     "sg_step_info": [u64, vp, vp],
     "sg_step_launch": [vp, i32, i32, u64],

@@ -281,6 +281,10 @@ __device__ void wait_owners(unsigned long long* f, int nr, const PeerTable& P, u
 }
 
 __global__ void signal_kernel(Group g) {
+  // launched with PDL too: it may start during the previous kernel's last wave (which calls
+  // launch_dependents), but waits for that kernel's completion and memory before it reads the
+  // epoch or publishes anything — only its launch latency is hidden
+  pdl_wait_primary();
   pdl_release_dependents();
   const int r = threadIdx.x;
   if (r < g.n) publish_ready(g.d[r].flags, g.d[r].nranks, g.d[r].rank, *g.d[r].peers);
@@ -295,6 +299,7 @@ constexpr int kWarps = 2;  // targets per block: small blocks retire and refill 
 // the last such warp (or, with no boundary targets, warp 0 of block 0) finishes the step.
 template <int ITERS>
 __global__ void __launch_bounds__(kWarps * 32) step_kernel(Group g) {
+  pdl_release_dependents();  // the next signal kernel may launch during the last wave
   int r = 0;
   while (r + 1 < g.n && (int64_t)blockIdx.x >= g.start[r + 1]) ++r;
   const StepArgs& d = g.d[r];
@@ -368,6 +373,7 @@ struct XGroup {
 constexpr int kXWarps = 8;
 
 __global__ void xsignal_kernel(XGroup g) {
+  pdl_wait_primary();  // as signal_kernel
   pdl_release_dependents();
   const int r = threadIdx.x;
   if (r < g.n) publish_ready(g.d[r].flags, g.d[r].nranks, g.d[r].rank, *g.d[r].peers);
@@ -384,6 +390,7 @@ constexpr int kXBlocksPerSM = 4;  // 256 threads x 64 registers: 4 resident bloc
 
 template <typename Wd, int IT>
 __global__ void __launch_bounds__(kXWarps * 32) xchg_kernel(XGroup g) {
+  pdl_release_dependents();  // the next signal kernel may launch during the last wave
   int r = 0;
   while (r + 1 < g.n && (int64_t)blockIdx.x >= g.start[r + 1]) ++r;
   const XchgArgs& d = g.d[r];
@@ -547,6 +554,17 @@ int32_t sg_signal_read(uint64_t signal, uint64_t* out_words, int64_t n) {
   SG_API_END
 }
 
+// Overwrite signal words (host -> device, synchronous).  Measurement and tests only: e.g. to
+// time one rank's step alone with its owners' ready words already published.
+int32_t sg_signal_write(uint64_t signal, const uint64_t* words, int64_t n) {
+  SG_API_BEGIN
+  Signal* s = get<Signal>(signal, ObjKind::Signal);
+  SG_REQUIRE(words && n == (int64_t)s->nwords(), "need exactly %zu words", s->nwords());
+  DeviceScope ds(s->device);
+  SG_CUDA(cudaMemcpy(s->words.ptr, words, s->nwords() * 8, cudaMemcpyHostToDevice));
+  SG_API_END
+}
+
 int32_t sg_step_create(uint64_t stencil, uint64_t plan, uint64_t src_field, uint64_t dst_field, uint64_t signal,
                        const uint64_t* peer_ptrs, const int64_t* peer_pitch_elems, const uint64_t* peer_flag_ptrs,
                        uint64_t* out_step) {
@@ -643,8 +661,7 @@ int32_t sg_step_launch(const uint64_t* steps, int32_t n, int32_t wait_done, uint
   SG_REQUIRE(g.start[n] < INT32_MAX, "too many targets for one launch");
   DeviceScope ds(device);
   cudaStream_t s = as_stream(stream);
-  signal_kernel<<<1, 32, 0, s>>>(g);
-  SG_CUDA_LAUNCH();
+  launch_pdl(signal_kernel, 1, 32, s, g);
   const unsigned grid = (unsigned)g.start[n];
   switch ((levels + 31) / 32) {
     case 1: launch_pdl(step_kernel<1>, grid, kWarps * 32, s, g); break;
@@ -752,8 +769,7 @@ int32_t sg_exchange_launch(const uint64_t* exchanges, int32_t n, int32_t wait_do
                                                                                   (kXWarps * kXRows)));
   DeviceScope ds(device);
   cudaStream_t s = as_stream(stream);
-  xsignal_kernel<<<1, 32, 0, s>>>(g);
-  SG_CUDA_LAUNCH();
+  launch_pdl(xsignal_kernel, 1, 32, s, g);
   const unsigned grid = (unsigned)g.start[n];
   const int it = (W + 31) / 32;
 #define SG_XLAUNCH(Wd)                                                            \

@@ -72,6 +72,14 @@ class Signal(N.Handle):
                                   + ")")
         return w["epoch"]
 
+    def publish_owners_ahead(self, epoch: int) -> None:
+        """Measurement only: mark every rank's ready word as published up to ``epoch`` so this
+        rank's launches run alone (one rank's step timed without its peers)."""
+        w = np.zeros(2 * self.nranks + 4, np.uint64)
+        N.call("sg_signal_read", self.handle, N.ptr(w), len(w))
+        w[:self.nranks] = epoch
+        N.call("sg_signal_write", self.handle, N.ptr(w), len(w))
+
     def read(self) -> dict:
         w = np.zeros(2 * self.nranks + 4, np.uint64)
         N.call("sg_signal_read", self.handle, N.ptr(w), len(w))
