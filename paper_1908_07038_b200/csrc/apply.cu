@@ -112,16 +112,21 @@ __global__ void __launch_bounds__(256) apply_warp_v2(ApplyArgs a) {
 }
 
 // ---- warp per target, 8-B loads (any pitch; dense odd rows) ----------------------------------
-template <int ITERS, int HINT = 0>
+// SPLIT: one warp per (target, field) instead of per target — F fields sharing one stencil then
+// keep as many gathers in flight as one field does (a warp looping over F fields waits F
+// latencies); the stencil entry is re-read per field from L1/L2.
+template <int ITERS, int HINT = 0, bool SPLIT = false>
 __global__ void __launch_bounds__(256) apply_warp_v1(ApplyArgs a) {
   const int lane = threadIdx.x & 31;
-  const int64_t pos = a.t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t pos = a.t0 + (SPLIT ? wg / a.nfields : wg);
   if (pos >= a.t1) return;
+  const int f_lo = SPLIT ? (int)(wg % a.nfields) : 0, f_hi = SPLIT ? f_lo + 1 : a.nfields;
   const int64_t t = a.list ? (int64_t)__ldg(a.list + pos) : pos;
   const int4 id = __ldg(a.idx + t);
   const double4 wt = ldg_w4(a.w + t);
   const int L = a.levels;
-  for (int f = 0; f < a.nfields; ++f) {
+  for (int f = f_lo; f < f_hi; ++f) {
     const double* r0 = a.src[f] + (int64_t)id.x * a.src_pitch[f];
     const double* r1 = a.src[f] + (int64_t)id.y * a.src_pitch[f];
     const double* r2 = a.src[f] + (int64_t)id.z * a.src_pitch[f];
@@ -430,6 +435,9 @@ void launch_apply(ApplyArgs a, int variant, cudaStream_t st) {
     } else if ((variant == 4 || variant == 5) && (L + 31) / 32 == 5) {
       if (variant == 4) apply_warp_v1<5, 2><<<grid, tpb, 0, st>>>(a);  // L2::256B prefetch
       else apply_warp_v1<5, 1><<<grid, tpb, 0, st>>>(a);                // L2::128B prefetch
+    } else if (a.nfields > 1 && (L + 31) / 32 == 5) {  // F fields: a warp per (target, field)
+      const unsigned gridf = (unsigned)((m * a.nfields * 32 + tpb - 1) / tpb);
+      apply_warp_v1<5, 0, true><<<gridf, tpb, 0, st>>>(a);
     } else {
       switch ((L + 31) / 32) {
         case 1: apply_warp_v1<1><<<grid, tpb, 0, st>>>(a); break;
