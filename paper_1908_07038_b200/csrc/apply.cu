@@ -435,9 +435,15 @@ void launch_apply(ApplyArgs a, int variant, cudaStream_t st) {
     } else if ((variant == 4 || variant == 5) && (L + 31) / 32 == 5) {
       if (variant == 4) apply_warp_v1<5, 2><<<grid, tpb, 0, st>>>(a);  // L2::256B prefetch
       else apply_warp_v1<5, 1><<<grid, tpb, 0, st>>>(a);                // L2::128B prefetch
-    } else if (a.nfields > 1 && (L + 31) / 32 == 5) {  // F fields: a warp per (target, field)
+    } else if (a.nfields > 1 && (L + 31) / 32 <= 5) {  // F fields: a warp per (target, field)
       const unsigned gridf = (unsigned)((m * a.nfields * 32 + tpb - 1) / tpb);
-      apply_warp_v1<5, 0, true><<<gridf, tpb, 0, st>>>(a);
+      switch ((L + 31) / 32) {
+        case 1: apply_warp_v1<1, 0, true><<<gridf, tpb, 0, st>>>(a); break;
+        case 2: apply_warp_v1<2, 0, true><<<gridf, tpb, 0, st>>>(a); break;
+        case 3: apply_warp_v1<3, 0, true><<<gridf, tpb, 0, st>>>(a); break;
+        case 4: apply_warp_v1<4, 0, true><<<gridf, tpb, 0, st>>>(a); break;
+        default: apply_warp_v1<5, 0, true><<<gridf, tpb, 0, st>>>(a); break;
+      }
     } else {
       switch ((L + 31) / 32) {
         case 1: apply_warp_v1<1><<<grid, tpb, 0, st>>>(a); break;
