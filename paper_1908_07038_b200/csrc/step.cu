@@ -68,18 +68,18 @@ __host__ __device__ inline int w_cur(int nr) { return 2 * nr + 1; }
 __host__ __device__ inline int w_count(int nr) { return 2 * nr + 2; }
 __host__ __device__ inline int w_error(int nr) { return 2 * nr + 3; }
 
-// Peers of one rank (device resident: only boundary warps and the finisher read it).
+// Peers of one rank, BY VALUE in the kernel parameters (constant bank): the signal words,
+// field pointers and roles of at most kPeers neighbours — no dependent global load on the
+// signalling path or in front of a peer-row load.
+constexpr int kPeers = 16;
 struct PeerTable {
   int32_t npeers;
-  int32_t rank[kMaxPeers];
-  int32_t role[kMaxPeers];
-  union {
-    const double* base[kMaxPeers];
-    const void* base_any[kMaxPeers];
-  };
-  int64_t pitch[kMaxPeers];  // elements
-  unsigned long long* flags[kMaxPeers];
-  bool sys[kMaxPeers];  // the peer is another GPU: flag accesses at system scope
+  int32_t rank[kPeers];
+  unsigned char role[kPeers];
+  unsigned char sys[kPeers];  // the peer is another GPU: flag accesses at system scope
+  const void* base_any[kPeers];
+  int64_t pitch[kPeers];  // elements
+  unsigned long long* flags[kPeers];
 };
 
 // Everything a target warp needs, passed BY VALUE in the kernel parameters (constant bank):
@@ -100,7 +100,7 @@ struct StepArgs {
   unsigned long long* flags;  // this rank's words
   unsigned long long timeout_ns;
   int32_t nranks, rank;
-  const PeerTable* peers;
+  PeerTable peers;
 };
 
 struct Group {
@@ -189,7 +189,7 @@ __device__ __forceinline__ const double* row_of(const StepArgs& d, int n) {
   if (n < d.ghost_lo) return d.src + (int64_t)n * d.src_pitch;
   const int g = n - (int)d.ghost_lo;
   const int s = __ldg(d.ghost_slot + g);
-  return d.peers->base[s] + (int64_t)__ldg(d.ghost_row + g) * d.peers->pitch[s];
+  return static_cast<const double*>(d.peers.base_any[s]) + (int64_t)__ldg(d.ghost_row + g) * d.peers.pitch[s];
 }
 
 // One target per warp.  BOUNDARY: rows may live on peers (weak loads after the acquire).
@@ -258,7 +258,7 @@ __device__ void finish_epoch(unsigned long long* f, int nr, int rank, const Peer
   f[w_epoch(nr)] = e;
 }
 __device__ void finish_step(const StepArgs& d, unsigned long long e, int wait_done) {
-  finish_epoch(d.flags, d.nranks, d.rank, *d.peers, e, wait_done, d.timeout_ns);
+  finish_epoch(d.flags, d.nranks, d.rank, d.peers, e, wait_done, d.timeout_ns);
 }
 // ready[me] = epoch + 1 into every reader's words (one thread per rank)
 __device__ void publish_ready(unsigned long long* f, int nr, int rank, const PeerTable& P) {
@@ -287,9 +287,9 @@ __global__ void signal_kernel(Group g) {
   pdl_wait_primary();
   pdl_release_dependents();
   const int r = threadIdx.x;
-  if (r < g.n) publish_ready(g.d[r].flags, g.d[r].nranks, g.d[r].rank, *g.d[r].peers);
+  if (r < g.n) publish_ready(g.d[r].flags, g.d[r].nranks, g.d[r].rank, g.d[r].peers);
   __syncthreads();  // every rank of this launch has published (single-GPU emulation)
-  if (r < g.n && g.d[r].n_boundary > 0) wait_owners(g.d[r].flags, g.d[r].nranks, *g.d[r].peers, g.d[r].timeout_ns);
+  if (r < g.n && g.d[r].n_boundary > 0) wait_owners(g.d[r].flags, g.d[r].nranks, g.d[r].peers, g.d[r].timeout_ns);
 }
 
 constexpr int kWarps = 2;  // targets per block: small blocks retire and refill (apply.cu)
@@ -360,7 +360,7 @@ struct XchgArgs {
   unsigned long long* flags;
   unsigned long long timeout_ns;
   int32_t nranks, rank;
-  const PeerTable* peers;
+  PeerTable peers;
 };
 
 struct XGroup {
@@ -376,9 +376,9 @@ __global__ void xsignal_kernel(XGroup g) {
   pdl_wait_primary();  // as signal_kernel
   pdl_release_dependents();
   const int r = threadIdx.x;
-  if (r < g.n) publish_ready(g.d[r].flags, g.d[r].nranks, g.d[r].rank, *g.d[r].peers);
+  if (r < g.n) publish_ready(g.d[r].flags, g.d[r].nranks, g.d[r].rank, g.d[r].peers);
   __syncthreads();  // every rank of this launch has published (single-GPU emulation)
-  if (r < g.n && g.d[r].n > 0) wait_owners(g.d[r].flags, g.d[r].nranks, *g.d[r].peers, g.d[r].timeout_ns);
+  if (r < g.n && g.d[r].n > 0) wait_owners(g.d[r].flags, g.d[r].nranks, g.d[r].peers, g.d[r].timeout_ns);
 }
 
 // A block moves kXRows ghost rows per warp (kXWarps warps): after griddepcontrol.wait (the
@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(kXWarps * 32) xchg_kernel(XGroup g) {
   const int lane = threadIdx.x & 31;
   unsigned long long* f = d.flags;
   const int nr = d.nranks;
-  const PeerTable& P = *d.peers;
+  const PeerTable& P = d.peers;
   pdl_wait_primary();  // the signal kernel has seen every owner's ready word for this epoch
   const unsigned long long e_sh = *(volatile unsigned long long*)(f + w_cur(nr));
   // resident grid: each warp moves kXRows rows per iteration, blocks stride over the rank's rows
@@ -460,7 +460,6 @@ struct Exchange : Object {
   int device = 0;
   int itemsize = 8;
   XchgArgs args{};
-  DevBuf peers;  // PeerTable
   uint64_t signal = 0;
 };
 
@@ -468,7 +467,6 @@ struct Step : Object {
   Step() : Object(ObjKind::Step) {}
   int device = 0;
   StepArgs args{};
-  DevBuf peers;  // PeerTable
   int64_t nblocks = 0;
   uint64_t signal = 0;
 };
@@ -478,6 +476,7 @@ struct Step : Object {
 PeerTable peer_table(const Plan* p, const Signal* sig, const uint64_t* peer_ptrs, const int64_t* peer_pitch_elems,
                      const uint64_t* peer_flag_ptrs) {
   const size_t np = p->peers.size();
+  SG_REQUIRE(np <= (size_t)kPeers, "%zu peers: signalled launches take at most %d", np, kPeers);
   SG_REQUIRE(np == 0 || (peer_ptrs && peer_pitch_elems && peer_flag_ptrs), "null peer arrays");
   SG_REQUIRE(p->recv_off.back() == 0 || p->has_remote,
              "plan has ghosts without an owner row (recv_remote); signalled peer reads need them");
@@ -595,8 +594,6 @@ int32_t sg_step_create(uint64_t stencil, uint64_t plan, uint64_t src_field, uint
   st->signal = signal;
   const PeerTable pt = peer_table(p, sig, peer_ptrs, peer_pitch_elems, peer_flag_ptrs);
   DeviceScope ds(s->device);
-  st->peers.alloc(s->device, sizeof(PeerTable));
-  SG_CUDA(cudaMemcpy(st->peers.ptr, &pt, sizeof(PeerTable), cudaMemcpyHostToDevice));
   StepArgs& d = st->args;
   d.idx = s->idx.as<int4>();
   d.w = s->w.as<double2>();
@@ -614,7 +611,7 @@ int32_t sg_step_create(uint64_t stencil, uint64_t plan, uint64_t src_field, uint
   d.timeout_ns = kTimeoutNs;
   d.nranks = sig->nranks;
   d.rank = sig->rank;
-  d.peers = st->peers.as<PeerTable>();
+  d.peers = pt;
   // boundary targets (a stencil row >= ghost_lo): the count the last reader checks against
   DevBuf cnt;
   cnt.alloc(s->device, 8);
@@ -723,8 +720,6 @@ int32_t sg_exchange_create(uint64_t plan, uint64_t field, uint64_t signal, const
   x->itemsize = f->itemsize;
   const PeerTable pt = peer_table(p, sig, peer_ptrs, peer_pitch_elems, peer_flag_ptrs);
   DeviceScope ds(p->device);
-  x->peers.alloc(p->device, sizeof(PeerTable));
-  SG_CUDA(cudaMemcpy(x->peers.ptr, &pt, sizeof(PeerTable), cudaMemcpyHostToDevice));
   XchgArgs& d = x->args;
   d.base = f->buf.ptr;
   d.pitch = f->pitch;
@@ -737,7 +732,7 @@ int32_t sg_exchange_create(uint64_t plan, uint64_t field, uint64_t signal, const
   d.timeout_ns = kTimeoutNs;
   d.nranks = sig->nranks;
   d.rank = sig->rank;
-  d.peers = x->peers.as<PeerTable>();
+  d.peers = pt;
   *out_exchange = registry_put(x.release());
   SG_API_END
 }
