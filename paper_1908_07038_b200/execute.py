@@ -49,6 +49,9 @@ def _device_list(rows: np.ndarray, device: int) -> Optional[DeviceArray]:
     return d
 
 
+MAX_SIGNAL_PEERS = 16  # kPeers of csrc/step.cu: the peer table travels in the kernel parameters
+
+
 class Signal(N.Handle):
     """A rank's step signal words in HBM (csrc/step.cu): ready[r], done[r], epoch, ..."""
 
@@ -174,7 +177,8 @@ class DistributedRemap:
         if self.fused and hasattr(ctx, "peer_signals"):
             self.signal = Signal(dev, ctx.nranks, ctx.rank)
             sigs = ctx.peer_signals(self.signal)
-            self.signalled = len({u for _, u in sigs}) == ctx.nranks
+            few = all(ctx.share(len(self.plan.peers) <= MAX_SIGNAL_PEERS))
+            self.signalled = few and len({u for _, u in sigs}) == ctx.nranks
             if self.signalled:
                 self.fused_step = FusedStep(weights, self.plan, src, dst, self.signal, self.peer_info, sigs)
                 self.stream_ordered = True

@@ -221,10 +221,12 @@ def _signalled_exchange(ctx, plan, dev_array):
     cache = ctx.__dict__.setdefault("_xcache", [])
     key = (id(plan), dev_array.ptr, dev_array.handle)
     hit = next((x for k, x in cache if k == key), None)
-    everyone = ctx.share((hit is not None, N.device_uuid(dev_array.device)))
-    if len({u for _, u in everyone}) != ctx.nranks:
-        return None  # ranks share a GPU: spinning launches must not wait on each other there
-    if all(h for h, _ in everyone):
+    from .execute import MAX_SIGNAL_PEERS
+
+    everyone = ctx.share((hit is not None, N.device_uuid(dev_array.device), len(plan.peers) <= MAX_SIGNAL_PEERS))
+    if len({u for _, u, _ in everyone}) != ctx.nranks or not all(f for _, _, f in everyone):
+        return None  # ranks share a GPU (spinning launches must not wait on each other there), or too many peers
+    if all(h for h, _, _ in everyone):
         return hit
     x = SignalledExchange.for_rank(ctx, plan, dev_array)
     cache.append((key, x))

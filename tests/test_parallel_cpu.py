@@ -3,6 +3,7 @@ parallel.py:1-195 contract) and DistContext over torch.distributed/gloo with wor
 > 1, each building the reference's halo plans (checked against golden fixtures)."""
 import os
 import socket
+import types
 
 import numpy as np
 import pytest
@@ -210,7 +211,7 @@ def _gloo_signal_worker(rank, world, port, q, same_gpu):
 
         E.SignalledExchange = FakeExchange
         ctx = sg.DistContext(device=0)
-        plan = object()
+        plan = types.SimpleNamespace(peers=[1 - rank])
         a, b = _FakeArray(1000 + rank, 1), _FakeArray(2000 + rank, 2)
         seq = [a, a, b if rank == 1 else a, a, a]
         got = [PAR._signalled_exchange(ctx, plan, x) for x in seq]
