@@ -37,6 +37,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "plan.cuh"
@@ -45,8 +47,18 @@
 namespace sg {
 
 // Signal words (uint64) of one rank, zeroed at creation.
+// Signal words allocated by THIS process, by address -> device.  A peer's words found here are
+// a same-process rank (the single-GPU emulation, or in-process ranks on other GPUs); anything
+// else (CUDA-IPC mappings of another process's words) is treated as another GPU: system scope.
+std::mutex g_local_signals_mu;
+std::unordered_map<uintptr_t, int> g_local_signals;
+
 struct Signal : Object {
   Signal() : Object(ObjKind::Signal) {}
+  ~Signal() override {
+    std::lock_guard<std::mutex> lk(g_local_signals_mu);
+    g_local_signals.erase(reinterpret_cast<uintptr_t>(words.ptr));
+  }
   int device = 0;
   int32_t nranks = 0, rank = 0;
   DevBuf words;
@@ -493,11 +505,15 @@ PeerTable peer_table(const Plan* p, const Signal* sig, const uint64_t* peer_ptrs
     pt.base_any[i] = reinterpret_cast<const void*>(peer_ptrs[i]);
     pt.pitch[i] = peer_pitch_elems[i];
     pt.flags[i] = reinterpret_cast<unsigned long long*>(peer_flag_ptrs[i]);
-    // the peer's signal words live on this GPU (same-device ranks) or another one
-    cudaPointerAttributes at{};
-    const bool known = cudaPointerGetAttributes(&at, pt.flags[i]) == cudaSuccess && at.type == cudaMemoryTypeDevice;
-    if (!known) cudaGetLastError();
-    pt.sys[i] = !(known && at.device == sig->device);
+    // .gpu scope only for a peer whose signal words this process allocated on this very device
+    // (ranks of a single-GPU emulation); IPC mappings and other GPUs: .sys
+    int peer_dev = -1;
+    {
+      std::lock_guard<std::mutex> lk(g_local_signals_mu);
+      auto it = g_local_signals.find((uintptr_t)peer_flag_ptrs[i]);
+      if (it != g_local_signals.end()) peer_dev = it->second;
+    }
+    pt.sys[i] = peer_dev != sig->device;
   }
   return pt;
 }
@@ -521,6 +537,10 @@ int32_t sg_signal_create(int32_t device, int32_t nranks, int32_t rank, uint64_t*
   s->words.alloc(device, s->nwords() * 8);
   SG_CUDA(cudaMemset(s->words.ptr, 0, s->nwords() * 8));
   SG_CUDA(cudaDeviceSynchronize());
+  {
+    std::lock_guard<std::mutex> lk(g_local_signals_mu);
+    g_local_signals[reinterpret_cast<uintptr_t>(s->words.ptr)] = device;
+  }
   *out_signal = registry_put(s.release());
   SG_API_END
 }
