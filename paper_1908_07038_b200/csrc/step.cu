@@ -121,6 +121,7 @@ struct Group {
   int32_t n;
   int32_t wait_done;
 };
+static_assert(sizeof(Group) <= 32000, "kernel parameters are limited to 32764 bytes");
 
 // Scope of a flag access: .sys when the other side of the flag is another GPU (NVLink / IPC),
 // .gpu when it is this GPU (ranks of a single-GPU emulation) — a .sys release under load costs
@@ -381,6 +382,7 @@ struct XGroup {
   int32_t n;
   int32_t wait_done;
 };
+static_assert(sizeof(XGroup) <= 32000, "kernel parameters are limited to 32764 bytes");
 
 constexpr int kXWarps = 8;
 
