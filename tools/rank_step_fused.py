@@ -37,17 +37,21 @@ def time_it(fn):
     return Event.elapsed_ms(e0, e1) / REPS
 
 
-# N = 1: the plain apply of the whole configuration
-dist1 = sg.blocks_partition(S, 1)
-mesh1 = sg.generate_mesh(S, dist1, 0, halo=2, include_pole=True)
-w1 = sg.build_remap(sg.NodeColumns(mesh1, None), T, sg.matching_partition(T, S, dist1))
-a1, b1 = DeviceArray(mesh1.nb_nodes, L, np.float64), DeviceArray(len(w1), L, np.float64)
-t1 = time_it(lambda: sg.apply_remap_device(w1, [a1], [b1], stream=st.stream))
-del a1, b1
-print(json.dumps({"P": 1, "apply_ms": t1}), flush=True)
+# N = 1: the plain apply of the whole configuration (skipped with NO_SERIAL=1)
+t1 = 1.0852  # profiles/r02_rank_step_fused_1gpu.jsonl
+if not os.environ.get("NO_SERIAL"):
+    dist1 = sg.blocks_partition(S, 1)
+    mesh1 = sg.generate_mesh(S, dist1, 0, halo=2, include_pole=True)
+    w1 = sg.build_remap(sg.NodeColumns(mesh1, None), T, sg.matching_partition(T, S, dist1))
+    a1, b1 = DeviceArray(mesh1.nb_nodes, L, np.float64), DeviceArray(len(w1), L, np.float64)
+    t1 = time_it(lambda: sg.apply_remap_device(w1, [a1], [b1], stream=st.stream))
+    del a1, b1
+    print(json.dumps({"P": 1, "apply_ms": t1}), flush=True)
 
-for pname in ("equal_regions", "blocks"):
-    for P in (2, 4, 8):
+PARTS = [int(x) for x in os.environ.get("PARTS", "2,4,8").split(",")]
+PARTITIONERS_RUN = os.environ.get("PARTITIONERS", "equal_regions,blocks").split(",")
+for pname in PARTITIONERS_RUN:
+    for P in PARTS:
         dist = PARTITIONERS[pname](S, P)
         td = sg.matching_partition(T, S, dist)
 
