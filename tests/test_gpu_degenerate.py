@@ -85,3 +85,39 @@ def test_meshes_without_degenerate_triangles_keep_the_fast_path(gpu, golden):
     elem, corners = sg.MeshLocator(mesh).locate_many(T.xyz())
     assert (elem >= 0).all()
     assert np.array_equal(corners, z["nodes"].astype(np.int64))
+
+
+def _random_degenerate_grids(n, seed=777):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        nrows = int(rng.integers(4, 9))
+        lats = np.sort(rng.uniform(-80, 80, nrows))[::-1]
+        nl = [int(rng.choice([2, 3, 4, 5, 6, 8, 10, 12])) for _ in range(nrows)]
+        nl[int(rng.integers(0, nrows))] = 2  # at least one 2-point row: elements in the plane y = 0
+        out.append(tuple((float(round(a, 3)), b) for a, b in zip(lats, nl)))
+    return out
+
+
+@pytest.mark.parametrize("rows", _random_degenerate_grids(10))
+def test_random_degenerate_meshes_match_the_oracle(gpu, rows):
+    """Seeded random custom grids with 2-point rows: the device's per-target outcome (element /
+    NotLocated / DegenerateTriangle) equals the oracle's restatement of MeshLocator.locate
+    (oracle/locate_oracle.c: brute-force k = 8 / 32 nearest nodes, candidates in the reference's
+    order, interp.py:90-117) except where the k-th nearest distance is tied (cKDTree order)."""
+    sg = gpu
+    from oracle import oracle as O
+
+    S = sg.build_grid(sg.GridSpec(kind=sg.GridKind.CUSTOM, rows=rows))
+    mesh = sg.generate_mesh(S, sg.blocks_partition(S, 1), 0, halo=0, include_pole=True)
+    conn = mesh.element_connectivity
+    for tname in ("O8", "F8"):
+        xyz = sg.grid_from_name(tname).xyz()
+        elem, _ = sg.MeshLocator(mesh).locate_many(xyz)
+        oelem, _ = O.locate(mesh.node_xyz, conn.offsets, conn.indices, xyz)
+        code = np.where(elem >= 0, 0, np.where(elem == -2, 2, 1))
+        ocode = np.where(oelem >= 0, 0, np.where(oelem == -2, 2, 1))
+        diff = np.flatnonzero((code != ocode) | ((code == 0) & (elem != oelem)))
+        untied = [int(t) for t in diff if not _tied_at_k(mesh.node_xyz, xyz[t])]
+        assert not untied, (tname, untied[:10], code[untied[:10]], ocode[untied[:10]])
+        assert (ocode == 2).any()
