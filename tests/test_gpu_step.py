@@ -305,3 +305,38 @@ def test_many_epochs_share_one_signal(gpu):
         assert np.array_equal(dst.to_numpy().view(np.uint64), exp.view(np.uint64))
         words = sigs[i].read()
         assert words["epoch"] == 400 and words["count"] == 0 and words["error"] == 0
+
+
+@pytest.mark.parametrize("P,part", [(4, "blocks"), (6, "equal_regions")])
+def test_emulated_fused_step_structured_bilinear(gpu, P, part):
+    """The fused step with 4-point structured-bilinear stencils (cfg5's method, csrc/bilinear.cu):
+    bitwise equal to the oracle's 4-point apply ((w0 a + w1 b) + w2 c) + w3 d on the exchanged
+    field, P ranks emulated as one launch."""
+    sg = gpu
+    from oracle import oracle as O
+    from paper_1908_07038_b200.device import DeviceArray, synchronize
+    from paper_1908_07038_b200.execute import emulated_fused_steps, launch_fused_steps
+    from paper_1908_07038_b200.partition import PARTITIONERS
+
+    S, T = sg.grid_from_name("O48"), sg.grid_from_name("O32")
+    L = 21
+    dist = PARTITIONERS[part](S, P)
+    td = sg.matching_partition(T, S, dist)
+    gvals = np.random.default_rng(12).normal(size=(S.npts + 2, L))
+
+    def prog(ctx):
+        mesh = sg.generate_mesh(S, dist, ctx.rank, halo=2, include_pole=True)
+        fs = sg.NodeColumns(mesh, ctx)
+        w = sg.build_bilinear(fs, T, td, ctx)
+        src = DeviceArray(mesh.nb_nodes, L, np.float64)
+        src.upload(np.where(mesh.node_ghost[:, None], 0.0, gvals[mesh.node_global]))
+        return w, fs.exchange_plan, src, DeviceArray(len(w), L, np.float64), mesh
+
+    ranks = sg.run_ranks(P, prog, devices=[0])
+    steps = emulated_fused_steps([r[:4] for r in ranks])
+    launch_fused_steps(steps)
+    synchronize(0)
+    assert all(w.nodes.shape[1] == 4 for w, *_ in ranks)
+    for w, plan, src, dst, mesh in ranks:
+        exp = O.apply_remap_k(w.nodes, w.weights, gvals[mesh.node_global])
+        assert np.array_equal(dst.to_numpy().view(np.uint64), exp.view(np.uint64))
