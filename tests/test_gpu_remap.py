@@ -644,3 +644,38 @@ def test_random_grid_pairs_partitions_vs_scaled_oracle(gpu, src, tgt, P, halo, p
         if located.any():
             ow = O.barycentric_weights_batched(mesh.node_xyz, c[located], txyz[w.target_global][located])
             assert np.abs(w.weights[located] - ow).max() <= W_TOL
+
+
+def test_execute_host_gather_plan_edge_cases(gpu):
+    """The device-built gather plan (device_gather_tables) with more chunks than source rows
+    per chunk can hold (empty chunks), one chunk, and a rank that owns no targets."""
+    sg = gpu
+    from paper_1908_07038_b200.device import DeviceArray, PinnedArray
+    from paper_1908_07038_b200.interp import execute_host
+
+    S, T = sg.grid_from_name("O8"), sg.grid_from_name("O16")
+    dist = sg.blocks_partition(S, 1)
+    mesh = sg.generate_mesh(S, dist, 0, halo=2, include_pole=True)
+    w = sg.build_remap(sg.NodeColumns(mesh, None), T, sg.matching_partition(T, S, dist))
+    L = 7
+    hs = PinnedArray((mesh.nb_nodes, L))
+    hs.array[:] = np.random.default_rng(9).normal(size=hs.array.shape)
+    exp = O.apply_remap(w.nodes, w.weights, hs.array)
+    ds, dd = DeviceArray(mesh.nb_nodes, L, np.float64), DeviceArray(len(w), L, np.float64)
+    for nchunks in (1, 2, 700, 1024):  # O8 has ~350 source nodes: most of 700 / 1024 chunks are empty
+        hd = PinnedArray((len(w), L))
+        rows = execute_host(w, [hs.array], [hd.array], [ds], [dd], nchunks=nchunks, mode="gather")
+        assert rows == w.distinct_sources()
+        assert np.array_equal(hd.array.view(np.uint64), exp.view(np.uint64)), nchunks
+    # a partition that owns no targets: an empty stencil, an empty host target
+    S2, T2 = sg.grid_from_name("O48"), sg.grid_from_name("O4")
+    d2 = sg.blocks_partition(S2, 8)
+    td2 = sg.matching_partition(T2, S2, d2)
+    empty = int(np.flatnonzero(np.bincount(td2.part_of, minlength=8) == 0)[0])
+    m2 = sg.generate_mesh(S2, d2, empty, halo=2, include_pole=True)
+    w2 = sg.build_remap(sg.NodeColumns(m2, None), T2, td2)
+    assert len(w2) == 0
+    h2 = PinnedArray((m2.nb_nodes, L))
+    out = np.empty((0, L))
+    execute_host(w2, [h2.array], [out], [DeviceArray(m2.nb_nodes, L, np.float64)],
+                 [DeviceArray(0, L, np.float64)], mode="gather")
