@@ -37,10 +37,12 @@ ok = all(np.array_equal(f.to_numpy(), m.node_global[:, None].astype(np.float64) 
          for f, m in zip(fields, meshes))
 t = []
 for _ in range(10):
-    if os.environ.get("FLUSH", "copy") == "read":  # read 2 GiB: evicts L2 with clean lines
+    mode = os.environ.get("FLUSH", "copy")
+    if mode == "read":  # read 2 GiB: evicts L2 with clean lines
         sg._native.call("sg_field_checksum", flush.handle, 0, 1 << 22, gid0.ctypes.data, C.byref(part))
-    else:  # copy 512 MB: leaves L2 full of dirty lines, written back during the timed launch
+    elif mode == "copy":  # copy 512 MB: leaves L2 full of dirty lines, written back during the timed launch
         sg._native.call("sg_rows_copy", 0, flush.ptr, 512, 0, flush.ptr + 256, 512, 0, 1 << 21, 256, 0)
+    # "none": back-to-back exchanges, warm L2 (the steady state of repeated exchanges)
     e0, e1 = Event(0), Event(0)
     e0.record()
     launch_exchanges(xs)
