@@ -392,14 +392,14 @@ def emulated_halo(sg, S, L, flush, parts=8, halo=2, partitioner="equal_regions",
     for d in fields:
         d.close()
     worst = max(ms)
-    return {"bytes_per_exchange": int(sum(nbytes)), "ms": worst, "GB_per_s": sum(nbytes) / (worst * 1e-3) / 1e9,
+    return {"bytes_per_exchange": int(sum(nbytes)), "worst_rank_pull_ms": worst,
             "signalled_one_launch_ms": one, "signalled_one_launch_GB_per_s": sum(nbytes) / (one * 1e-3) / 1e9,
             "signalled_epochs": epochs,
             "worst_rank_bytes": int(nbytes[int(np.argmax(ms))]), "per_rank_ms": [round(x, 4) for x in ms],
             "scope": f"cfg4 point O1280, {L} lev, halo {halo}, {partitioner} P={parts}, EMULATED on one GPU: "
                      "all ranks' fields in this GPU's HBM, each rank's pull kernel timed alone with L2 "
-                     "flushed (ms = max over ranks), and all ranks' signalled pulls as one launch "
-                     "(signalled_one_launch_ms). HBM, not NVLink (needs >1 GPU)"}
+                     "flushed (worst_rank_pull_ms = max over ranks; not concurrent), and all ranks' signalled "
+                     "pulls as ONE launch (signalled_one_launch_*, concurrent). HBM, not NVLink (needs >1 GPU)"}
 
 
 def emulated_fused_step(sg, source, target, L, parts=8, partitioner="equal_regions", reps=10):
