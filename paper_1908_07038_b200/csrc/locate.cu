@@ -273,33 +273,58 @@ struct TargetOut {
   int32_t* best_tri; // [m]
 };
 
-__device__ __forceinline__ bool lu_solve3(const double M_in[3][3], const double rhs[3], double x[3]) {
-  double M[3][3];
-  double b[3] = {rhs[0], rhs[1], rhs[2]};
+// np.linalg.solve(M, p) for a 3x3 system exactly as the reference's LAPACK does it: numpy's
+// bundled OpenBLAS dgesv = getrf_single -> getf2 (left-looking LU: per column, apply the earlier
+// pivots, subtract dot(L, u) from the U part, subtract the dgemv_n tail sum from the rest, pick
+// the first max |.| pivot, swap rows, scale by the pivot's reciprocal) then getrs -> dlaswp +
+// trsv NLU / NUN (axpy updates with FMA, divisions by the diagonal).  The kernels' roundings:
+// dot / gemv tail sums are FMA chains from 0 subtracted as one term; axpy is FMA.  Bitwise equal
+// to np.linalg.solve on every cfg2 target (108,160) and every fixture; false = singular (a zero
+// pivot: LinAlgError in the reference, interp.py:66-67).
+__device__ __forceinline__ bool lu_solve3(const double M[3][3], const double rhs[3], double x[3]) {
+  double A[3][3];  // column-major: A[col][row]
   for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) M[i][j] = M_in[i][j];
-  int piv[3] = {0, 1, 2};
+    for (int j = 0; j < 3; ++j) A[j][i] = M[i][j];
+  int ipiv[3];
+  bool singular = false;
+#pragma unroll
   for (int j = 0; j < 3; ++j) {
-    int p = j;
-    double amax = fabs(M[j][j]);
-    for (int i = j + 1; i < 3; ++i)
-      if (fabs(M[i][j]) > amax) { amax = fabs(M[i][j]); p = i; }
-    if (M[p][j] == 0.0) return false;
-    if (p != j) {
-      for (int k = 0; k < 3; ++k) { double t = M[j][k]; M[j][k] = M[p][k]; M[p][k] = t; }
-      int t = piv[j]; piv[j] = piv[p]; piv[p] = t;
+    double* b = A[j];
+    for (int i = 0; i < j; ++i)  // earlier pivots applied to this column
+      if (ipiv[i] != i) { const double t = b[i]; b[i] = b[ipiv[i]]; b[ipiv[i]] = t; }
+    for (int i = 1; i < j; ++i) {  // U part: b[i] -= dot(L[i, 0:i], b[0:i])
+      double d = 0.0;
+      for (int k = 0; k < i; ++k) d = __fma_rn(A[k][i], b[k], d);
+      b[i] = __dsub_rn(b[i], d);
     }
-    double r = 1.0 / M[j][j];
-    for (int i = j + 1; i < 3; ++i) M[i][j] *= r;
+    for (int i = j; i < 3; ++i) {  // dgemv_n tail rows: b[i] += -1 * sum_k A[i,k] b[k]
+      double t = 0.0;
+      for (int k = 0; k < j; ++k) t = __fma_rn(A[k][i], b[k], t);
+      b[i] = __fma_rn(-1.0, t, b[i]);
+    }
+    int jp = j;  // idamax: first maximum
     for (int i = j + 1; i < 3; ++i)
-      for (int k = j + 1; k < 3; ++k) M[i][k] = __fma_rn(-M[i][j], M[j][k], M[i][k]);
+      if (fabs(b[i]) > fabs(b[jp])) jp = i;
+    ipiv[j] = jp;
+    const double piv = b[jp];
+    if (piv == 0.0) {
+      singular = true;
+      continue;
+    }
+    if (jp != j)
+      for (int k = 0; k <= j; ++k) { const double t = A[k][j]; A[k][j] = A[k][jp]; A[k][jp] = t; }
+    const double r = 1.0 / piv;
+    for (int i = j + 1; i < 3; ++i) b[i] = __dmul_rn(b[i], r);
   }
-  double y[3] = {b[piv[0]], b[piv[1]], b[piv[2]]};
-  for (int j = 0; j < 3; ++j)
-    for (int i = j + 1; i < 3; ++i) y[i] = __fma_rn(-y[j], M[i][j], y[i]);
-  for (int j = 2; j >= 0; --j) {
-    y[j] /= M[j][j];
-    for (int i = 0; i < j; ++i) y[i] = __fma_rn(-y[j], M[i][j], y[i]);
+  if (singular) return false;
+  double y[3] = {rhs[0], rhs[1], rhs[2]};
+  for (int i = 0; i < 3; ++i)  // dlaswp
+    if (ipiv[i] != i) { const double t = y[i]; y[i] = y[ipiv[i]]; y[ipiv[i]] = t; }
+  for (int i = 0; i < 3; ++i)  // trsv, unit lower: axpy with -y[i]
+    for (int k = i + 1; k < 3; ++k) y[k] = __fma_rn(-y[i], A[i][k], y[k]);
+  for (int i = 2; i >= 0; --i) {  // trsv, upper: divide, then axpy
+    y[i] = __ddiv_rn(y[i], A[i][i]);
+    for (int k = 0; k < i; ++k) y[k] = __fma_rn(-y[i], A[i][k], y[k]);
   }
   x[0] = y[0]; x[1] = y[1]; x[2] = y[2];
   return true;
