@@ -607,6 +607,21 @@ def run_single(args):
         parity = {"checked": True, "against": kind,
                   "device_bitwise_vs_cpu": bool(np.array_equal(device_out.view(np.uint64), out.view(np.uint64))),
                   "e2e_bitwise_vs_cpu": bool(np.array_equal(hdst[F - 1].array.view(np.uint64), out.view(np.uint64)))}
+        if method == "fe":  # the stencils of the timed kernel vs the reference's search and solver
+            from oracle import oracle as O
+
+            t0s = time.perf_counter()
+            conn = mesh.element_connectivity
+            txyz = T.xyz()[w.target_global]
+            e_o, c_o = O.locate_kdtree(mesh.node_xyz, conn.offsets, conn.indices, txyz)
+            ow = O.barycentric_weights_batched(mesh.node_xyz, c_o, txyz)
+            parity.update({
+                "stencils_bitwise_vs_reference_search": bool((e_o >= 0).all() and np.array_equal(w.nodes, c_o)),
+                "weights_bitwise_vs_reference_dgesv": bool(np.array_equal(w.weights.view(np.uint64),
+                                                                          ow.view(np.uint64))),
+                "stencil_check": "every target: oracle.locate_kdtree (the reference's cKDTree k=8/32 candidates "
+                                 "and scoring) + np.linalg.solve, as interp.py:102-117 / 61-71",
+                "stencil_check_s": round(time.perf_counter() - t0s, 1)})
 
     h2d_moved = int(w.__dict__.get("last_host_rows_moved", n)) * L * 8 * F
     peak, peak_src = measured_peak()

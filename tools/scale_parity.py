@@ -31,4 +31,5 @@ print(json.dumps({"source": "O2560", "target": "O1280", "source_nodes": mesh.nb_
                   "locator": loc.stats(), "mesh_s": t_mesh, "locator_s": t_loc, "build_remap_s": t_build,
                   "oracle_locate_s": t_oracle, "oracle_unlocated": int((e < 0).sum()),
                   "stencil_mismatches": int((w.nodes != c).any(axis=1).sum()),
-                  "max_weight_diff": float(np.abs(w.weights - ow).max())}), flush=True)
+                  "max_weight_diff": float(np.abs(w.weights - ow).max()),
+                  "weights_bitwise": bool(np.array_equal(w.weights.view(np.uint64), ow.view(np.uint64)))}), flush=True)
