@@ -352,9 +352,12 @@ __device__ void finish_target(const LocView& v, V3 q, int64_t t, int best, uint8
           st = 4;  // interp.py:69-70
         } else {
           w[0] = x[0] / s; w[1] = x[1] / s; w[2] = x[2] / s;
-          const V3 vproj = V3{__fma_rn(w[2], c.x, __fma_rn(w[1], b.x, __dmul_rn(w[0], a.x))),
-                              __fma_rn(w[2], c.y, __fma_rn(w[1], b.y, __dmul_rn(w[0], a.y))),
-                              __fma_rn(w[2], c.z, __fma_rn(w[1], b.z, __dmul_rn(w[0], a.z)))};
+          // w @ column_stack([a, b, c]).T: numpy's matmul -> OpenBLAS dgemv_t tail row
+          // `a0*x0 + a1*x1 + a2*x2`, which its compiler contracted to fma(a2,x2,fma(a0,x0,a1*x1))
+          // (bitwise on all 108,160 cfg2 targets); then ddot with p
+          const V3 vproj = V3{__fma_rn(w[2], c.x, __fma_rn(w[0], a.x, __dmul_rn(w[1], b.x))),
+                              __fma_rn(w[2], c.y, __fma_rn(w[0], a.y, __dmul_rn(w[1], b.y))),
+                              __fma_rn(w[2], c.z, __fma_rn(w[0], a.z, __dmul_rn(w[1], b.z)))};
           sc = dot_blas(vproj, q);
         }
       }

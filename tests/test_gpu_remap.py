@@ -57,7 +57,7 @@ def test_serial_stencils_bitexact(gpu, golden, name, src, tgt):
     assert np.array_equal(w.nodes, z["nodes"].astype(np.int64))
     # weights bit-identical to the reference's np.linalg.solve (locate.cu lu_solve3 = OpenBLAS dgesv)
     assert np.array_equal(w.weights.view(np.uint64), z["weights"].view(np.uint64))
-    assert np.abs(w.scale - z["scale"]).max() <= W_TOL
+    assert np.array_equal(w.scale.view(np.uint64), z["scale"].view(np.uint64))
     assert not w.fallback.any()
     L = z["out"].shape[1]
     f = fs.create_field("s", levels=L)
