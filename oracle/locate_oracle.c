@@ -213,3 +213,58 @@ int oracle_locate_knn(const double* xyz, int64_t n, const int64_t* off, const in
   free(fill);
   return 0;
 }
+
+/* np.linalg.solve(M, p) for 3x3 systems restated operation for operation as numpy's bundled
+ * OpenBLAS dgesv evaluates it (getrf_single -> getf2 left-looking LU, getrs -> dlaswp + trsv):
+ * the kernels' roundings — dot / dgemv_n tail sums as FMA chains from 0 subtracted as one
+ * term, pivot scaling by the reciprocal, FMA axpy in trsv, division by the diagonal.  The
+ * checker for the device's lu_solve3 (csrc/locate.cu); pinned bitwise against np.linalg.solve
+ * and the golden weights by tests/test_oracle.py.  M row-major (m, 3, 3); returns 0, or the
+ * 1-based index of the first singular system. */
+int64_t oracle_dgesv3(const double* Mall, const double* pall, double* xall, int64_t m) {
+  int64_t bad = 0;
+  for (int64_t t = 0; t < m; ++t) {
+    const double* Mi = Mall + 9 * t;
+    double A[3][3]; /* column-major: A[col][row] */
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) A[j][i] = Mi[3 * i + j];
+    int ipiv[3], singular = 0;
+    for (int j = 0; j < 3; ++j) {
+      double* b = A[j];
+      for (int i = 0; i < j; ++i)
+        if (ipiv[i] != i) { double s = b[i]; b[i] = b[ipiv[i]]; b[ipiv[i]] = s; }
+      for (int i = 1; i < j; ++i) {
+        double d = 0.0;
+        for (int k = 0; k < i; ++k) d = fma(A[k][i], b[k], d);
+        b[i] = b[i] - d;
+      }
+      for (int i = j; i < 3; ++i) {
+        double s = 0.0;
+        for (int k = 0; k < j; ++k) s = fma(A[k][i], b[k], s);
+        b[i] = fma(-1.0, s, b[i]);
+      }
+      int jp = j;
+      for (int i = j + 1; i < 3; ++i)
+        if (fabs(b[i]) > fabs(b[jp])) jp = i;
+      ipiv[j] = jp;
+      const double piv = b[jp];
+      if (piv == 0.0) { singular = 1; continue; }
+      if (jp != j)
+        for (int k = 0; k <= j; ++k) { double s = A[k][j]; A[k][j] = A[k][jp]; A[k][jp] = s; }
+      const double r = 1.0 / piv;
+      for (int i = j + 1; i < 3; ++i) b[i] = b[i] * r;
+    }
+    double* y = xall + 3 * t;
+    y[0] = pall[3 * t]; y[1] = pall[3 * t + 1]; y[2] = pall[3 * t + 2];
+    if (singular) { if (!bad) bad = t + 1; continue; }
+    for (int i = 0; i < 3; ++i)
+      if (ipiv[i] != i) { double s = y[i]; y[i] = y[ipiv[i]]; y[ipiv[i]] = s; }
+    for (int i = 0; i < 3; ++i)
+      for (int k = i + 1; k < 3; ++k) y[k] = fma(-y[i], A[i][k], y[k]);
+    for (int i = 2; i >= 0; --i) {
+      y[i] = y[i] / A[i][i];
+      for (int k = 0; k < i; ++k) y[k] = fma(-y[i], A[i][k], y[k]);
+    }
+  }
+  return bad;
+}

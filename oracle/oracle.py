@@ -36,6 +36,8 @@ def _c():
         _lib.oracle_locate_knn.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                            C.c_int64, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         _lib.oracle_locate_knn.restype = C.c_int
+        _lib.oracle_dgesv3.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
+        _lib.oracle_dgesv3.restype = C.c_int64
     return _lib
 
 
@@ -235,6 +237,17 @@ def locate_kdtree(node_xyz, conn_off, conn_idx, points, workers: int = -1):
         elem[todo], corners[todo] = e, c
         todo = todo[e == -1]
     return elem, corners
+
+
+def dgesv3_restated(M: np.ndarray, p: np.ndarray) -> np.ndarray:
+    """np.linalg.solve for (m, 3, 3) systems restated as numpy's OpenBLAS dgesv evaluates it
+    (locate_oracle.c oracle_dgesv3; the checker of csrc/locate.cu lu_solve3, interp.py:65)."""
+    M = np.ascontiguousarray(M, np.float64)
+    p = np.ascontiguousarray(p, np.float64)
+    x = np.empty((len(M), 3))
+    if _c().oracle_dgesv3(M.ctypes.data, p.ctypes.data, x.ctypes.data, len(M)):
+        raise np.linalg.LinAlgError("singular matrix")
+    return x
 
 
 def barycentric_weights_batched(xyz, corners, points):

@@ -167,3 +167,22 @@ def test_oracle_degenerate_candidates_equal_reference(golden, gname):
         ref = z[f"{gname}__{tname}__code"]
         diff = np.flatnonzero((code != ref) | ((code == 0) & (elem != z[f"{gname}__{tname}__elem"])))
         assert len(diff) <= 2, (tname, diff)
+
+
+@pytest.mark.parametrize("name,src,tgt", [("cfg1_O32_O16", "O32", "O16"), ("serial_F8_F4", "F8", "F4"),
+                                          ("cfg2_O320_O160", "O320", "O160")])
+def test_dgesv_restatement_equals_numpy_and_reference(golden, name, src, tgt):
+    """The restated 3x3 dgesv (what csrc/locate.cu computes) equals np.linalg.solve on this
+    host and, renormalised, the reference's golden weights, bit for bit (interp.py:61-71)."""
+    z = golden(name)
+    S, mesh = serial_mesh(z, src)
+    T = sg.grid_with_latitudes(tgt, z["tgt_lat"])
+    xyz = mesh.node_xyz
+    nodes = z["nodes"].astype(np.int64)
+    M = np.stack([xyz[nodes[:, 0]], xyz[nodes[:, 1]], xyz[nodes[:, 2]]], axis=2)
+    p = T.xyz()[z["target_global"]]
+    x = O.dgesv3_restated(M, p)
+    ref = np.linalg.solve(M, p[..., None])[..., 0]
+    assert np.array_equal(x.view(np.uint64), ref.view(np.uint64))
+    s = (x[:, 0] + x[:, 1]) + x[:, 2]
+    assert np.array_equal((x / s[:, None]).view(np.uint64), z["weights"].view(np.uint64))
