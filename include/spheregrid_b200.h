@@ -266,6 +266,11 @@ int32_t sg_step_create(uint64_t stencil, uint64_t plan, uint64_t src_field, uint
                        const uint64_t* peer_flag_ptrs, uint64_t* out_step);
 int32_t sg_step_info(uint64_t step, int64_t* out_m, int64_t* out_n_boundary);
 int32_t sg_step_launch(const uint64_t* steps, int32_t n, int32_t wait_done, uint64_t stream);
+/* Test/emulation entry: the same launch over every rank of a single-GPU emulation WITH the tail
+ * waits (wait_done = 1) as one cooperative launch — all blocks co-resident, so a rank's finisher
+ * may spin on the done words of readers in the same grid.  Status 1 if the grid does not fit
+ * the GPU at once (small problems only). */
+int32_t sg_step_launch_cooperative(const uint64_t* steps, int32_t n, uint64_t stream);
 int32_t sg_step_check(uint64_t step, uint64_t* out_error, uint64_t* out_epoch);
 int32_t sg_step_set_timeout(uint64_t step, uint64_t timeout_ns);
 /* The halo exchange alone, signalled (functionspace.py:107-118; cfg4): one signal kernel + one
@@ -277,6 +282,7 @@ int32_t sg_exchange_create(uint64_t plan, uint64_t field, uint64_t signal, const
                            const int64_t* peer_pitch_elems, const uint64_t* peer_flag_ptrs,
                            uint64_t* out_exchange);
 int32_t sg_exchange_launch(const uint64_t* exchanges, int32_t n, int32_t wait_done, uint64_t stream);
+int32_t sg_exchange_launch_cooperative(const uint64_t* exchanges, int32_t n, uint64_t stream);
 int32_t sg_exchange_set_timeout(uint64_t exchange, uint64_t timeout_ns);
 int32_t sg_exchange_signal(uint64_t exchange, uint64_t* out_signal);
 

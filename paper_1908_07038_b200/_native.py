@@ -113,10 +113,12 @@ _SIGS = {
     "sg_step_create": [u64, u64, u64, u64, u64, vp, vp, vp, vp],
     "sg_step_info": [u64, vp, vp],
     "sg_step_launch": [vp, i32, i32, u64],
+    "sg_step_launch_cooperative": [vp, i32, u64],
     "sg_step_check": [u64, vp, vp],
     "sg_step_set_timeout": [u64, u64],
     "sg_exchange_create": [u64, u64, u64, vp, vp, vp, vp],
     "sg_exchange_launch": [vp, i32, i32, u64],
+    "sg_exchange_launch_cooperative": [vp, i32, u64],
     "sg_exchange_set_timeout": [u64, u64],
     "sg_exchange_signal": [u64, vp],
     "sg_meshgen_create": [i32, vp, i32, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp],

@@ -454,16 +454,30 @@ __global__ void __launch_bounds__(kXWarps * 32) xchg_kernel(XGroup g) {
 
 // Launch with programmatic stream serialization: may start while the preceding kernel of the
 // stream (the signal kernel) is still running; the kernel calls pdl_wait_primary() where needed.
+// cooperative = true instead: every block co-resident (checked), no PDL — the single-GPU
+// emulation in which the ranks' tail waits (wait_done) may spin on each other's blocks.
 template <class G>
-void launch_pdl(void (*kernel)(G), unsigned grid, unsigned block, cudaStream_t s, const G& g) {
+void launch_pdl(void (*kernel)(G), unsigned grid, unsigned block, cudaStream_t s, const G& g,
+                bool cooperative = false) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  if (cooperative) {
+    int dev = 0, nsm = 0, per_sm = 0;
+    SG_CUDA(cudaGetDevice(&dev));
+    SG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, (int)block, 0));
+    SG_REQUIRE((int64_t)grid <= (int64_t)per_sm * nsm,
+               "cooperative launch of %u blocks exceeds the %d x %d co-resident blocks", grid, per_sm, nsm);
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+  } else {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+  }
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   SG_CUDA(cudaLaunchKernelEx(&cfg, kernel, g));
@@ -660,10 +674,10 @@ int32_t sg_step_info(uint64_t step, int64_t* out_m, int64_t* out_n_boundary) {
   SG_API_END
 }
 
-int32_t sg_step_launch(const uint64_t* steps, int32_t n, int32_t wait_done, uint64_t stream) {
-  SG_API_BEGIN
+static void step_launch(const uint64_t* steps, int32_t n, int32_t wait_done, uint64_t stream, bool coop) {
   SG_REQUIRE(steps && n >= 1 && n <= kMaxGroup, "1..%d steps per launch", kMaxGroup);
-  SG_REQUIRE(!(n > 1 && wait_done), "a multi-rank launch on one GPU cannot wait for its own ranks (wait_done=0)");
+  SG_REQUIRE(coop || !(n > 1 && wait_done),
+             "a multi-rank launch on one GPU cannot wait for its own ranks (wait_done=0)");
   Group g{};
   g.n = n;
   g.wait_done = wait_done ? 1 : 0;
@@ -683,14 +697,28 @@ int32_t sg_step_launch(const uint64_t* steps, int32_t n, int32_t wait_done, uint
   launch_pdl(signal_kernel, 1, 32, s, g);
   const unsigned grid = (unsigned)g.start[n];
   switch ((levels + 31) / 32) {
-    case 1: launch_pdl(step_kernel<1>, grid, kWarps * 32, s, g); break;
-    case 2: launch_pdl(step_kernel<2>, grid, kWarps * 32, s, g); break;
-    case 3: launch_pdl(step_kernel<3>, grid, kWarps * 32, s, g); break;
-    case 4: launch_pdl(step_kernel<4>, grid, kWarps * 32, s, g); break;
-    case 5: launch_pdl(step_kernel<5>, grid, kWarps * 32, s, g); break;
-    default: launch_pdl(step_kernel<0>, grid, kWarps * 32, s, g); break;
+    case 1: launch_pdl(step_kernel<1>, grid, kWarps * 32, s, g, coop); break;
+    case 2: launch_pdl(step_kernel<2>, grid, kWarps * 32, s, g, coop); break;
+    case 3: launch_pdl(step_kernel<3>, grid, kWarps * 32, s, g, coop); break;
+    case 4: launch_pdl(step_kernel<4>, grid, kWarps * 32, s, g, coop); break;
+    case 5: launch_pdl(step_kernel<5>, grid, kWarps * 32, s, g, coop); break;
+    default: launch_pdl(step_kernel<0>, grid, kWarps * 32, s, g, coop); break;
   }
   SG_CUDA_LAUNCH();
+}
+
+int32_t sg_step_launch(const uint64_t* steps, int32_t n, int32_t wait_done, uint64_t stream) {
+  SG_API_BEGIN
+  step_launch(steps, n, wait_done, stream, false);
+  SG_API_END
+}
+
+// Every rank of a single-GPU emulation in ONE cooperative launch WITH the tail waits
+// (wait_done = 1): all blocks co-resident, so the ranks' last blocks may spin on each other.
+// Small problems only (the grid must fit the GPU at once).
+int32_t sg_step_launch_cooperative(const uint64_t* steps, int32_t n, uint64_t stream) {
+  SG_API_BEGIN
+  step_launch(steps, n, 1, stream, true);
   SG_API_END
 }
 
@@ -759,10 +787,10 @@ int32_t sg_exchange_create(uint64_t plan, uint64_t field, uint64_t signal, const
   SG_API_END
 }
 
-int32_t sg_exchange_launch(const uint64_t* exchanges, int32_t n, int32_t wait_done, uint64_t stream) {
-  SG_API_BEGIN
+static void exchange_launch(const uint64_t* exchanges, int32_t n, int32_t wait_done, uint64_t stream, bool coop) {
   SG_REQUIRE(exchanges && n >= 1 && n <= kMaxGroup, "1..%d exchanges per launch", kMaxGroup);
-  SG_REQUIRE(!(n > 1 && wait_done), "a multi-rank launch on one GPU cannot wait for its own ranks (wait_done=0)");
+  SG_REQUIRE(coop || !(n > 1 && wait_done),
+             "a multi-rank launch on one GPU cannot wait for its own ranks (wait_done=0)");
   XGroup g{};
   g.n = n;
   g.wait_done = wait_done ? 1 : 0;
@@ -791,12 +819,12 @@ int32_t sg_exchange_launch(const uint64_t* exchanges, int32_t n, int32_t wait_do
   const int it = (W + 31) / 32;
 #define SG_XLAUNCH(Wd)                                                            \
   switch (it) {                                                                   \
-    case 1: launch_pdl(xchg_kernel<Wd, 1>, grid, kXWarps * 32, s, g); break;           \
-    case 2: launch_pdl(xchg_kernel<Wd, 2>, grid, kXWarps * 32, s, g); break;           \
-    case 3: launch_pdl(xchg_kernel<Wd, 3>, grid, kXWarps * 32, s, g); break;           \
-    case 4: launch_pdl(xchg_kernel<Wd, 4>, grid, kXWarps * 32, s, g); break;           \
-    case 5: launch_pdl(xchg_kernel<Wd, 5>, grid, kXWarps * 32, s, g); break;           \
-    default: launch_pdl(xchg_kernel<Wd, 0>, grid, kXWarps * 32, s, g); break;          \
+    case 1: launch_pdl(xchg_kernel<Wd, 1>, grid, kXWarps * 32, s, g, coop); break;         \
+    case 2: launch_pdl(xchg_kernel<Wd, 2>, grid, kXWarps * 32, s, g, coop); break;         \
+    case 3: launch_pdl(xchg_kernel<Wd, 3>, grid, kXWarps * 32, s, g, coop); break;         \
+    case 4: launch_pdl(xchg_kernel<Wd, 4>, grid, kXWarps * 32, s, g, coop); break;         \
+    case 5: launch_pdl(xchg_kernel<Wd, 5>, grid, kXWarps * 32, s, g, coop); break;         \
+    default: launch_pdl(xchg_kernel<Wd, 0>, grid, kXWarps * 32, s, g, coop); break;        \
   }
   if (item == 8) {
     SG_XLAUNCH(unsigned long long)
@@ -805,6 +833,17 @@ int32_t sg_exchange_launch(const uint64_t* exchanges, int32_t n, int32_t wait_do
   }
 #undef SG_XLAUNCH
   SG_CUDA_LAUNCH();
+}
+
+int32_t sg_exchange_launch(const uint64_t* exchanges, int32_t n, int32_t wait_done, uint64_t stream) {
+  SG_API_BEGIN
+  exchange_launch(exchanges, n, wait_done, stream, false);
+  SG_API_END
+}
+
+int32_t sg_exchange_launch_cooperative(const uint64_t* exchanges, int32_t n, uint64_t stream) {
+  SG_API_BEGIN
+  exchange_launch(exchanges, n, 1, stream, true);
   SG_API_END
 }
 

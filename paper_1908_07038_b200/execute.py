@@ -137,6 +137,14 @@ def launch_fused_steps(steps: Sequence[FusedStep], stream: int = 0, wait_done: b
     N.call("sg_step_launch", N.ptr(arr), len(arr), int(bool(wait_done)), stream)
 
 
+def launch_fused_steps_cooperative(steps: Sequence[FusedStep], stream: int = 0) -> None:
+    """Every rank of a single-GPU emulation as ONE cooperative launch with the tail waits
+    (wait_done): all blocks are co-resident, so each rank's finisher can wait for its readers'
+    done words as it does with one GPU per rank.  Small problems only (the grid must fit)."""
+    arr = np.array([s.handle for s in steps], np.uint64)
+    N.call("sg_step_launch_cooperative", N.ptr(arr), len(arr), stream)
+
+
 class DistributedRemap:
     def __init__(self, fs, weights: InterpolationWeights, ctx, src: DeviceArray, dst: DeviceArray,
                  variant: int = APPLY_DEFAULT, overlap: bool = True, fused: bool = False):
@@ -315,6 +323,13 @@ class SignalledExchange(N.Handle):
 def launch_exchanges(xs: Sequence[SignalledExchange], stream: int = 0, wait_done: bool = False) -> None:
     arr = np.array([x.handle for x in xs], np.uint64)
     N.call("sg_exchange_launch", N.ptr(arr), len(arr), int(bool(wait_done)), stream)
+
+
+def launch_exchanges_cooperative(xs: Sequence[SignalledExchange], stream: int = 0) -> None:
+    """Cooperative single-GPU emulation of the exchange with the tail waits (see
+    ``launch_fused_steps_cooperative``)."""
+    arr = np.array([x.handle for x in xs], np.uint64)
+    N.call("sg_exchange_launch_cooperative", N.ptr(arr), len(arr), stream)
 
 
 def emulated_exchanges(ranks: Sequence[tuple]) -> List[SignalledExchange]:

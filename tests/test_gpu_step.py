@@ -5,7 +5,8 @@ ranks write into each other's HBM instead of host or NCCL barriers.
 One GPU cannot host ranks whose separate launches wait on each other (B200_PROFILING.md), so
 P ranks are emulated as ONE launch over every rank's data (``launch_fused_steps``): the
 protocol (epochs, ready/done words, the last-block count) and the peer reads run exactly as
-with one GPU per rank, minus the tail wait.  Reference behaviour: halo_exchange
+with one GPU per rank, minus the tail wait — which the cooperative variant
+(``launch_fused_steps_cooperative``, every block co-resident) runs too, on small problems.  Reference behaviour: halo_exchange
 (functionspace.py:107-118) then apply_remap (interp.py:206-228), in the order of
 cli.py:138-144; results must be bitwise equal to the oracle apply on the exchanged field."""
 import numpy as np
@@ -340,3 +341,74 @@ def test_emulated_fused_step_structured_bilinear(gpu, P, part):
     for w, plan, src, dst, mesh in ranks:
         exp = O.apply_remap_k(w.nodes, w.weights, gvals[mesh.node_global])
         assert np.array_equal(dst.to_numpy().view(np.uint64), exp.view(np.uint64))
+
+
+@pytest.mark.parametrize("S,T,P,L,part", [("O16", "O32", 2, 7, "blocks"), ("O16", "O24", 4, 33, "equal_regions"),
+                                          ("F8", "O24", 3, 137, "blocks")])  # grids of <= 32 x 148 blocks
+def test_cooperative_emulation_runs_the_tail_waits(gpu, S, T, P, L, part):
+    """The finisher's tail wait (wait_done = 1: an owner waits for every reader's done word
+    before the next epoch may overwrite its rows) exercised on one GPU: every rank in ONE
+    cooperative launch (all blocks co-resident), so a rank's last block may spin on the done
+    words that other ranks' blocks of the same grid write.  Exchange + step, three epochs,
+    bitwise vs the oracle, done words = epochs."""
+    sg = gpu
+    from oracle import oracle as O
+    from paper_1908_07038_b200.device import DeviceArray, synchronize
+    from paper_1908_07038_b200.execute import (emulated_exchanges, emulated_fused_steps,
+                                               launch_exchanges_cooperative, launch_fused_steps_cooperative)
+
+    Sg, Tg = sg.grid_from_name(S), sg.grid_from_name(T)
+    gvals = np.random.default_rng(P * 31 + L).normal(size=(Sg.npts + 2, L))
+    ranks = _ranks(sg, Sg, Tg, P, L, part, gvals)
+    xf = []
+    for r in ranks:
+        d = DeviceArray(r[2].shape[0], L, np.float64)
+        d.upload(np.where(r[5].node_ghost[:, None], 0.0, gvals[r[5].node_global]))
+        xf.append(d)
+    xs = emulated_exchanges([(r[1], d) for r, d in zip(ranks, xf)])
+    steps = emulated_fused_steps([r[:4] for r in ranks])
+    for _ in range(3):
+        launch_exchanges_cooperative(xs)
+        launch_fused_steps_cooperative(steps)
+    synchronize(0)
+    assert sum(s.n_boundary for s in steps) > 0
+    for i, (w, plan, src, dst, n_owned, mesh) in enumerate(ranks):
+        assert np.array_equal(xf[i].to_numpy(), gvals[mesh.node_global])
+        exp = O.apply_remap(w.nodes, w.weights, gvals[mesh.node_global])
+        assert np.array_equal(dst.to_numpy().view(np.uint64), exp.view(np.uint64)), f"rank {i}"
+        for words in (xs[i].signal.read(), steps[i].signal.read()):
+            assert words["epoch"] == 3 and words["error"] == 0 and words["count"] == 0
+            assert all(words["done"][p] == 3 for p in plan.send)
+            assert all(words["ready"][p] == 3 for p in plan.recv)
+
+
+def test_tail_wait_times_out_when_a_reader_never_reads(gpu):
+    """wait_done = 1 really waits: rank 0 alone (owners' ready words published ahead, so only
+    the tail wait can block) waits for its readers' done words, which never come; the bounded
+    wait sets the error word instead of hanging."""
+    sg = gpu
+    from paper_1908_07038_b200.device import synchronize
+    from paper_1908_07038_b200.execute import emulated_fused_steps, launch_fused_steps
+
+    Sg, Tg = sg.grid_from_name("O32"), sg.grid_from_name("O48")
+    ranks = _ranks(sg, Sg, Tg, 2, 4, "blocks", np.zeros((Sg.npts + 2, 4)))
+    steps = emulated_fused_steps([r[:4] for r in ranks])
+    assert ranks[0][1].send  # rank 1 reads rank 0's rows
+    steps[0].signal.publish_owners_ahead(1)
+    steps[0].set_timeout(1e-3)
+    launch_fused_steps(steps[:1], wait_done=True)
+    synchronize(0)
+    with pytest.raises(sg.SpheregridError, match="timed out"):
+        steps[0].check()
+
+
+def test_cooperative_launch_refuses_a_grid_that_does_not_fit(gpu):
+    sg = gpu
+    from paper_1908_07038_b200 import _native as N
+    from paper_1908_07038_b200.execute import emulated_fused_steps, launch_fused_steps_cooperative
+
+    Sg, Tg = sg.grid_from_name("O400"), sg.grid_from_name("O800")
+    ranks = _ranks(sg, Sg, Tg, 2, 1, "blocks", np.zeros((Sg.npts + 2, 1)))
+    steps = emulated_fused_steps([r[:4] for r in ranks])
+    with pytest.raises(N.NativeError, match="co-resident"):
+        launch_fused_steps_cooperative(steps)
