@@ -41,7 +41,7 @@ void launch_apply(ApplyArgs a, int variant, cudaStream_t st);
 int gather_piece_rows(int levels);
 bool gather_fits(int levels);
 void launch_gather_tma(const double* host, int64_t host_rows, const int2* pieces, const int64_t* pdst, double* out,
-                       int64_t p0, int64_t p1, int levels, int piece_rows, cudaStream_t st);
+                       int64_t p0, int64_t p1, int levels, int piece_rows, cudaStream_t st, int ctas_per_sm = 2);
 
 }  // namespace detail
 }  // namespace sg

@@ -35,6 +35,7 @@ struct HostPlan {
   std::vector<std::vector<std::pair<int64_t, int64_t>>> runs;  // chunk c: referenced source rows
   int64_t rows_copied = 0;
   cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
+  cudaStream_t s_in2 = nullptr;  // gather mode: odd chunks' gathers (overlaps consecutive gathers' tails)
   std::vector<cudaEvent_t> ev_in, ev_cmp;
   std::vector<int4> idx_host;           // stencil copy (compact rebuilds)
   std::vector<unsigned char> mark_host; // referenced source rows
@@ -86,6 +87,15 @@ inline void copy_rows_nt(char* dst, const char* src, size_t bytes) {
 // reads than warp loads: tools/probes/pcie_gather_probe.cu measured 50.5 GB/s vs 48.6 for the
 // warp-per-row gather below (DMA of every row: 55.6 GB/s, but on 1/0.77 more bytes).
 constexpr int kGatherStages = 4;
+constexpr int kGatherStreams = 1;
+constexpr int kGatherCtasPerSM = 4;  // 113.8-114.6 ms vs 115.3-115.6 at 2 (profiles/r02_e2e_gather_knobs.jsonl)
+
+int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  const int x = atoi(v);
+  return x < lo ? lo : (x > hi ? hi : x);
+}
 constexpr int kGatherPieceDoubles = 12 * 137;  // ~13 KB per stage
 
 __global__ void __launch_bounds__(160) gather_tma(const double* __restrict__ host, int64_t host_rows,
@@ -194,13 +204,14 @@ int gather_piece_rows(int levels) { return std::max(1, kGatherPieceDoubles / lev
 bool gather_fits(int levels) { return (size_t)levels * 8 + 16 <= (size_t)kGatherPieceDoubles * 8; }
 
 void launch_gather_tma(const double* host, int64_t host_rows, const int2* pieces, const int64_t* pdst, double* out,
-                       int64_t p0, int64_t p1, int levels, int piece_rows, cudaStream_t st) {
+                       int64_t p0, int64_t p1, int levels, int piece_rows, cudaStream_t st, int ctas_per_sm) {
   if (p1 <= p0) return;
   const int slot = gather_slot(levels, piece_rows);
   const size_t smem = 128 + (size_t)kGatherStages * slot * 8;
   SG_CUDA(cudaFuncSetAttribute(gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  // two CTAs per SM (4 stages x ~13 KB each): the apply of the previous chunk co-resides
-  const unsigned grid = (unsigned)std::min<int64_t>(p1 - p0, 148 * 2);
+  // ctas_per_sm CTAs per SM (4 stages x ~13 KB each; 4 x 53 KB fit): the apply of the
+  // previous chunk (no shared memory) co-resides
+  const unsigned grid = (unsigned)std::min<int64_t>(p1 - p0, 148 * ctas_per_sm);
   gather_tma<<<grid, 160, smem, st>>>(host, host_rows, pieces, pdst, out, p0, p1, levels, slot);
   SG_CUDA_LAUNCH();
 }
@@ -284,6 +295,7 @@ HostPlan* host_plan(Stencil* s, int nchunks) {
   SG_CUDA(cudaStreamCreateWithFlags(&hp->s_in, cudaStreamNonBlocking));
   SG_CUDA(cudaStreamCreateWithFlags(&hp->s_cmp, cudaStreamNonBlocking));
   SG_CUDA(cudaStreamCreateWithFlags(&hp->s_out, cudaStreamNonBlocking));
+  SG_CUDA(cudaStreamCreateWithFlags(&hp->s_in2, cudaStreamNonBlocking));
   hp->ev_in.resize(nchunks);
   hp->ev_cmp.resize(nchunks);
   for (int c = 0; c < nchunks; ++c) {
@@ -560,6 +572,7 @@ void Stencil::destroy_host_plan() {
   if (hp->s_in) cudaStreamDestroy(hp->s_in);
   if (hp->s_cmp) cudaStreamDestroy(hp->s_cmp);
   if (hp->s_out) cudaStreamDestroy(hp->s_out);
+  if (hp->s_in2) cudaStreamDestroy(hp->s_in2);
   if (cur != device && cur >= 0) cudaSetDevice(cur);
   delete hp;
   host_plan = nullptr;
@@ -624,6 +637,9 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
   // TMA ring stage must hold at least one 16-B aligned row superset; flags bit 3 forces the
   // warp-per-row gather (kept for comparison)
   const bool tma_gather = gather && !(flags & 8) && gather_fits(p.levels);
+  // measurement knobs of the gather pipeline (tools/e2e_sweep.py): gather streams, CTAs per SM
+  const int gather_streams = env_int("SG_GATHER_STREAMS", kGatherStreams, 1, 2);
+  const int gather_ctas = env_int("SG_GATHER_CTAS", kGatherCtasPerSM, 1, 8);
   std::vector<const double*> gsrc_host(gather ? nfields : 0);
   for (int f = 0; f < (int)gsrc_host.size(); ++f)
     gsrc_host[f] = static_cast<const double*>(mapped(host_src[f], "gather"));
@@ -673,16 +689,22 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
         goto issued;
       }
       if (gather) {  // GPU gather of the chunk's referenced rows from the mapped user array
+        // two gather streams: chunk c+1's gather starts while chunk c's last CTAs drain, so
+        // the link does not idle at every chunk boundary; the apply of chunk c waits for the
+        // gathers of chunks c and c-1 (each stream is ordered, so that covers every chunk <= c)
+        cudaStream_t gs = (gather_streams > 1 && (c & 1)) ? hp->s_in2 : hp->s_in;
         for (int f = 0; f < nfields; ++f) {
           if (tma_gather)
             launch_gather_tma(gsrc_host[f], s->source_nnodes, hp->pieces.as<int2>(), hp->pdst.as<int64_t>(),
-                              hp->csrc[f]->as<double>(), hp->pb[c], hp->pb[c + 1], p.levels, hp->piece_rows, hp->s_in);
+                              hp->csrc[f]->as<double>(), hp->pb[c], hp->pb[c + 1], p.levels, hp->piece_rows, gs,
+                              gather_ctas);
           else
             launch_gather_rows(gsrc_host[f], hp->gsrc.as<int32_t>(), hp->csrc[f]->as<double>(), hp->cb[c],
-                               hp->cb[c + 1], p.levels, hp->s_in);
+                               hp->cb[c + 1], p.levels, gs);
         }
         copied += hp->cb[c + 1] - hp->cb[c];
-        SG_CUDA(cudaEventRecord(hp->ev_in[c], hp->s_in));
+        SG_CUDA(cudaEventRecord(hp->ev_in[c], gs));
+        if (gather_streams > 1 && c > 0) SG_CUDA(cudaStreamWaitEvent(hp->s_cmp, hp->ev_in[c - 1], 0));
         goto issued;
       }
       {
@@ -746,6 +768,7 @@ int32_t sg_remap_execute_host(uint64_t stencil, const uint64_t* src_fields, cons
   SG_CUDA(cudaStreamSynchronize(hp->s_out));
   SG_CUDA(cudaStreamSynchronize(hp->s_cmp));
   SG_CUDA(cudaStreamSynchronize(hp->s_in));
+  SG_CUDA(cudaStreamSynchronize(hp->s_in2));
   if (out_rows_copied) *out_rows_copied = compact ? copied : hp->rows_copied;
   SG_API_END
 }
