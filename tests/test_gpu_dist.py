@@ -100,3 +100,84 @@ def test_bench_torchrun_two_processes(gpu, extra):
     assert all(h["ghosts_bitwise"] and h["bytes_per_exchange"] > 0 for h in line["halo_sweep"])
     b = [h["bytes_per_exchange"] for h in line["halo_sweep"]]
     assert b[0] < b[1] < b[2]
+
+
+def _signal_worker(rank, world, port, q):
+    """One rank of the signalled step / exchange with its peers' fields AND signal words mapped
+    through CUDA IPC (DistContext.peer_fields / peer_signals), as with one GPU per rank.  Both
+    processes share the test box's GPU, so no launch may wait for the other process: every
+    epoch the owners' ready words are published ahead from the host and the tail wait is off
+    (wait_done = 0).  What this proves across processes: IPC-mapped signal words (system
+    scope) are written by the peer's kernels — ready by its signal kernel, done by its
+    finisher — and ghost rows are read straight from the peer's field."""
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.setdefault("GLOO_SOCKET_IFNAME", "lo")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1908_07038_b200 as sg
+        from oracle import oracle as O
+        from paper_1908_07038_b200.device import DeviceArray, synchronize
+        from paper_1908_07038_b200.execute import (FusedStep, Signal, SignalledExchange, launch_exchanges,
+                                                   launch_fused_steps)
+
+        sg.set_device(0)
+        ctx = sg.DistContext(device=0, transport="ipc")
+        S, T = sg.grid_from_name("O32"), sg.grid_from_name("O48")
+        dist_s = sg.blocks_partition(S, world)
+        mesh = sg.generate_mesh(S, dist_s, rank, halo=2, include_pole=True)
+        fs = sg.NodeColumns(mesh, ctx)
+        plan = fs.exchange_plan
+        w = sg.build_remap(fs, T, sg.matching_partition(T, S, dist_s), ctx)
+        L = 9
+        gvals = np.random.default_rng(44).normal(size=(S.npts + 2, L))
+        init = np.where(mesh.node_ghost[:, None], 0.0, gvals[mesh.node_global])
+        src, xf = DeviceArray(mesh.nb_nodes, L, np.float64), DeviceArray(mesh.nb_nodes, L, np.float64)
+        src.upload(init)
+        xf.upload(init)
+        dst = DeviceArray(len(w), L, np.float64)
+        sig, xsig = Signal(0, world, rank), Signal(0, world, rank)
+        step = FusedStep(w, plan, src, dst, sig, ctx.peer_fields(src, plan), ctx.peer_signals(sig))
+        x = SignalledExchange(plan, xf, xsig, ctx.peer_fields(xf, plan), ctx.peer_signals(xsig))
+        epochs = 3
+        for e in range(1, epochs + 1):
+            sig.publish_owners_ahead(e)
+            xsig.publish_owners_ahead(e)
+            synchronize(0)
+            ctx.barrier()  # every rank's rows final and no peer kernel in flight
+            launch_exchanges([x], wait_done=False)
+            launch_fused_steps([step], wait_done=False)
+            synchronize(0)
+            ctx.barrier()
+        exp = O.apply_remap(w.nodes, w.weights, gvals[mesh.node_global])
+        ok_step = bool(np.array_equal(dst.to_numpy().view(np.uint64), exp.view(np.uint64)))
+        ok_x = bool(np.array_equal(xf.to_numpy(), gvals[mesh.node_global]))
+        ws, wx = sig.read(), xsig.read()
+        done_ok = all(ws["done"][p] == epochs and wx["done"][p] == epochs for p in plan.send)
+        words_ok = (ws["epoch"] == wx["epoch"] == epochs and ws["error"] == wx["error"] == 0
+                    and ws["count"] == wx["count"] == 0)
+        q.put((rank, ok_step, ok_x, bool(done_ok and words_ok), int(step.n_boundary), len(plan.send)))
+        ctx.barrier()
+        ctx.close_ipc()
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, False, False, False, repr(e), 0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_signalled_step_with_ipc_signals_across_processes(gpu, world):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_signal_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(o[1] and o[2] and o[3] for o in out), out
+    assert sum(o[4] for o in out) > 0 and all(o[5] > 0 for o in out), out  # peer reads and readers exist
