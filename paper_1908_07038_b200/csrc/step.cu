@@ -126,19 +126,28 @@ static_assert(sizeof(Group) <= 32000, "kernel parameters are limited to 32764 by
 // Scope of a flag access: .sys when the other side of the flag is another GPU (NVLink / IPC),
 // .gpu when it is this GPU (ranks of a single-GPU emulation) — a .sys release under load costs
 // tens of µs more than a .gpu one (tools/xchg_sweep.py, profiles/r02_fused_step.md).
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p, bool sys) {
+// One fence + relaxed (strong) accesses instead of a release / acquire per peer: a release
+// fence followed by a strong store is a release pattern, a strong load followed by an acquire
+// fence an acquire pattern (PTX memory model) — one MEMBAR per rank instead of one per peer.
+__device__ __forceinline__ void fence_acq_rel(bool sys) {
+  if (sys)
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p, bool sys) {
   unsigned long long v;
   if (sys)
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   else
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v, bool sys) {
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v, bool sys) {
   if (sys)
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
   else
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 // Programmatic dependent launch: the signal kernel lets the step / pull kernel start at once
 // (interior targets need nothing from it); code that reads the current epoch the signal kernel
@@ -159,12 +168,13 @@ __device__ __forceinline__ unsigned long long atom_add_acq_rel(unsigned long lon
   return old;
 }
 
-// Spin until *p >= e; false (and the error word set) after timeout_ns.
+// Spin until *p >= e (strong relaxed loads: the caller fences once after all its waits);
+// false (and the error word set) after timeout_ns.
 __device__ bool wait_geq(const unsigned long long* p, unsigned long long e, unsigned long long* err, int code,
                          unsigned long long timeout_ns, bool sys) {
-  if (ld_acquire(p, sys) >= e) return true;
+  if (ld_relaxed(p, sys) >= e) return true;
   const unsigned long long t0 = now_ns();
-  while (ld_acquire(p, sys) < e) {
+  while (ld_relaxed(p, sys) < e) {
     __nanosleep(64);
     if (now_ns() - t0 > timeout_ns) {
       atomicExch(err, (unsigned long long)code);
@@ -260,13 +270,23 @@ __device__ __forceinline__ void apply_target(const StepArgs& d, int64_t t, int4 
 // then (one GPU per rank) wait until every reader of my rows is done; epoch = e.
 __device__ void finish_epoch(unsigned long long* f, int nr, int rank, const PeerTable& P, unsigned long long e,
                              int wait_done, unsigned long long timeout_ns) {
-  // each st.release.sys orders this thread's (and, through the acq_rel count, every counted
-  // block's) earlier reads of the peers' rows before the done word
+  // one release fence orders this thread's (and, through the acq_rel count, every counted
+  // block's) earlier reads of the peers' rows before every done word
+  bool any = false, sys = false;
   for (int s = 0; s < P.npeers; ++s)
-    if (P.role[s] & kRoleRecv) st_release(P.flags[s] + w_done(nr, rank), e, P.sys[s]);
-  if (wait_done)
+    if (P.role[s] & kRoleRecv) any = true, sys |= P.sys[s];
+  if (any) fence_acq_rel(sys);
+  for (int s = 0; s < P.npeers; ++s)
+    if (P.role[s] & kRoleRecv) st_relaxed(P.flags[s] + w_done(nr, rank), e, P.sys[s]);
+  if (wait_done) {
+    bool wsys = false, waited = false;
     for (int s = 0; s < P.npeers; ++s)
-      if (P.role[s] & kRoleSend) wait_geq(f + w_done(nr, P.rank[s]), e, f + w_error(nr), 2, timeout_ns, P.sys[s]);
+      if (P.role[s] & kRoleSend) {
+        wait_geq(f + w_done(nr, P.rank[s]), e, f + w_error(nr), 2, timeout_ns, P.sys[s]);
+        waited = true, wsys |= P.sys[s];
+      }
+    if (waited) fence_acq_rel(wsys);  // acquire: the readers are done before the next epoch writes
+  }
   f[w_count(nr)] = 0;
   f[w_epoch(nr)] = e;
 }
@@ -279,8 +299,12 @@ __device__ void publish_ready(unsigned long long* f, int nr, int rank, const Pee
   f[w_cur(nr)] = e;
   // the owned rows were written by earlier kernels of this stream (complete); the release store
   // orders them before the ready word at system scope — no separate fence.sc.sys (18 µs here)
+  bool any = false, sys = false;
   for (int s = 0; s < P.npeers; ++s)
-    if (P.role[s] & kRoleSend) st_release(P.flags[s] + w_ready(rank), e, P.sys[s]);
+    if (P.role[s] & kRoleSend) any = true, sys |= P.sys[s];
+  if (any) fence_acq_rel(sys);
+  for (int s = 0; s < P.npeers; ++s)
+    if (P.role[s] & kRoleSend) st_relaxed(P.flags[s] + w_ready(rank), e, P.sys[s]);
 }
 
 // Every owner of this rank's ghosts has published epoch e (one thread; acquire at the owner's
@@ -289,8 +313,13 @@ __device__ void publish_ready(unsigned long long* f, int nr, int rank, const Pee
 // an acquire of its own.
 __device__ void wait_owners(unsigned long long* f, int nr, const PeerTable& P, unsigned long long timeout_ns) {
   const unsigned long long e = f[w_cur(nr)];
+  bool any = false, sys = false;
   for (int s = 0; s < P.npeers; ++s)
-    if (P.role[s] & kRoleRecv) wait_geq(f + w_ready(P.rank[s]), e, f + w_error(nr), 1, timeout_ns, P.sys[s]);
+    if (P.role[s] & kRoleRecv) {
+      wait_geq(f + w_ready(P.rank[s]), e, f + w_error(nr), 1, timeout_ns, P.sys[s]);
+      any = true, sys |= P.sys[s];
+    }
+  if (any) fence_acq_rel(sys);  // acquire pattern over every owner's ready word
 }
 
 __global__ void signal_kernel(Group g) {
