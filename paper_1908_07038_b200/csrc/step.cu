@@ -293,45 +293,48 @@ __device__ void finish_epoch(unsigned long long* f, int nr, int rank, const Peer
 __device__ void finish_step(const StepArgs& d, unsigned long long e, int wait_done) {
   finish_epoch(d.flags, d.nranks, d.rank, d.peers, e, wait_done, d.timeout_ns);
 }
-// ready[me] = epoch + 1 into every reader's words (one thread per rank)
-__device__ void publish_ready(unsigned long long* f, int nr, int rank, const PeerTable& P) {
-  const unsigned long long e = f[w_epoch(nr)] + 1;
-  f[w_cur(nr)] = e;
-  // the owned rows were written by earlier kernels of this stream (complete); the release store
-  // orders them before the ready word at system scope — no separate fence.sc.sys (18 µs here)
-  bool any = false, sys = false;
-  for (int s = 0; s < P.npeers; ++s)
-    if (P.role[s] & kRoleSend) any = true, sys |= P.sys[s];
-  if (any) fence_acq_rel(sys);
-  for (int s = 0; s < P.npeers; ++s)
-    if (P.role[s] & kRoleSend) st_relaxed(P.flags[s] + w_ready(rank), e, P.sys[s]);
+// The signal kernels: one thread per (rank, peer slot) of the launch, so the flag accesses of
+// all peers go out in parallel instead of one after another.
+//  * publish: ready[me] = epoch + 1 into every reader's words.  The owned rows were written by
+//    earlier kernels of this stream (complete); a release fence + strong store orders them
+//    before the ready word at the reader's scope (no separate fence.sc.sys: 18 µs here).
+//  * after __syncthreads (every rank of a single-GPU emulation has published): wait until each
+//    owner of this rank's ghosts published the same epoch, then an acquire fence.  The step /
+//    pull kernel that depends on the signal kernel (griddepcontrol.wait) reads the owners' rows
+//    without an acquire of its own.
+constexpr int kSignalThreads = kMaxGroup * kPeers;
+
+template <class G>
+__device__ void signal_body(const G& g, bool (*needs_owners)(const G&, int)) {
+  const int r = threadIdx.x / kPeers, s = threadIdx.x % kPeers;
+  const bool rank_ok = r < g.n;
+  const bool live = rank_ok && s < g.d[r].peers.npeers;
+  unsigned long long* f = rank_ok ? g.d[r].flags : nullptr;
+  const int nr = rank_ok ? g.d[r].nranks : 0;
+  const unsigned long long e = rank_ok ? f[w_epoch(nr)] + 1 : 0;
+  if (rank_ok && s == 0) f[w_cur(nr)] = e;
+  if (live && (g.d[r].peers.role[s] & kRoleSend)) {
+    const bool sys = g.d[r].peers.sys[s];
+    fence_acq_rel(sys);
+    st_relaxed(g.d[r].peers.flags[s] + w_ready(g.d[r].rank), e, sys);
+  }
+  __syncthreads();
+  if (live && (g.d[r].peers.role[s] & kRoleRecv) && needs_owners(g, r)) {
+    const bool sys = g.d[r].peers.sys[s];
+    wait_geq(f + w_ready(g.d[r].peers.rank[s]), e, f + w_error(nr), 1, g.d[r].timeout_ns, sys);
+    fence_acq_rel(sys);  // acquire pattern over the owner's ready word
+  }
 }
 
-// Every owner of this rank's ghosts has published epoch e (one thread; acquire at the owner's
-// scope).  Runs in the signal kernel after ALL ranks of the launch published theirs, so the
-// step / pull kernel that depends on it (griddepcontrol.wait) reads the owners' rows without
-// an acquire of its own.
-__device__ void wait_owners(unsigned long long* f, int nr, const PeerTable& P, unsigned long long timeout_ns) {
-  const unsigned long long e = f[w_cur(nr)];
-  bool any = false, sys = false;
-  for (int s = 0; s < P.npeers; ++s)
-    if (P.role[s] & kRoleRecv) {
-      wait_geq(f + w_ready(P.rank[s]), e, f + w_error(nr), 1, timeout_ns, P.sys[s]);
-      any = true, sys |= P.sys[s];
-    }
-  if (any) fence_acq_rel(sys);  // acquire pattern over every owner's ready word
-}
+__device__ bool step_needs_owners(const Group& g, int r) { return g.d[r].n_boundary > 0; }
 
-__global__ void signal_kernel(Group g) {
+__global__ void __launch_bounds__(kSignalThreads) signal_kernel(Group g) {
   // launched with PDL too: it may start during the previous kernel's last wave (which calls
   // launch_dependents), but waits for that kernel's completion and memory before it reads the
   // epoch or publishes anything — only its launch latency is hidden
   pdl_wait_primary();
   pdl_release_dependents();
-  const int r = threadIdx.x;
-  if (r < g.n) publish_ready(g.d[r].flags, g.d[r].nranks, g.d[r].rank, g.d[r].peers);
-  __syncthreads();  // every rank of this launch has published (single-GPU emulation)
-  if (r < g.n && g.d[r].n_boundary > 0) wait_owners(g.d[r].flags, g.d[r].nranks, g.d[r].peers, g.d[r].timeout_ns);
+  signal_body(g, step_needs_owners);
 }
 
 constexpr int kWarps = 2;  // targets per block: small blocks retire and refill (apply.cu)
@@ -415,13 +418,12 @@ static_assert(sizeof(XGroup) <= 32000, "kernel parameters are limited to 32764 b
 
 constexpr int kXWarps = 8;
 
-__global__ void xsignal_kernel(XGroup g) {
+__device__ bool xchg_needs_owners(const XGroup& g, int r) { return g.d[r].n > 0; }
+
+__global__ void __launch_bounds__(kSignalThreads) xsignal_kernel(XGroup g) {
   pdl_wait_primary();  // as signal_kernel
   pdl_release_dependents();
-  const int r = threadIdx.x;
-  if (r < g.n) publish_ready(g.d[r].flags, g.d[r].nranks, g.d[r].rank, g.d[r].peers);
-  __syncthreads();  // every rank of this launch has published (single-GPU emulation)
-  if (r < g.n && g.d[r].n > 0) wait_owners(g.d[r].flags, g.d[r].nranks, g.d[r].peers, g.d[r].timeout_ns);
+  signal_body(g, xchg_needs_owners);
 }
 
 // A block moves kXRows ghost rows per warp (kXWarps warps): after griddepcontrol.wait (the
@@ -723,7 +725,7 @@ static void step_launch(const uint64_t* steps, int32_t n, int32_t wait_done, uin
   SG_REQUIRE(g.start[n] < INT32_MAX, "too many targets for one launch");
   DeviceScope ds(device);
   cudaStream_t s = as_stream(stream);
-  launch_pdl(signal_kernel, 1, 32, s, g);
+  launch_pdl(signal_kernel, 1, kSignalThreads, s, g);
   const unsigned grid = (unsigned)g.start[n];
   switch ((levels + 31) / 32) {
     case 1: launch_pdl(step_kernel<1>, grid, kWarps * 32, s, g, coop); break;
@@ -843,7 +845,7 @@ static void exchange_launch(const uint64_t* exchanges, int32_t n, int32_t wait_d
                                                                                   (kXWarps * kXRows)));
   DeviceScope ds(device);
   cudaStream_t s = as_stream(stream);
-  launch_pdl(xsignal_kernel, 1, 32, s, g);
+  launch_pdl(xsignal_kernel, 1, kSignalThreads, s, g);
   const unsigned grid = (unsigned)g.start[n];
   const int it = (W + 31) / 32;
 #define SG_XLAUNCH(Wd)                                                            \
