@@ -444,19 +444,33 @@ __global__ void __launch_bounds__(kXWarps * 32) xchg_kernel(XGroup g) {
   unsigned long long* f = d.flags;
   const int nr = d.nranks;
   const PeerTable& P = d.peers;
+  // resident grid: each warp moves kXRows rows per iteration, blocks stride over the rank's rows
+  const int64_t stride = nb * kXWarps * kXRows;
+  int64_t i0 = (b * kXWarps + (threadIdx.x >> 5)) * kXRows;
+  // the next iteration's ghost / owner / slot indices are loaded while this iteration's rows
+  // are in flight: one memory round trip per iteration instead of two
+  int nslot[kXRows], nrem[kXRows], nrow[kXRows];
+  if (IT > 0 && i0 < d.n) {
+#pragma unroll
+    for (int q = 0; q < kXRows; ++q) {
+      const int64_t i = min(i0 + q, d.n - 1);  // a short tail repeats the last row (idempotent)
+      nslot[q] = __ldg(d.slot + i);
+      nrem[q] = __ldg(d.remote + i);
+      nrow[q] = __ldg(d.rows + i);
+    }
+  }
+  // (the plan's index arrays are static: their first loads above overlap the signal kernel)
   pdl_wait_primary();  // the signal kernel has seen every owner's ready word for this epoch
   const unsigned long long e_sh = *(volatile unsigned long long*)(f + w_cur(nr));
-  // resident grid: each warp moves kXRows rows per iteration, blocks stride over the rank's rows
-  for (int64_t i0 = (b * kXWarps + (threadIdx.x >> 5)) * kXRows; i0 < d.n; i0 += nb * kXWarps * kXRows) {
+  for (; i0 < d.n; i0 += stride) {
     if (IT > 0) {
       const Wd* src[kXRows];
       Wd* dst[kXRows];
 #pragma unroll
       for (int q = 0; q < kXRows; ++q) {
-        const int64_t i = min(i0 + q, d.n - 1);  // a short tail repeats the last row (idempotent)
-        const int s = __ldg(d.slot + i);
-        src[q] = static_cast<const Wd*>(P.base_any[s]) + (int64_t)__ldg(d.remote + i) * P.pitch[s];
-        dst[q] = static_cast<Wd*>(d.base) + (int64_t)__ldg(d.rows + i) * d.pitch;
+        const int s = nslot[q];
+        src[q] = static_cast<const Wd*>(P.base_any[s]) + (int64_t)nrem[q] * P.pitch[s];
+        dst[q] = static_cast<Wd*>(d.base) + (int64_t)nrow[q] * d.pitch;
       }
       Wd v[kXRows][IT > 0 ? IT : 1];
 #pragma unroll
@@ -464,6 +478,15 @@ __global__ void __launch_bounds__(kXWarps * 32) xchg_kernel(XGroup g) {
 #pragma unroll
         for (int k = 0; k < IT; ++k)
           if (lane + 32 * k < d.W) v[q][k] = ld_weak(src[q] + lane + 32 * k);
+      if (i0 + stride < d.n) {
+#pragma unroll
+        for (int q = 0; q < kXRows; ++q) {
+          const int64_t i = min(i0 + stride + q, d.n - 1);
+          nslot[q] = __ldg(d.slot + i);
+          nrem[q] = __ldg(d.remote + i);
+          nrow[q] = __ldg(d.rows + i);
+        }
+      }
 #pragma unroll
       for (int q = 0; q < kXRows; ++q)
 #pragma unroll
