@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(kSignalThreads) xsignal_kernel(XGroup g) {
 // before its stores (4 rows x IT words in flight per lane: the copy is latency-bound
 // otherwise); the last block to finish (acq_rel count) finishes the epoch.
 constexpr int kXRows = 4;
-constexpr int kXBlocksPerSM = 4;  // 256 threads x 64 registers: 4 resident blocks per SM
+constexpr int kXBlocksPerSM = 3;  // 256 threads x 80 registers: 3 resident blocks per SM (r02_exchange_xblocks.jsonl)
 
 template <typename Wd, int IT>
 __global__ void __launch_bounds__(kXWarps * 32) xchg_kernel(XGroup g) {
