@@ -303,8 +303,12 @@ class DistContext:
         if transport not in ("nvlink", "nccl", "ipc"):
             raise ValueError(f"unknown transport {transport!r}")
         self.transport = transport
-        self._ipc: Dict[int, tuple] = {}  # peer rank -> (ipc handle bytes, mapped ptr, device)
-        self._ipc_sig: Dict[int, tuple] = {}  # same, for the peers' step signals
+        # CUDA-IPC mappings of peers' buffers, (peer rank, ipc handle bytes, device) -> mapped
+        # pointer, kept until close_ipc: several objects (a remap's fused step, an exchange of
+        # another field, ...) may use several of a peer's buffers at the same time, so a new
+        # buffer never unmaps an old one that an existing kernel argument still points into
+        self._ipc: Dict[tuple, int] = {}
+        self._ipc_sig: Dict[tuple, int] = {}  # same, for the peers' step signal words
         self._dist = dist
         self.rank = dist.get_rank()
         self.nranks = dist.get_world_size()
@@ -412,11 +416,28 @@ class DistContext:
         N.call("sg_comm_info", self.nccl_comm(), *[N.ref(x) for x in v])
         return {"nranks": v[0].value, "rank": v[1].value, "device": v[2].value, "nccl_version": v[3].value}
 
+    @staticmethod
+    def _ipc_map(cache: Dict[tuple, int], r: int, blob: bytes, device: int) -> int:
+        """This process's mapping of peer r's buffer with IPC handle ``blob`` (opened once)."""
+        import ctypes as C
+
+        from . import _native as N
+
+        key = (r, blob, device)
+        ptr = cache.get(key)
+        if ptr is None:
+            p = C.c_uint64(0)
+            hb = (C.c_uint8 * 64).from_buffer_copy(blob)
+            N.call("sg_ipc_open", device, N.ref(hb), 64, N.ref(p))
+            ptr = cache[key] = p.value
+        return ptr
+
     def peer_fields(self, dev_array, plan=None) -> list:
         """(ptr, pitch, device) of every rank's copy of this field, via CUDA IPC.  Collective
-        on every call (each rank may pass a different buffer per call); a peer's mapping is
-        reused while its IPC handle is unchanged and closed when the peer's buffer changes.
-        Plans must carry their owner rows (``recv_remote``, set by build_exchange_plan)."""
+        on every call (each rank may pass a different buffer per call); each peer buffer is
+        mapped once and stays mapped until close_ipc, so objects built on earlier calls keep
+        valid pointers.  Plans must carry their owner rows (``recv_remote``, set by
+        build_exchange_plan)."""
         import ctypes as C
 
         from . import _native as N
@@ -428,24 +449,13 @@ class DistContext:
         for r, (blob, pitch, dev) in enumerate(everyone):
             if r == self.rank:
                 got.append((dev_array.ptr, dev_array.pitch, dev_array.device))
-                continue
-            old = self._ipc.get(r)
-            if old is not None and old[0] == blob and old[2] == dev_array.device:
-                got.append((old[1], pitch, dev))
-                continue
-            if old is not None:
-                N.call("sg_ipc_close", old[2], old[1])
-            p = C.c_uint64(0)
-            hb = (C.c_uint8 * 64).from_buffer_copy(blob)
-            N.call("sg_ipc_open", dev_array.device, N.ref(hb), 64, N.ref(p))
-            self._ipc[r] = (blob, p.value, dev_array.device)
-            got.append((p.value, pitch, dev))
+            else:
+                got.append((self._ipc_map(self._ipc, r, blob, dev_array.device), pitch, dev))
         return got
 
     def peer_signals(self, signal) -> list:
         """(pointer to rank r's step signal words, mapped here through CUDA IPC, device uuid)
-        for every rank.  Collective; mappings are cached per peer while its handle is
-        unchanged and closed by close_ipc."""
+        for every rank.  Collective; each peer signal is mapped once, until close_ipc."""
         import ctypes as C
 
         from . import _native as N
@@ -457,23 +467,16 @@ class DistContext:
         for r, (blob, uuid) in enumerate(everyone):
             if r == self.rank:
                 got.append((signal.ptr, uuid))
-                continue
-            old = self._ipc_sig.get(r)
-            if old is None or old[0] != blob:
-                if old is not None:
-                    N.call("sg_ipc_close", old[2], old[1])
-                p = C.c_uint64(0)
-                hb = (C.c_uint8 * 64).from_buffer_copy(blob)
-                N.call("sg_ipc_open", signal.device, N.ref(hb), 64, N.ref(p))
-                old = self._ipc_sig[r] = (blob, p.value, signal.device)
-            got.append((old[1], uuid))
+            else:
+                got.append((self._ipc_map(self._ipc_sig, r, blob, signal.device), uuid))
         return got
 
     def close_ipc(self) -> None:
-        """Unmap every peer field and step signal opened through CUDA IPC."""
+        """Unmap every peer field and step signal opened through CUDA IPC (call when no kernel
+        that uses them is pending: after the last step / exchange of this context)."""
         from . import _native as N
 
-        for _, ptr, dev in list(self._ipc.values()) + list(self._ipc_sig.values()):
+        for (_, _, dev), ptr in list(self._ipc.items()) + list(self._ipc_sig.items()):
             N.call("sg_ipc_close", dev, ptr)
         self._ipc.clear()
         self._ipc_sig.clear()

@@ -130,7 +130,7 @@ def _signal_worker(rank, world, port, q):
         fs = sg.NodeColumns(mesh, ctx)
         plan = fs.exchange_plan
         w = sg.build_remap(fs, T, sg.matching_partition(T, S, dist_s), ctx)
-        L = 9
+        L = 300  # > 2 MB per field: separate allocations, not one sub-allocated block
         gvals = np.random.default_rng(44).normal(size=(S.npts + 2, L))
         init = np.where(mesh.node_ghost[:, None], 0.0, gvals[mesh.node_global])
         src, xf = DeviceArray(mesh.nb_nodes, L, np.float64), DeviceArray(mesh.nb_nodes, L, np.float64)
@@ -140,6 +140,12 @@ def _signal_worker(rank, world, port, q):
         sig, xsig = Signal(0, world, rank), Signal(0, world, rank)
         step = FusedStep(w, plan, src, dst, sig, ctx.peer_fields(src, plan), ctx.peer_signals(sig))
         x = SignalledExchange(plan, xf, xsig, ctx.peer_fields(xf, plan), ctx.peer_signals(xsig))
+        # a third peer buffer and signal mapped AFTER the step and exchange were built: their
+        # mappings of the peers' src / signal words must stay valid (large fields get their
+        # own allocation, so an unmap would really unmap)
+        other, osig = DeviceArray(mesh.nb_nodes, 512, np.float64), Signal(0, world, rank)
+        ctx.peer_fields(other, plan)
+        ctx.peer_signals(osig)
         epochs = 3
         for e in range(1, epochs + 1):
             sig.publish_owners_ahead(e)
