@@ -7,6 +7,7 @@
 // referenced rows straight out of the pinned, mapped user array: no host CPU work, no DMA of
 // unreferenced rows) and zero-copy (the apply kernel reads/writes pinned host memory directly).
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 #include <emmintrin.h>
 
 #include <algorithm>
@@ -164,17 +165,17 @@ __global__ void __launch_bounds__(256) gather_rows(const double* __restrict__ ho
   for (int64_t u = u0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); u < u1; u += stride) {
     const double* src = host + (int64_t)__ldg(gsrc + u) * levels;
     double* dst = out + u * levels;
-    if (IT == 0) {
+    if constexpr (IT == 0) {
       for (int l = lane; l < levels; l += 32) dst[l] = src[l];
-      continue;
+    } else {
+      double v[IT];
+#pragma unroll
+      for (int i = 0; i < IT; ++i)
+        if (lane + 32 * i < levels) v[i] = src[lane + 32 * i];
+#pragma unroll
+      for (int i = 0; i < IT; ++i)
+        if (lane + 32 * i < levels) dst[lane + 32 * i] = v[i];
     }
-    double v[IT > 0 ? IT : 1];
-#pragma unroll
-    for (int i = 0; i < IT; ++i)
-      if (lane + 32 * i < levels) v[i] = src[lane + 32 * i];
-#pragma unroll
-    for (int i = 0; i < IT; ++i)
-      if (lane + 32 * i < levels) dst[lane + 32 * i] = v[i];
   }
 }
 
@@ -488,7 +489,7 @@ void device_gather_tables(Stencil* s, HostPlan* hp, int levels, cudaStream_t st)
   SG_CUDA(cub::DeviceScan::InclusiveScan(nullptr, b1, (int32_t*)nullptr, (int32_t*)nullptr, MaxOp(), (int)mm, st));
   SG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b2, (int32_t*)nullptr, (int32_t*)nullptr, (int)(nn + 1), st));
   SG_CUDA(cub::DeviceScan::InclusiveScan(nullptr, b3, (int32_t*)nullptr, (int32_t*)nullptr, MaxOp(), (int)nn, st));
-  SG_CUDA(cub::DeviceSelect::Flagged(nullptr, b4, cub::CountingInputIterator<int32_t>(0), (unsigned char*)nullptr,
+  SG_CUDA(cub::DeviceSelect::Flagged(nullptr, b4, thrust::counting_iterator<int32_t>(0), (unsigned char*)nullptr,
                                      (int32_t*)nullptr, (int64_t*)nullptr, (int)nn, st));
   const Part p_tmp = part(std::max(std::max(b1, b2), std::max(b3, b4)) + 16);
   DevBuf arena;
@@ -513,7 +514,7 @@ void device_gather_tables(Stencil* s, HostPlan* hp, int levels, cudaStream_t st)
     plan_piece_flags<<<gn, 256, 0, st>>>(mark.as<int32_t>(), seg.as<int32_t>(), n, prows, flag.as<unsigned char>());
     SG_CUDA_LAUNCH();
     tb = tmp.bytes;
-    SG_CUDA(cub::DeviceSelect::Flagged(tmp.ptr, tb, cub::CountingInputIterator<int32_t>(0), flag.as<unsigned char>(),
+    SG_CUDA(cub::DeviceSelect::Flagged(tmp.ptr, tb, thrust::counting_iterator<int32_t>(0), flag.as<unsigned char>(),
                                        starts.as<int32_t>(), nsel.as<int64_t>(), (int)n, st));
   } else {
     SG_CUDA(cudaMemsetAsync(nsel.ptr, 0, 8, st));

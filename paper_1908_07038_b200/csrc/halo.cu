@@ -36,24 +36,24 @@ namespace {
 // wider than 8 slices go in chunks of 4 slices.
 template <typename Wd, int IT>
 __device__ __forceinline__ void copy_row(Wd* __restrict__ dst, const Wd* __restrict__ src, int W, int lane) {
-  if (IT > 0) {
-    Wd v[IT > 0 ? IT : 1];
+  if constexpr (IT > 0) {
+    Wd v[IT];
 #pragma unroll
     for (int i = 0; i < IT; ++i)
       if (lane + 32 * i < W) v[i] = src[lane + 32 * i];
 #pragma unroll
     for (int i = 0; i < IT; ++i)
       if (lane + 32 * i < W) dst[lane + 32 * i] = v[i];
-    return;
-  }
-  for (int b = 0; b < W; b += 128) {
-    Wd v[4];
+  } else {
+    for (int b = 0; b < W; b += 128) {
+      Wd v[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (b + lane + 32 * i < W) v[i] = src[b + lane + 32 * i];
+      for (int i = 0; i < 4; ++i)
+        if (b + lane + 32 * i < W) v[i] = src[b + lane + 32 * i];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (b + lane + 32 * i < W) dst[b + lane + 32 * i] = v[i];
+      for (int i = 0; i < 4; ++i)
+        if (b + lane + 32 * i < W) dst[b + lane + 32 * i] = v[i];
+    }
   }
 }
 
@@ -92,34 +92,34 @@ __global__ void __launch_bounds__(256) pull_rows(Wd* __restrict__ f, int64_t pit
   const int64_t r0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kPullRows;
   if (r0 >= n) return;
   const int lane = threadIdx.x & 31;
-  if (IT == 0) {
+  if constexpr (IT == 0) {
     for (int64_t r = r0; r < min(r0 + kPullRows, n); ++r) {
       const int s = slot[r];
       const Wd* src = static_cast<const Wd*>(peers.base[s]) + (int64_t)remote[r] * peers.pitch_w[s];
       copy_row<Wd, 0>(f + (int64_t)rows[r] * pitch_w, src, W, lane);
     }
-    return;
+  } else {
+    const Wd* src[kPullRows];
+    Wd* dst[kPullRows];
+#pragma unroll
+    for (int q = 0; q < kPullRows; ++q) {
+      const int64_t r = min(r0 + q, n - 1);  // a short tail repeats the last row (idempotent)
+      const int s = slot[r];
+      src[q] = static_cast<const Wd*>(peers.base[s]) + (int64_t)remote[r] * peers.pitch_w[s];
+      dst[q] = f + (int64_t)rows[r] * pitch_w;
+    }
+    Wd v[kPullRows][IT];
+#pragma unroll
+    for (int q = 0; q < kPullRows; ++q)
+#pragma unroll
+      for (int i = 0; i < IT; ++i)
+        if (lane + 32 * i < W) v[q][i] = src[q][lane + 32 * i];
+#pragma unroll
+    for (int q = 0; q < kPullRows; ++q)
+#pragma unroll
+      for (int i = 0; i < IT; ++i)
+        if (lane + 32 * i < W) dst[q][lane + 32 * i] = v[q][i];
   }
-  const Wd* src[kPullRows];
-  Wd* dst[kPullRows];
-#pragma unroll
-  for (int q = 0; q < kPullRows; ++q) {
-    const int64_t r = min(r0 + q, n - 1);  // a short tail repeats the last row (idempotent)
-    const int s = slot[r];
-    src[q] = static_cast<const Wd*>(peers.base[s]) + (int64_t)remote[r] * peers.pitch_w[s];
-    dst[q] = f + (int64_t)rows[r] * pitch_w;
-  }
-  Wd v[kPullRows][IT > 0 ? IT : 1];
-#pragma unroll
-  for (int q = 0; q < kPullRows; ++q)
-#pragma unroll
-    for (int i = 0; i < IT; ++i)
-      if (lane + 32 * i < W) v[q][i] = src[q][lane + 32 * i];
-#pragma unroll
-  for (int q = 0; q < kPullRows; ++q)
-#pragma unroll
-    for (int i = 0; i < IT; ++i)
-      if (lane + 32 * i < W) dst[q][lane + 32 * i] = v[q][i];
 }
 
 // Launches KERNEL<Wd, IT> with IT = ceil(W / 32) (0 = chunked loop beyond 8 slices).
