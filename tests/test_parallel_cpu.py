@@ -242,3 +242,39 @@ def test_signalled_exchange_decisions_are_collective(same_gpu):
         # call 1 builds; call 3 rebuilds on BOTH ranks because rank 1's buffer changed
         assert [len(o[2]) for o in out] == [2, 2]
         assert out[1][2] == [1001, 2001] and out[0][2] == [1000, 1000]
+
+
+def test_dist_context_keeps_every_peer_mapping_until_close(monkeypatch):
+    """DistContext's CUDA-IPC mapping cache (host logic, no GPU): each (peer, handle, device)
+    is opened once; sharing a NEW buffer of a peer never unmaps an older one that a built step
+    or exchange may still point into; close_ipc unmaps everything exactly once."""
+    import ctypes
+
+    from paper_1908_07038_b200 import _native as N
+    from paper_1908_07038_b200.parallel import DistContext
+
+    calls = []
+    nxt = iter(range(0x1000, 0x100000, 0x1000))
+
+    def fake_call(name, *args):
+        calls.append(name)
+        if name == "sg_ipc_open":  # (device, handle address, 64, out-pointer address)
+            ctypes.c_uint64.from_address(args[3]).value = next(nxt)
+        elif name == "sg_ipc_close":
+            closed.append(args[1])
+        else:
+            raise AssertionError(name)
+
+    closed = []
+    monkeypatch.setattr(N, "call", fake_call)
+    ctx = DistContext.__new__(DistContext)  # only the cache logic: no process group needed
+    ctx._ipc, ctx._ipc_sig = {}, {}
+    a1 = DistContext._ipc_map(ctx._ipc, 1, b"A" * 64, 0)
+    a1_again = DistContext._ipc_map(ctx._ipc, 1, b"A" * 64, 0)
+    b1 = DistContext._ipc_map(ctx._ipc, 1, b"B" * 64, 0)  # peer 1 shares another buffer
+    a2 = DistContext._ipc_map(ctx._ipc, 2, b"A" * 64, 0)  # same bytes from another peer: own key
+    s1 = DistContext._ipc_map(ctx._ipc_sig, 1, b"S" * 64, 0)
+    assert a1 == a1_again and len({a1, b1, a2, s1}) == 4
+    assert calls.count("sg_ipc_open") == 4 and not closed  # nothing unmapped while in use
+    ctx.close_ipc()
+    assert sorted(closed) == sorted([a1, b1, a2, s1]) and not ctx._ipc and not ctx._ipc_sig
