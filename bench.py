@@ -251,6 +251,42 @@ def import_reference():
     return R, None
 
 
+def reference_threaded(R, nodes, weights, src_hosts, n, L, expect, reps=2):
+    """The reference's own ``apply_remap`` (interp.py:206-228) with every host thread: the
+    targets split into one contiguous chunk per thread, each chunk a reference
+    ``InterpolationWeights`` + target ``Field`` whose host array is a view into one output,
+    all chunks run at once from a thread pool — as the reference's ``run_ranks`` threads would
+    run their ranks' applies (numpy releases the GIL in its gathers and ufuncs).  Returns
+    (best seconds per step, threads, bitwise equal to ``expect``)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    m = len(nodes)
+    nt = max(1, min(os.cpu_count() or 1, 64))
+    bounds = np.linspace(0, m, nt + 1).astype(np.int64)
+    out = np.empty((m, L))
+    parts = []
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        RW = R.InterpolationWeights(target_global=np.arange(a, b, dtype=np.int64),
+                                    nodes=np.ascontiguousarray(nodes[a:b], np.int64),
+                                    weights=np.ascontiguousarray(weights[a:b]), fallback=np.zeros(b - a, bool),
+                                    source_nnodes=n)
+        parts.append((RW, R.Field(name="dst", shape=(int(b - a), L), kind=R.Kind.REAL64, host=out[a:b])))
+    srcs = [R.Field(name=f"src{f}", shape=(n, L), kind=R.Kind.REAL64, host=h) for f, h in enumerate(src_hosts)]
+
+    def step(ex):
+        for sf in srcs:
+            list(ex.map(lambda pr: R.apply_remap(pr[0], sf, pr[1]), parts))
+
+    times = []
+    with ThreadPoolExecutor(nt) as ex:
+        step(ex)  # warm-up
+        for _ in range(reps):
+            t = time.perf_counter()
+            step(ex)
+            times.append(time.perf_counter() - t)
+    return min(times), nt, bool(np.array_equal(out.view(np.uint64), expect.view(np.uint64)))
+
+
 def run_reference(args):
     """--impl reference: the reference's OWN code path on this host, rank 0 only.
 
@@ -322,6 +358,8 @@ def run_reference(args):
     units = m * L * F
     ms = 1e3 * sum(times) / len(times)
     value = units / (ms * 1e-3) / 1e9
+    t_thr, nthr, thr_ok = reference_threaded(R, W.nodes, W.weights, [sf.host for sf in srcs], mesh.nb_nodes, L,
+                                             dsts[-1].host)
     line = {
         "metric": metric_name(source, target, method, L), "value": value, "unit": "Gpts·lev/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -338,7 +376,11 @@ def run_reference(args):
                       "product_imported": "paper_1908_07038_b200" in sys.modules},
         "cpu_baseline": {"value": value, "unit": "Gpts·lev/s", "cores": 1, "kind": "reference",
                          "sample": f"full {source}->{target} apply x{F} field(s) per step: the reference's own "
-                                   "apply_remap (numpy, single-threaded as the reference runs it)"},
+                                   "apply_remap (numpy, single-threaded as the reference runs it at P=1)"},
+        "threaded": {"value": units / t_thr / 1e9, "unit": "Gpts·lev/s", "cores": nthr, "bitwise_vs_1_core": thr_ok,
+                     "sample": f"the same step with {nthr} host threads: the reference's own apply_remap on "
+                               f"{nthr} contiguous target chunks at once (as its run_ranks threads would run "
+                               "P ranks; numpy releases the GIL), best of 2 — reported beside the 1-core value"},
         "e2e": {"value": value, "unit": "Gpts·lev/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -604,6 +646,12 @@ def run_single(args):
         cpu = {"value": units / min(times) / 1e9, "unit": "Gpts·lev/s", "cores": 1, "kind": kind,
                "sample": f"full {source}->{target} apply x{F} field(s), best of 2: {what}, numpy single-threaded "
                          "as the reference runs it"}
+        if R is not None:
+            t_thr, nthr, thr_ok = reference_threaded(R, w.nodes, w.weights, [h.array for h in hsrc], n, L, out)
+            cpu["threaded"] = {"value": units / t_thr / 1e9, "unit": "Gpts·lev/s", "cores": nthr,
+                               "bitwise_vs_1_core": thr_ok,
+                               "sample": f"the reference's own apply_remap on {nthr} target chunks from {nthr} "
+                                         "threads at once (numpy releases the GIL), best of 2"}
         parity = {"checked": True, "against": kind,
                   "device_bitwise_vs_cpu": bool(np.array_equal(device_out.view(np.uint64), out.view(np.uint64))),
                   "e2e_bitwise_vs_cpu": bool(np.array_equal(hdst[F - 1].array.view(np.uint64), out.view(np.uint64)))}
