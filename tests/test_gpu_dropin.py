@@ -269,3 +269,25 @@ def test_cli_remap_report(gpu, tmp_path):
     text = out.read_text()
     assert text.startswith("# field:")
     assert len([ln for ln in text.splitlines() if not ln.startswith("#")]) == 128
+
+
+def test_integration_dropin_snippet_runs(gpu):
+    """INTEGRATION.md's drop-in program (the reference pipeline's order, cli.py:119-154) runs as
+    written on this package — grid names shrunk to O32 -> O16 so it takes seconds; 8 ranks
+    on the test box's GPU."""
+    import os
+    import re
+
+    from conftest import ROOT
+
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    block = re.search(r"```python\n(.*?)```", text, re.S).group(1)
+    code = "\n".join(line[3:] if line.startswith("   ") else line for line in block.splitlines())
+    assert '"O1280"' in code and '"O640"' in code and "sg.run_ranks(8, program)" in code
+    code = code.replace('"O1280"', '"O32"').replace('"O640"', '"O16"')
+    code = code.replace("sg.apply_remap(w, f, tf)", "sg.apply_remap(w, f, tf)\n    return len(w), tf.host.shape")
+    code = code.replace("sg.run_ranks(8, program)", "RESULT = sg.run_ranks(8, program)")
+    ns = {}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    assert sum(r[0] for r in ns["RESULT"]) == sg.grid_from_name("O16").npts
+    assert all(r[1][1] == 137 for r in ns["RESULT"])
