@@ -727,11 +727,14 @@ def run_multi(args):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     ndev = sg._native.device_count()
     dev = local % max(ndev, 1)
-    if ndev < world and args.transport == "nccl":
-        raise SystemExit(f"{world} ranks on {ndev} GPU(s): NCCL needs one GPU per rank (use --transport ipc)")
     sg.set_device(dev)
     local = dev
     ctx = sg.DistContext(device=local, transport=args.transport)
+    # one GPU per rank? (device UUIDs, not the visible-device count: a launcher may give each
+    # process only its own GPU)
+    own_gpu = len(set(ctx.share(sg._native.device_uuid(local)))) == world
+    if not own_gpu and args.transport == "nccl":
+        raise SystemExit(f"{world} ranks share GPUs: NCCL needs one GPU per rank (use --transport ipc)")
     source, target, L, F, method = config(args.config)
     t0 = time.time()
     S, T, mesh, fs, tdist, w = setup_remap(sg, source, target, world, rank, ctx, method, args.partitioner)
@@ -748,8 +751,16 @@ def run_multi(args):
         dist.all_reduce(t, op=op)
         return t.tolist()
 
-    run = DistributedRemap(fs, w, ctx, f.device, tf.device, variant=args.variant, fused=args.fused)
     fallback, err = None, ""
+    try:  # a failed peer mapping raises on every rank together (DistContext._all_or_none)
+        run = DistributedRemap(fs, w, ctx, f.device, tf.device, variant=args.variant, fused=args.fused)
+    except sg.SpheregridError as exc:
+        if not own_gpu:
+            raise SystemExit(f"rank {rank}: peer memory unavailable and ranks share GPUs: {exc}")
+        fallback = f"peer memory unavailable ({exc}); NCCL exchange + apply used"
+        log(f"rank {rank}: {fallback}")
+        args.transport = ctx.transport = "nccl"
+        run = DistributedRemap(fs, w, ctx, f.device, tf.device, variant=args.variant, fused=False)
     try:
         run.step()
         run.synchronize()  # raises if a device-side wait of the fused step timed out
@@ -820,7 +831,12 @@ def run_multi(args):
         if transport == "nccl":
             return (lambda: plan.exchange_nccl(d, ctx.nccl_comm(), stream)), True, "nccl pack/send/recv/unpack"
         if transport == "nvlink":
-            x = _signalled_exchange(ctx, plan, d)
+            try:
+                x = _signalled_exchange(ctx, plan, d)
+            except sg.SpheregridError:  # raised on every rank together: peer memory unavailable
+                x = None
+                if own_gpu:
+                    return exchanger(plan, d, stream, "nccl")
             if x is not None:
                 return (lambda: x.launch(stream)), True, "signalled pull over NVLink, one kernel per rank"
         return (lambda: ctx.device_exchange(plan, d, stream)), False, "pull kernel between host barriers"
@@ -892,7 +908,7 @@ def run_multi(args):
               "against": "per rank: analytic field on every local row (owned + ghost) and the oracle apply "
                          "(interp.py:219-223) on the rank's own stencils"}
     comm = {"transport": args.transport, "transport_fallback": fallback, "exchange": hlabel}
-    if ndev >= world:
+    if own_gpu:
         info = ctx.comm_info()
         nr = allreduce([float(info["nranks"])], dist.ReduceOp.MIN)[0]
         comm.update({"nccl_nranks": int(nr), "nccl_version": info["nccl_version"],
@@ -919,7 +935,7 @@ def run_multi(args):
             tot = allreduce([rb], dist.ReduceOp.SUM)[0]
             entry = {"halo": h, "bytes_per_exchange": tot}
             # the transport of the run, then NCCL (the library baseline) when each rank has a GPU
-            transports = [args.transport] + (["nccl"] if args.transport != "nccl" and ndev >= world else [])
+            transports = [args.transport] + (["nccl"] if args.transport != "nccl" and own_gpu else [])
             for k, tr in enumerate(transports):
                 d.upload(init)
                 xrun, xtimed, xlabel = exchanger(plan, d, hs.stream, tr)

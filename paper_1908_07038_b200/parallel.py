@@ -445,13 +445,28 @@ class DistContext:
         h = (C.c_uint8 * 64)()
         N.call("sg_ipc_handle", dev_array.handle, N.ref(h), 64)
         everyone = self.share((bytes(h), dev_array.pitch, dev_array.device))
-        got = []
-        for r, (blob, pitch, dev) in enumerate(everyone):
-            if r == self.rank:
-                got.append((dev_array.ptr, dev_array.pitch, dev_array.device))
-            else:
-                got.append((self._ipc_map(self._ipc, r, blob, dev_array.device), pitch, dev))
-        return got
+
+        def mapped():
+            return [(dev_array.ptr, dev_array.pitch, dev_array.device) if r == self.rank else
+                    (self._ipc_map(self._ipc, r, blob, dev_array.device), pitch, dev)
+                    for r, (blob, pitch, dev) in enumerate(everyone)]
+
+        return self._all_or_none(mapped)
+
+    def _all_or_none(self, local_step):
+        """Run a rank-local step that may fail (opening CUDA-IPC mappings), then agree: if it
+        failed on ANY rank every rank raises the same error class, so no rank goes on to the
+        next collective while another has left (which would hang the job)."""
+        from .errors import SpheregridError
+
+        try:
+            out, err = local_step(), ""
+        except Exception as exc:  # noqa: BLE001 - reported collectively below
+            out, err = None, f"rank {self.rank}: {exc}"
+        errs = [e for e in self.share(err) if e]
+        if errs:
+            raise SpheregridError("CUDA-IPC mapping of peer memory failed (" + "; ".join(errs) + ")")
+        return out
 
     def peer_signals(self, signal) -> list:
         """(pointer to rank r's step signal words, mapped here through CUDA IPC, device uuid)
@@ -463,13 +478,9 @@ class DistContext:
         h = (C.c_uint8 * 64)()
         N.call("sg_signal_ipc_handle", signal.handle, N.ref(h), 64)
         everyone = self.share((bytes(h), N.device_uuid(signal.device)))
-        got = []
-        for r, (blob, uuid) in enumerate(everyone):
-            if r == self.rank:
-                got.append((signal.ptr, uuid))
-            else:
-                got.append((self._ipc_map(self._ipc_sig, r, blob, signal.device), uuid))
-        return got
+        return self._all_or_none(lambda: [
+            (signal.ptr, uuid) if r == self.rank else (self._ipc_map(self._ipc_sig, r, blob, signal.device), uuid)
+            for r, (blob, uuid) in enumerate(everyone)])
 
     def close_ipc(self) -> None:
         """Unmap every peer field and step signal opened through CUDA IPC (call when no kernel

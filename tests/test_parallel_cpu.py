@@ -278,3 +278,64 @@ def test_dist_context_keeps_every_peer_mapping_until_close(monkeypatch):
     assert calls.count("sg_ipc_open") == 4 and not closed  # nothing unmapped while in use
     ctx.close_ipc()
     assert sorted(closed) == sorted([a1, b1, a2, s1]) and not ctx._ipc and not ctx._ipc_sig
+
+
+def _gloo_ipc_fail_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    import paper_1908_07038_b200._native as N
+    import paper_1908_07038_b200.parallel as PAR
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ.setdefault("GLOO_SOCKET_IFNAME", "lo")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        def fake_call(name, *args):
+            if name == "sg_ipc_handle":
+                return None
+            raise AssertionError(name)
+
+        N.call = fake_call
+
+        def failing_map(cache, r, blob, device):
+            if rank == 1:
+                raise RuntimeError("cudaIpcOpenMemHandle: peer access unsupported")
+            return 0x1000 + r
+
+        PAR.DistContext._ipc_map = staticmethod(failing_map)
+        ctx = sg.DistContext(device=0)
+        arr = _FakeArray(0x5000 + rank, 1)
+        arr.pitch = 137
+        try:
+            ctx.peer_fields(arr)
+            outcome = "returned"
+        except sg.SpheregridError as exc:
+            outcome = "raised: " + str(exc)
+        after = ctx.share(rank)  # the next collective still lines up on both ranks
+        q.put((rank, outcome, after))
+        ctx.barrier()
+    except Exception as exc:  # noqa: BLE001 - reported to the test instead of a queue timeout
+        q.put((rank, "error: " + repr(exc), None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_mapping_failure_raises_on_every_rank():
+    """An IPC mapping that fails on ONE rank makes every rank raise (DistContext._all_or_none),
+    so no rank enters the next collective alone — the N>1 bench then falls back to NCCL
+    together instead of hanging."""
+    import torch.multiprocessing as mp
+
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_ipc_fail_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(o[1].startswith("raised") and "rank 1" in o[1] for o in out), out
+    assert all(o[2] == [0, 1] for o in out)
