@@ -395,14 +395,17 @@ def gather_field(fs, f: Field, ctx) -> Optional[np.ndarray]:
     D2H.  Device-current fields are read from their mirror, host ones through one staging
     upload.  Message counters as the reference: every other rank sends rank 0 one message of
     its gids and values."""
-    if not _device_path(fs):
+    single = ctx is None or ctx.nranks == 1
+    device_path = _device_path(fs)
+    if not single:  # collective decision: every rank takes the same path
+        device_path = all(ctx.share(bool(device_path)))
+    if not device_path:
         return _gather_host(fs, f, ctx)
     dev, _, n = _owned_device_rows(fs, f)
     L, dt = f.levels, f.host.dtype
     row_bytes = L * dt.itemsize
     gids = np.ascontiguousarray(fs.owned_global, np.int64)
     device = dev.device
-    single = ctx is None or ctx.nranks == 1
     peers = None if single else ctx.peer_fields(dev)  # collective: every rank's owned rows
     if not single:
         parts = ctx.gather_to_root(gids.tobytes())  # the reference's message: gids + values
@@ -461,9 +464,10 @@ def scatter_field(fs, f: Field, ctx, global_values: Optional[np.ndarray]) -> Non
     dt, L = f.host.dtype, f.levels
     same_dtype = not root or (isinstance(global_values, np.ndarray) and global_values.dtype == dt
                               and global_values.shape == (fs.global_size, L))
-    if not single:  # collective decision: the reference's byte-reinterpreting quirk stays on the host
-        same_dtype = all(ctx.share(bool(same_dtype)))
-    if not (_device_path(fs) and same_dtype):
+    device_path = _device_path(fs) and same_dtype
+    if not single:  # collective decision (the reference's byte-reinterpreting quirk stays on the host)
+        device_path = all(ctx.share(bool(device_path)))
+    if not device_path:
         return _scatter_host(fs, f, ctx, global_values)
     rows = fs.owned_row_index()
     n = len(rows)
